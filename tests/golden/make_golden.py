@@ -1,0 +1,186 @@
+"""Regenerate the golden fixtures by running the REFERENCE implementation.
+
+Run in the build container only (the reference is not on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every fixture is produced by importing ``cavityflow`` (the reference package)
+and calling its public API on seeded inputs; nothing here reimplements the
+algorithm.  The fixtures pin ``oracle/`` (tests/test_oracle.py) and, on the
+GPU, the CUDA path (tests/test_gpu_*.py).
+"""
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SRC = "/root/reference/pkg/src"
+if REF_SRC not in sys.path:
+    sys.path.insert(0, REF_SRC)
+
+import cavityflow as cf  # noqa: E402
+from cavityflow import sim  # noqa: E402
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrays)
+    print("wrote", path, sum(np.asarray(a).nbytes for a in arrays.values()), "bytes raw")
+
+
+def compliant_state(n, seed, scale):
+    cfg = sim.SimConfig(n=n, h=1.0 / n, dt=0.01, t_end=0.0)
+    st = sim.initial_state(cfg)
+    rng = np.random.default_rng(seed)
+    st.vel.u[:] = scale * rng.standard_normal(st.vel.u.shape)
+    st.vel.v[:] = scale * rng.standard_normal(st.vel.v.shape)
+    st.vel.w[:] = scale * rng.standard_normal(st.vel.w.shape)
+    sim.enforce_boundaries(st)
+    return st
+
+
+def sparse_fixtures():
+    out = {}
+    for n, h in ((5, 0.7), (16, 1.0 / 16)):
+        full = sim.poisson_full_csr(n, h)
+        sym = sim.poisson_symmetric(n, h)
+        x = np.random.default_rng(n).uniform(-1, 1, n ** 3)
+        out[f"n{n}_h"] = np.float64(h)
+        out[f"n{n}_row_ptr"] = full.row_ptr
+        out[f"n{n}_col_idx"] = full.col_idx
+        out[f"n{n}_values"] = full.values
+        out[f"n{n}_sym_row_ptr"] = sym.row_ptr
+        out[f"n{n}_sym_col_idx"] = sym.col_idx
+        out[f"n{n}_sym_values"] = sym.values
+        out[f"n{n}_x"] = x
+        out[f"n{n}_spmv"] = cf.spmv(full, x)
+        out[f"n{n}_spmv_sym"] = cf.spmv_sym(sym, x)
+        with cf.WorkerPool(3) as pool:
+            out[f"n{n}_dot_t3"] = np.float64(cf.dot(x, out[f"n{n}_spmv"], pool))
+        out[f"n{n}_dot_t1"] = np.float64(cf.dot(x, out[f"n{n}_spmv"]))
+        y = out[f"n{n}_spmv"].copy()
+        cf.multiply_add_inplace(y, 0.7391, x)
+        out[f"n{n}_maxpy"] = y
+        dic = cf.dic_from(full)
+        out[f"n{n}_dic_diag"] = dic.modified_diag
+        out[f"n{n}_dic_apply"] = dic.apply(x)
+    save("sparse.npz", **out)
+
+
+def pcg_fixtures():
+    out = {}
+    for n in (12, 32):
+        h = 1.0 / n
+        a_sym = sim.poisson_symmetric(n, h)
+        a_full = sim.poisson_full_csr(n, h)
+        b = np.random.default_rng(0).uniform(-1, 1, n ** 3)
+        b -= b.mean()
+        out[f"n{n}_b"] = b
+        for tag, a, pre, variant in (
+            ("jacobi_opt", a_sym, cf.jacobi_from(a_sym), "optimized"),
+            ("dic_base", a_full, cf.dic_from(a_full), "baseline"),
+            ("none_opt", a_sym, None, "optimized"),
+        ):
+            op = (lambda x, out=None, a=a: cf.spmv_sym(a, x, out=out)) if a is a_sym else \
+                (lambda x, out=None, a=a: cf.spmv(a, x, out=out))
+            x, st = cf.pcg(op, b, precond=pre, tol=1e-8, max_iter=20000, variant=variant)
+            out[f"n{n}_{tag}_x"] = x
+            out[f"n{n}_{tag}_it"] = np.int64(st.iterations)
+            out[f"n{n}_{tag}_res"] = np.float64(st.final_residual_rel)
+        # warm start from a perturbed guess
+        x0 = np.random.default_rng(1).uniform(-1, 1, n ** 3) * 1e-3
+        x, st = cf.pcg(lambda v, out=None: cf.spmv_sym(a_sym, v, out=out), b, x0=x0,
+                       precond=cf.jacobi_from(a_sym), tol=1e-8, max_iter=20000, variant="optimized")
+        out[f"n{n}_x0"] = x0
+        out[f"n{n}_warm_x"] = x
+        out[f"n{n}_warm_it"] = np.int64(st.iterations)
+    # config 2 (128^3, tol 1e-8): iteration counts and solution checksums only
+    n = 128
+    a_sym = sim.poisson_symmetric(n, 1.0 / n)
+    with cf.WorkerPool(os.cpu_count()) as pool:
+        for seed in (0, 1):
+            b = np.random.default_rng(seed).uniform(-1, 1, n ** 3)
+            b -= b.mean()
+            x, st = cf.pcg(lambda v, out=None: cf.spmv_sym(a_sym, v, out=out, pool=pool), b,
+                           precond=cf.jacobi_from(a_sym), tol=1e-8, max_iter=20000,
+                           variant="optimized", pool=pool)
+            out[f"c2_seed{seed}_it"] = np.int64(st.iterations)
+            out[f"c2_seed{seed}_res"] = np.float64(st.final_residual_rel)
+            out[f"c2_seed{seed}_xnorm"] = np.float64(np.linalg.norm(x))
+            out[f"c2_seed{seed}_xsum"] = np.float64(x.sum())
+            out[f"c2_seed{seed}_x_sample"] = x[:: 4099].copy()
+    save("pcg.npz", **out)
+
+
+def advection_fixtures():
+    out = {}
+    for n, dt, scale, seed in ((6, 0.3, 0.4, 11), (16, 0.01, 20.0, 12)):
+        st = compliant_state(n, seed, scale)
+        cfg = sim.SimConfig(n=n, h=1.0 / n, dt=dt, t_end=0.0)
+        new = sim.solve_advection(st, cfg)
+        for c, a in zip("uvw", st.vel.components()):
+            out[f"n{n}_in_{c}"] = a
+        for c, a in zip("uvw", new.components()):
+            out[f"n{n}_out_{c}"] = a
+        out[f"n{n}_dt"] = np.float64(dt)
+        out[f"n{n}_div"] = cf.divergence(st.vel).data
+        # pressure correction of the advected field with a seeded pressure
+        p = cf.ScalarField(st.vel.spec, np.random.default_rng(seed + 100).standard_normal(n ** 3))
+        st2 = sim.SimState(vel=new.copy(), p=p)
+        div_post = sim.apply_pressure_correction(st2, p, cfg)
+        out[f"n{n}_p"] = p.data
+        for c, a in zip("uvw", st2.vel.components()):
+            out[f"n{n}_corr_{c}"] = a
+        out[f"n{n}_div_post"] = np.float64(div_post)
+    save("advection.npz", **out)
+
+
+def cavity_fixtures():
+    out = {}
+    runs = {
+        # BASELINE config 1 geometry in reference physics (nu = 0, lid accel)
+        "c1_opt_jacobi": dict(n=16, h=1.0 / 16, dt=0.01, t_end=0.1, tol=1e-6, max_iter=10000,
+                              variant="optimized", preconditioner="jacobi"),
+        "c1_base_dic": dict(n=16, h=1.0 / 16, dt=0.01, t_end=0.1, tol=1e-6, max_iter=10000,
+                            variant="baseline", preconditioner="dic"),
+        "n8_warm": dict(n=8, dt=0.4, t_end=1.2, warm_start=True, variant="optimized",
+                        preconditioner="jacobi"),
+        # the reference golden-snapshot configuration (tests/data/make_reference.py)
+        "n8_golden": dict(n=8, dt=0.4, t_end=1.2, variant="baseline"),
+    }
+    for tag, kw in runs.items():
+        cfg = sim.SimConfig(output_dir=None, **kw)
+        state = sim.initial_state(cfg)
+        cache = sim.PoissonCache()
+        its, res, dpre, dpost = [], [], [], []
+        for s in range(cfg.num_steps):
+            st = sim.step(state, cfg, cache)
+            its.append(st.solve.iterations)
+            res.append(st.solve.final_residual_rel)
+            dpre.append(st.div_pre)
+            dpost.append(st.div_post)
+            if s == 0:
+                for c, a in zip("uvw", state.vel.components()):
+                    out[f"{tag}_step1_{c}"] = a.copy()
+                out[f"{tag}_step1_p"] = state.p.data.copy()
+        for c, a in zip("uvw", state.vel.components()):
+            out[f"{tag}_{c}"] = a
+        out[f"{tag}_p"] = state.p.data
+        out[f"{tag}_its"] = np.array(its, dtype=np.int64)
+        out[f"{tag}_res"] = np.array(res)
+        out[f"{tag}_div_pre"] = np.array(dpre)
+        out[f"{tag}_div_post"] = np.array(dpost)
+    # the reference's own committed golden snapshot, as read by its reader
+    snap = cf.read_snapshot("/root/reference/pkg/tests/data/reference_n8_step3.csv")
+    for c in "xyzuvwp":
+        out[f"ref_csv_{c}"] = snap.column(c)
+    save("cavity.npz", **out)
+
+
+if __name__ == "__main__":
+    sparse_fixtures()
+    advection_fixtures()
+    cavity_fixtures()
+    pcg_fixtures()
