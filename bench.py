@@ -1,0 +1,323 @@
+"""Benchmark of the cavity time-step hot path (BASELINE.json config 4).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 256]
+
+One bench "step" is one full time step of the 256^3 lid-driven cavity
+(h=1/256, dt=0.002, CG tol 1e-8, Jacobi PCG, optimized variant) in
+reference physics, continuing the simulation from rest.
+Inputs: the fields, resident in HBM; at 537 MB of velocity+pressure (and
+4 x 134 MB of CG vectors) every pass is far larger than the 126 MB L2, so
+no flush is needed between iterations.
+
+value   = CG iterations / second over the K timed steps (whole steps, so
+          advection/divergence/correction time is included), device-timed
+          with CUDA events between barrier+synchronize brackets, max over ranks.
+e2e     = the same metric through the public API with the state in pinned
+          HOST memory: H2D of u,v,w,p + step() + D2H of u,v,w,p every step.
+roofline: the fused CG iteration (dir + update kernels), algorithmic bytes
+          88*N per iteration / measured loop time per
+          iteration, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline: the oracle port (oracle/, the reference's algorithm in C with
+          the reference's WorkerPool chunking) on a bounded sample: 256^3
+          Jacobi PCG iterations with the symmetric SpMV, all host threads.
+--impl reference: that CPU path alone, as the driver's reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CG iterations/s and fused-iteration HBM GB/s (% of peak); sim steps/s at 256³"
+UNIT = "CG iterations/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- CPU baseline
+
+
+def cpu_baseline(n: int, iters: int, threads: int):
+    """Oracle PCG on a 256^3 Poisson system: CG iterations/s on host cores."""
+    import numpy as np
+
+    import oracle as orc
+
+    a = orc.poisson_sym(n, 1.0 / n)
+    b = np.random.default_rng(0).uniform(-1, 1, n ** 3)
+    pre = orc.jacobi_from(a)
+    op = lambda v, o: orc.spmv_sym(a, v, threads, o)  # noqa: E731
+    orc.pcg(op, b, precond=pre, tol=1e-8, max_iter=20000, variant="optimized", threads=threads, max_count=1)
+    t0 = time.perf_counter()
+    _, st = orc.pcg(op, b, precond=pre, tol=1e-8, max_iter=20000, variant="optimized", threads=threads,
+                    max_count=iters)
+    dt = time.perf_counter() - t0
+    return st.iterations / dt, dt, st.iterations
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle as orc
+
+    threads = os.cpu_count() or 1
+    n = args.n
+    a = orc.poisson_sym(n, 1.0 / n)
+    b = np.random.default_rng(0).uniform(-1, 1, n ** 3)
+    pre = orc.jacobi_from(a)
+    op = lambda v, o: orc.spmv_sym(a, v, threads, o)  # noqa: E731
+    per_step = args.ref_iters
+    for _ in range(args.warmup):
+        orc.pcg(op, b, precond=pre, tol=1e-8, max_iter=20000, threads=threads, max_count=per_step)
+    t0 = time.perf_counter()
+    total = 0
+    for _ in range(args.steps):
+        _, st = orc.pcg(op, b, precond=pre, tol=1e-8, max_iter=20000, threads=threads, max_count=per_step)
+        total += st.iterations
+    dt = time.perf_counter() - t0
+    value = total / dt
+    sample = (f"{n}^3 Poisson Jacobi-PCG (symmetric CSR SpMV, reference chunking), {per_step} iterations "
+              f"per step, oracle port in C/OpenMP")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cavity-{n}^3 pressure solve (CPU sample)", "n": n, "tol": 1e-8},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+
+
+def load_traffic():
+    """Per-iteration DRAM bytes of the fused CG kernels from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_cg_r01.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_iteration")
+    except Exception:
+        return None
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_03697_b200 as cf
+
+    torch.cuda.set_device(local_rank)
+    cf.load_library()
+    n = args.n
+    cfg = cf.SimConfig(n=n, h=1.0 / n, dt=args.dt, t_end=args.dt * (args.warmup + 2 * args.steps), tol=1e-8,
+                       max_iter=20000, variant="optimized", preconditioner="jacobi")
+    state = cf.initial_state(cfg)
+    cache = cf.PoissonCache()
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        cf.step(state, cfg, cache)
+    ws = cache.operator(cfg)._cg_ws
+
+    # ---- device-resident timed region
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    its, loop_ms, launches = [], 0.0, 0
+    with ClockSampler(local_rank) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            s = cf.step(state, cfg, cache)
+            its.append(s.solve.iterations)
+            loop_ms += ws.last_loop_ms
+            # forces, advect, divergence, cg-init, correct + 2 kernels per iteration,
+            # the while body is unrolled by two (an odd count adds 2 early-exit launches)
+            launches += 5 + 4 * ((s.solve.iterations + 1) // 2)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms, float(sum(its))], device="cuda", dtype=torch.float64)
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ms_max, total_its = float(mx[0]), float(t[1])
+    else:
+        ms_max, total_its = ms, float(sum(its))
+    value = total_its / (ms_max / 1e3)
+
+    # ---- end to end through the public API with host-resident state
+    phys = [*state.vel._phys, state.p.data]
+    pinned = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in phys]
+    for h_, d_ in zip(pinned, phys):
+        h_.copy_(d_)
+    h2d = sum(t.numel() * t.element_size() for t in phys)
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_its = 0
+    e2.record(stream)
+    for _ in range(args.steps):
+        for h_, d_ in zip(pinned, phys):
+            d_.copy_(h_, non_blocking=True)
+        s = cf.step(state, cfg, cache)
+        e2e_its += s.solve.iterations
+        phys = [*state.vel._phys, state.p.data]
+        for h_, d_ in zip(pinned, phys):
+            h_.copy_(d_, non_blocking=True)
+    e3.record(stream)
+    barrier()
+    e2e_ms = e2.elapsed_time(e3)
+    e2e_value = e2e_its * (world if world > 1 else 1) / (e2e_ms / 1e3)
+
+    if rank != 0:
+        return 0
+    peak, peak_kind = peaks()
+    cells = n ** 3
+    alg_bytes = 88 * cells
+    iter_s = (loop_ms / 1e3) / max(sum(its), 1)
+    achieved = alg_bytes / iter_s / 1e9
+    traffic = load_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"lid-driven cavity {n}^3 (BASELINE config 4), one time step per bench step",
+                   "n": n, "h": 1.0 / n, "dt": args.dt, "tol": 1e-8, "preconditioner": "jacobi",
+                   "variant": "optimized", "physics": "reference (lid acceleration, inviscid)",
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (no flush needed)"},
+        "sim_steps_per_s": args.steps / (ms_max / 1e3),
+        "cg_iterations": its,
+        "fused_iter_us": iter_s * 1e6,
+        "fused_iter_gbs": achieved,
+        "fused_iter_frac": achieved / peak,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "fused CG iteration (cg_dir_kernel + cg_update_kernel)",
+                     "algorithmic_bytes_per_iteration": alg_bytes, "design_bytes_per_iteration": 64 * cells,
+                     "peak_kind": peak_kind},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, dt, k = cpu_baseline(n, args.cpu_iters, threads)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"{n}^3 Jacobi-PCG, {k} iterations ({dt:.1f} s), oracle port"}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--dt", type=float, default=0.002)
+    ap.add_argument("--cpu-iters", type=int, default=40)
+    ap.add_argument("--ref-iters", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,572 @@
+// cf_cg.cu -- fused, device-resident conjugate gradient for the pressure
+// system (src/solver.py:33-171 with the matrix-free operator of
+// src/sim.py:296-333).
+//
+// Per iteration the reference does 1 SpMV, 3 dots, 3 axpys and a
+// preconditioner apply with 3 host syncs -- 88 B/cell of
+// HBM traffic at best.  Here an iteration is two kernels and no host sync:
+//
+//   dir:    p_k = z_k + beta*p_{k-1}  (z = M^-1 r formed on the fly from r,
+//           so p is built tile-by-tile with its halo) then A p_k by the
+//           z-march stencil, partial p.Ap; the last block forms alpha.
+//           HBM: read r, p_{k-1}; write p_k                    = 24 B/cell
+//   update: A p_k recomputed from p_k (cheaper than storing Ap: 8 B vs 16 B),
+//           x += alpha p, r -= alpha Ap, partials r.r and r.z; the last block
+//           checks sqrt(r.r)/|b| <= tol, forms beta.
+//           HBM: read p, r, x; write r, x                       = 40 B/cell
+//
+// 64 B/cell instead of 88, with every per-element operation identical to
+// the reference's (same rounding, -fmad=false); only the dot-product
+// summation order differs (a fixed two-level tree, deterministic).
+// The iteration loop is a CUDA graph with a conditional WHILE node whose
+// condition is cleared on the device when the solve stops.
+#include <mutex>
+#include <vector>
+
+#include "cf_dic.cuh"
+#include "cf_stencil.cuh"
+
+namespace cf {
+
+enum PrecKind { PK_NONE = 0, PK_JCONST = 1, PK_JVEC = 2, PK_ZVEC = 3 };
+
+struct CgScalars {
+    double rz, alpha, beta, pap, rr, norm_b, res, tol;
+    long long it, max_iter;
+    int done, status;  // status: 0 running, 1 converged, 2 max_iter, 3 breakdown
+};
+
+enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_BREAKDOWN = 3 };
+
+struct CgTickets {
+    unsigned int init, dir, upd, pad;
+};
+
+template <int PK>
+__device__ __forceinline__ double zval(double r, const double *__restrict__ jd, long long i, double zc)
+{
+    // z = M^-1 r: src/solver.py:71-76 (none) and src/precond.py:94 (Jacobi)
+    if (PK == PK_NONE) return r;
+    if (PK == PK_JCONST) return r * zc;
+    return r * __ldg(jd + i);
+}
+
+// ---------------------------------------------------------------- init
+// r = b, x = 0, |b|^2 and r.z (src/solver.py:60-61, :130-143).
+template <int PK>
+__global__ void __launch_bounds__(kMarchThreads) cg_init_flat(long long n, const double *__restrict__ b,
+                                                              double *__restrict__ r, double *__restrict__ x,
+                                                              const double *__restrict__ jd, double zc,
+                                                              CgScalars *sc, double *partials,
+                                                              CgTickets *tk)
+{
+    __shared__ double red[32];
+    __shared__ int is_last;
+    double bb = 0.0, rz = 0.0;
+    const long long stride = (long long)gridDim.x * kMarchThreads;
+    for (long long i = (long long)blockIdx.x * kMarchThreads + threadIdx.x; i < n; i += stride) {
+        const double bi = b[i];
+        r[i] = bi;
+        x[i] = 0.0;
+        bb = bb + bi * bi;
+        rz = rz + bi * zval<PK>(bi, jd, i, zc);
+    }
+    bb = block_sum<kMarchThreads>(bb, red);
+    rz = block_sum<kMarchThreads>(rz, red);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = bb;
+        partials[2 * blockIdx.x + 1] = rz;
+    }
+    if (last_block(&tk->init, &is_last)) {
+        bb = reduce_partials<kMarchThreads>(partials, gridDim.x, 2, red);
+        rz = reduce_partials<kMarchThreads>(partials + 1, gridDim.x, 2, red);
+        if (threadIdx.x == 0) {
+            sc->norm_b = sqrt(bb);
+            sc->rz = rz;
+            sc->beta = 0.0;
+            sc->it = 0;
+            sc->res = INFINITY;
+            if (sc->norm_b == 0.0) {  // src/solver.py:62-64
+                sc->done = 1;
+                sc->status = ST_CONVERGED;
+                sc->res = 0.0;
+            }
+        }
+    }
+}
+
+// r = b - A x0, x = x0 (src/solver.py:134-139).
+template <int ORDER, int PK>
+__global__ void __launch_bounds__(kMarchThreads) cg_init_x0(Box bx, double off, double diag,
+                                                            const double *__restrict__ b,
+                                                            const double *__restrict__ x0,
+                                                            double *__restrict__ r, double *__restrict__ x,
+                                                            const double *__restrict__ jd, double zc,
+                                                            CgScalars *sc, double *partials,
+                                                            CgTickets *tk)
+{
+    __shared__ double red[32];
+    __shared__ int is_last;
+    double bb = 0.0, rz = 0.0;
+    auto load = [&](long long i) { return __ldg(x0 + i); };
+    auto epi = [&](long long i, double c, double ax) {
+        const double bi = b[i];
+        const double rn = bi + -1.0 * ax;
+        r[i] = rn;
+        x[i] = c;
+        bb = bb + bi * bi;
+        rz = rz + rn * zval<PK>(rn, jd, i, zc);
+    };
+    march<ORDER>(bx, off, diag, load, epi);
+    bb = block_sum<kMarchThreads>(bb, red);
+    rz = block_sum<kMarchThreads>(rz, red);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = bb;
+        partials[2 * blockIdx.x + 1] = rz;
+    }
+    if (last_block(&tk->init, &is_last)) {
+        bb = reduce_partials<kMarchThreads>(partials, gridDim.x, 2, red);
+        rz = reduce_partials<kMarchThreads>(partials + 1, gridDim.x, 2, red);
+        if (threadIdx.x == 0) {
+            sc->norm_b = sqrt(bb);
+            sc->rz = rz;
+            sc->beta = 0.0;
+            sc->it = 0;
+            sc->res = INFINITY;
+            if (sc->norm_b == 0.0) {
+                sc->done = 1;
+                sc->status = ST_CONVERGED;
+                sc->res = 0.0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- direction
+template <int ORDER, int PK>
+__global__ void __launch_bounds__(kMarchThreads) cg_dir_kernel(Box bx, double off, double diag,
+                                                               const double *__restrict__ r,
+                                                               const double *__restrict__ jd,
+                                                               const double *__restrict__ zbuf,
+                                                               const double *__restrict__ p_old,
+                                                               double *__restrict__ p_new, double zc,
+                                                               CgScalars *sc, double *partials,
+                                                               CgTickets *tk)
+{
+    __shared__ double red[32];
+    __shared__ int is_last;
+    if (sc->done) return;
+    const bool first = sc->it == 0;
+    const double beta = sc->beta;
+    double pap = 0.0;
+    // p = z + beta*p_old (src/solver.py:167-170); the first direction is z
+    // itself (:142).
+    auto load = [&](long long i) {
+        const double z = PK == PK_ZVEC ? __ldg(zbuf + i) : zval<PK>(__ldg(r + i), jd, i, zc);
+        return first ? z : z + beta * __ldg(p_old + i);
+    };
+    auto epi = [&](long long i, double c, double ax) {
+        p_new[i] = c;
+        pap = pap + c * ax;
+    };
+    march<ORDER>(bx, off, diag, load, epi);
+    pap = block_sum<kMarchThreads>(pap, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = pap;
+    if (last_block(&tk->dir, &is_last)) {
+        pap = reduce_partials<kMarchThreads>(partials, gridDim.x, 1, red);
+        if (threadIdx.x == 0) {
+            sc->pap = pap;
+            if (pap <= 0.0) {  // src/solver.py:151-152
+                sc->status = ST_BREAKDOWN;
+                sc->done = 1;
+            } else {
+                sc->alpha = sc->rz / pap;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- update
+template <int ORDER, int PK>
+__global__ void __launch_bounds__(kMarchThreads) cg_update_kernel(Box bx, double off, double diag,
+                                                                  const double *__restrict__ p,
+                                                                  double *__restrict__ r,
+                                                                  double *__restrict__ x,
+                                                                  const double *__restrict__ jd,
+                                                                  double zc, CgScalars *sc,
+                                                                  double *partials, CgTickets *tk,
+                                                                  int use_cond,
+                                                                  cudaGraphConditionalHandle cond)
+{
+    __shared__ double red[32];
+    __shared__ int is_last;
+    if (sc->done) {
+        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    const double alpha = sc->alpha, malpha = -alpha;
+    double rr = 0.0, rz = 0.0;
+    auto load = [&](long long i) { return __ldg(p + i); };
+    auto epi = [&](long long i, double c, double ax) {
+        x[i] = x[i] + alpha * c;             // src/solver.py:155
+        const double rn = r[i] + malpha * ax;  // :157
+        r[i] = rn;
+        rr = rr + rn * rn;                     // :159
+        if (PK != PK_ZVEC) rz = rz + rn * zval<PK>(rn, jd, i, zc);  // :163-164
+    };
+    march<ORDER>(bx, off, diag, load, epi);
+    rr = block_sum<kMarchThreads>(rr, red);
+    if (PK != PK_ZVEC) rz = block_sum<kMarchThreads>(rz, red);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = rr;
+        partials[2 * blockIdx.x + 1] = rz;
+    }
+    if (last_block(&tk->upd, &is_last)) {
+        rr = reduce_partials<kMarchThreads>(partials, gridDim.x, 2, red);
+        if (PK != PK_ZVEC) rz = reduce_partials<kMarchThreads>(partials + 1, gridDim.x, 2, red);
+        if (threadIdx.x == 0) {
+            sc->rr = rr;
+            sc->it += 1;
+            sc->res = sqrt(rr) / sc->norm_b;
+            if (sc->res <= sc->tol) {  // :160-162
+                sc->status = ST_CONVERGED;
+                sc->done = 1;
+            } else if (sc->it >= sc->max_iter) {  // :147
+                sc->status = ST_MAXITER;
+                sc->done = 1;
+            } else if (PK != PK_ZVEC) {
+                sc->beta = rz / sc->rz;  // :165-166
+                sc->rz = rz;
+            }
+            if (sc->done && use_cond) cudaGraphSetConditional(cond, 0);
+        }
+    }
+}
+
+// r.z after a DIC apply (src/solver.py:143 for mode 0, :164-166 for mode 1).
+__global__ void __launch_bounds__(kMarchThreads) cg_rz_kernel(long long n, const double *__restrict__ r,
+                                                              const double *__restrict__ z, CgScalars *sc,
+                                                              double *partials, CgTickets *tk, int mode)
+{
+    __shared__ double red[32];
+    __shared__ int is_last;
+    if (sc->done) return;
+    double rz = 0.0;
+    const long long stride = (long long)gridDim.x * kMarchThreads;
+    for (long long i = (long long)blockIdx.x * kMarchThreads + threadIdx.x; i < n; i += stride)
+        rz = rz + r[i] * z[i];
+    rz = block_sum<kMarchThreads>(rz, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = rz;
+    if (last_block(&tk->pad, &is_last)) {
+        rz = reduce_partials<kMarchThreads>(partials, gridDim.x, 1, red);
+        if (threadIdx.x == 0) {
+            if (mode == 1) sc->beta = rz / sc->rz;
+            sc->rz = rz;
+        }
+    }
+}
+
+}  // namespace cf
+
+// ---------------------------------------------------------------- workspace
+struct cf_cg {
+    cf::Box bx;
+    double h, off, diag;
+    int order;
+    long long n;
+    double *r = nullptr, *x = nullptr, *p[2] = {nullptr, nullptr}, *jd = nullptr;
+    double *partials = nullptr;
+    cf::CgScalars *sc = nullptr;
+    cf::CgScalars *sc_host = nullptr;
+    cf::CgTickets *tk = nullptr;
+    int grid_init = 1, grid_init_x0 = 1, grid_dir = 1, grid_upd = 1;
+    // DIC (CF_PRECOND_DIC): level-scheduled factor attached by cf_cg_set_dic
+    bool has_dic = false;
+    cf::DicData dic;
+    double *zbuf = nullptr, *wbuf = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    float last_loop_ms = 0.f;
+    // one instantiated while-graph per (preconditioner kind)
+    cudaGraphExec_t exec[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaGraph_t graph[4] = {nullptr, nullptr, nullptr, nullptr};
+    double zc_graph[4] = {0, 0, 0, 0};
+    std::mutex mu;
+};
+
+namespace cf {
+
+template <int ORDER, int PK>
+static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond)
+{
+    for (int half = 0; half < 2; ++half) {
+        const double *p_old = ws->p[half];
+        double *p_new = ws->p[half ^ 1];
+        cg_dir_kernel<ORDER, PK><<<ws->grid_dir, kMarchThreads, 0, s>>>(
+            ws->bx, ws->off, ws->diag, ws->r, ws->jd, ws->zbuf, p_old, p_new, zc, ws->sc, ws->partials,
+            ws->tk);
+        CF_CHECK_LAUNCH("cg_dir_kernel");
+        cg_update_kernel<ORDER, PK><<<ws->grid_upd, kMarchThreads, 0, s>>>(
+            ws->bx, ws->off, ws->diag, p_new, ws->r, ws->x, ws->jd, zc, ws->sc, ws->partials, ws->tk, 1,
+            cond);
+        CF_CHECK_LAUNCH("cg_update_kernel");
+        if (PK == PK_ZVEC) {
+            // z = M^-1 r by the level sweeps, then r.z and beta (src/solver.py:163-166)
+            int rc = dic_apply_launch(ws->dic, ws->r, ws->wbuf, ws->zbuf, &ws->sc->done, s);
+            if (rc != CF_OK) return rc;
+            cg_rz_kernel<<<ws->grid_init, kMarchThreads, 0, s>>>(ws->n, ws->r, ws->zbuf, ws->sc, ws->partials,
+                                                                 ws->tk, 1);
+            CF_CHECK_LAUNCH("cg_rz_kernel");
+        }
+    }
+    return CF_OK;
+}
+
+template <int ORDER, int PK>
+static int build_graph(cf_cg *ws, cudaStream_t s, double zc)
+{
+    cudaGraph_t g;
+    CF_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle cond;
+    CF_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CF_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    // capture the body on a private stream (capture-to-graph)
+    cudaStream_t cs;
+    CF_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CF_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    int rc = capture_body<ORDER, PK>(ws, cs, zc, cond);
+    cudaGraph_t captured;
+    cudaError_t e = cudaStreamEndCapture(cs, &captured);
+    cudaStreamDestroy(cs);
+    if (rc != CF_OK) return rc;
+    CF_CUDA(e);
+    cudaGraphExec_t exec;
+    CF_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    ws->graph[PK] = g;
+    ws->exec[PK] = exec;
+    ws->zc_graph[PK] = zc;
+    (void)s;
+    return CF_OK;
+}
+
+template <int ORDER, int PK>
+static int launch_init(cf_cg *ws, const double *b, const double *x0, double zc, cudaStream_t s)
+{
+    // for DIC the init pass computes r and |b| (its r.z is replaced below)
+    constexpr int IPK = PK == PK_ZVEC ? PK_NONE : PK;
+    if (x0) {
+        cg_init_x0<ORDER, IPK><<<ws->grid_init_x0, kMarchThreads, 0, s>>>(
+            ws->bx, ws->off, ws->diag, b, x0, ws->r, ws->x, ws->jd, zc, ws->sc, ws->partials, ws->tk);
+    } else {
+        cg_init_flat<IPK><<<ws->grid_init, kMarchThreads, 0, s>>>(ws->n, b, ws->r, ws->x, ws->jd, zc,
+                                                                  ws->sc, ws->partials, ws->tk);
+    }
+    CF_CHECK_LAUNCH("cg_init");
+    if (PK == PK_ZVEC) {  // z = M^-1 r, rz = r.z (src/solver.py:141-143)
+        int rc = dic_apply_launch(ws->dic, ws->r, ws->wbuf, ws->zbuf, &ws->sc->done, s);
+        if (rc != CF_OK) return rc;
+        cg_rz_kernel<<<ws->grid_init, kMarchThreads, 0, s>>>(ws->n, ws->r, ws->zbuf, ws->sc, ws->partials, ws->tk,
+                                                             0);
+        CF_CHECK_LAUNCH("cg_rz_kernel");
+    }
+    return CF_OK;
+}
+
+template <int ORDER, int PK>
+static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, cudaStream_t s)
+{
+    int rc = launch_init<ORDER, PK>(ws, b, x0, zc, s);
+    if (rc != CF_OK) return rc;
+    if (!ws->exec[PK] || ws->zc_graph[PK] != zc) {
+        if (ws->exec[PK]) {
+            cudaGraphExecDestroy(ws->exec[PK]);
+            cudaGraphDestroy(ws->graph[PK]);
+            ws->exec[PK] = nullptr;
+        }
+        rc = build_graph<ORDER, PK>(ws, s, zc);
+        if (rc != CF_OK) return rc;
+    }
+    CF_CUDA(cudaEventRecord(ws->ev0, s));
+    CF_CUDA(cudaGraphLaunch(ws->exec[PK], s));
+    CF_CUDA(cudaEventRecord(ws->ev1, s));
+    return CF_OK;
+}
+
+template <int ORDER>
+static int solve_dispatch(cf_cg *ws, int pk, const double *b, const double *x0, double zc,
+                          cudaStream_t s)
+{
+    switch (pk) {
+    case PK_NONE: return solve_impl<ORDER, PK_NONE>(ws, b, x0, zc, s);
+    case PK_JCONST: return solve_impl<ORDER, PK_JCONST>(ws, b, x0, zc, s);
+    case PK_JVEC: return solve_impl<ORDER, PK_JVEC>(ws, b, x0, zc, s);
+    case PK_ZVEC: return solve_impl<ORDER, PK_ZVEC>(ws, b, x0, zc, s);
+    default: set_error("unsupported preconditioner kind"); return CF_EINVAL;
+    }
+}
+
+template <int ORDER>
+static void set_grids(cf_cg *ws)
+{
+    ws->grid_dir = march_grid((const void *)cg_dir_kernel<ORDER, PK_JCONST>, ws->bx);
+    ws->grid_upd = march_grid((const void *)cg_update_kernel<ORDER, PK_JCONST>, ws->bx);
+    ws->grid_init_x0 = march_grid((const void *)cg_init_x0<ORDER, PK_JCONST>, ws->bx);
+    long long want = (ws->n + kMarchThreads - 1) / kMarchThreads;
+    long long cap = (long long)num_sms() * blocks_per_sm((const void *)cg_init_flat<PK_JCONST>, kMarchThreads, 0);
+    ws->grid_init = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+}  // namespace cf
+
+extern "C" {
+
+int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void *stream)
+{
+    CF_REQUIRE(out && nx >= 1 && ny >= 1 && nz >= 1 && h > 0, "cf_cg_create: bad grid");
+    CF_REQUIRE(order == CF_ORDER_CSR || order == CF_ORDER_SYM, "cf_cg_create: bad order");
+    cf_cg *ws = new cf_cg();
+    ws->bx = cf::Box{nx, ny, nz, 0, 0};
+    ws->h = h;
+    ws->off = -1.0 / (h * h);
+    ws->diag = 6.0 / (h * h);
+    ws->order = order;
+    ws->n = (long long)nx * ny * nz;
+    if (order == CF_ORDER_CSR) cf::set_grids<CF_ORDER_CSR>(ws);
+    else cf::set_grids<CF_ORDER_SYM>(ws);
+    int maxg = ws->grid_dir > ws->grid_upd ? ws->grid_dir : ws->grid_upd;
+    if (ws->grid_init > maxg) maxg = ws->grid_init;
+    if (ws->grid_init_x0 > maxg) maxg = ws->grid_init_x0;
+    size_t vec = (size_t)ws->n * sizeof(double);
+    cudaError_t e = cudaSuccess;
+    for (double **b : {&ws->r, &ws->x, &ws->p[0], &ws->p[1]})
+        if (e == cudaSuccess) e = cudaMalloc(b, vec);
+    if (e == cudaSuccess) e = cudaMalloc(&ws->partials, sizeof(double) * 2 * (size_t)maxg);
+    if (e == cudaSuccess) e = cudaMalloc(&ws->sc, sizeof(cf::CgScalars));
+    if (e == cudaSuccess) e = cudaMalloc(&ws->tk, sizeof(cf::CgTickets));
+    if (e == cudaSuccess) e = cudaMemsetAsync(ws->tk, 0, sizeof(cf::CgTickets), cf::as_stream(stream));
+    if (e == cudaSuccess) e = cudaMallocHost(&ws->sc_host, sizeof(cf::CgScalars));
+    if (e == cudaSuccess) e = cudaEventCreate(&ws->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&ws->ev1);
+    if (e != cudaSuccess) {
+        int rc = cf::cuda_fail(e, "cf_cg_create");
+        cf_cg_destroy(ws);
+        return rc;
+    }
+    *out = ws;
+    return CF_OK;
+}
+
+int cf_cg_destroy(cf_cg *ws)
+{
+    if (!ws) return CF_OK;
+    for (int k = 0; k < 4; ++k) {
+        if (ws->exec[k]) cudaGraphExecDestroy(ws->exec[k]);
+        if (ws->graph[k]) cudaGraphDestroy(ws->graph[k]);
+    }
+    for (double *b : {ws->r, ws->x, ws->p[0], ws->p[1], ws->jd, ws->partials, ws->zbuf, ws->wbuf})
+        if (b) cudaFree(b);
+    if (ws->sc) cudaFree(ws->sc);
+    if (ws->tk) cudaFree(ws->tk);
+    if (ws->sc_host) cudaFreeHost(ws->sc_host);
+    if (ws->ev0) cudaEventDestroy(ws->ev0);
+    if (ws->ev1) cudaEventDestroy(ws->ev1);
+    delete ws;
+    return CF_OK;
+}
+
+int cf_cg_solve(cf_cg *ws, const double *b, double *x, const double *x0, double tol, int64_t max_iter,
+                int precond, const double *inv_diag, int64_t *iters_host, double *res_host, void *stream)
+{
+    CF_REQUIRE(ws && b && x, "cf_cg_solve: null argument");
+    CF_REQUIRE(tol > 0, "tol must be positive");
+    CF_REQUIRE(max_iter >= 1, "max_iter must be >= 1");
+    std::lock_guard<std::mutex> lk(ws->mu);
+    cudaStream_t s = cf::as_stream(stream);
+    int pk;
+    double zc = 0.0;
+    if (precond == CF_PRECOND_NONE) {
+        pk = cf::PK_NONE;
+    } else if (precond == CF_PRECOND_JACOBI) {
+        if (inv_diag == nullptr) {
+            pk = cf::PK_JCONST;
+            zc = 1.0 / ws->diag;  // jacobi_from: 1.0 / diag (src/precond.py:138)
+        } else {
+            pk = cf::PK_JVEC;
+            if (!ws->jd) CF_CUDA(cudaMalloc(&ws->jd, (size_t)ws->n * sizeof(double)));
+            CF_CUDA(cudaMemcpyAsync(ws->jd, inv_diag, (size_t)ws->n * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, s));
+        }
+    } else if (precond == CF_PRECOND_DIC) {
+        CF_REQUIRE(ws->has_dic, "cf_cg_solve: CF_PRECOND_DIC needs cf_cg_set_dic first");
+        pk = cf::PK_ZVEC;
+    } else {
+        cf::set_error("cf_cg_solve: preconditioner kind not supported by the fused path");
+        return CF_EINVAL;
+    }
+    cf::CgScalars *h = ws->sc_host;
+    *h = cf::CgScalars{};
+    h->tol = tol;
+    h->max_iter = max_iter;
+    CF_CUDA(cudaMemcpyAsync(ws->sc, h, sizeof(*h), cudaMemcpyHostToDevice, s));
+    int rc = ws->order == CF_ORDER_CSR ? cf::solve_dispatch<CF_ORDER_CSR>(ws, pk, b, x0, zc, s)
+                                       : cf::solve_dispatch<CF_ORDER_SYM>(ws, pk, b, x0, zc, s);
+    if (rc != CF_OK) return rc;
+    CF_CUDA(cudaMemcpyAsync(h, ws->sc, sizeof(*h), cudaMemcpyDeviceToHost, s));
+    CF_CUDA(cudaStreamSynchronize(s));
+    CF_CUDA(cudaEventElapsedTime(&ws->last_loop_ms, ws->ev0, ws->ev1));
+    if (h->norm_b == 0.0) {
+        CF_CUDA(cudaMemsetAsync(x, 0, (size_t)ws->n * sizeof(double), s));  // exact solution of A x = 0
+    } else {
+        CF_CUDA(cudaMemcpyAsync(x, ws->x, (size_t)ws->n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    if (iters_host) *iters_host = h->it;
+    if (res_host) *res_host = h->res;
+    if (h->status == cf::ST_BREAKDOWN) {
+        cf::set_error("p^T A p = " + std::to_string(h->pap) + " at iteration " +
+                      std::to_string(h->it + 1));
+        return CF_BREAKDOWN;
+    }
+    return h->status == cf::ST_CONVERGED ? CF_OK : CF_NOT_CONVERGED;
+}
+
+int cf_cg_set_dic(cf_cg *ws, const int32_t *lp, const int32_t *lc, const double *lv, const int32_t *up,
+                  const int32_t *uc, const double *uv, const double *d, const int32_t *level_rows,
+                  const int64_t *level_ptr_host, int nlevels)
+{
+    CF_REQUIRE(ws && lp && lc && lv && up && uc && uv && d && level_rows && level_ptr_host && nlevels >= 0,
+               "cf_cg_set_dic: null argument");
+    CF_REQUIRE(level_ptr_host[nlevels] == ws->n, "cf_cg_set_dic: level schedule does not cover the grid");
+    std::lock_guard<std::mutex> lk(ws->mu);
+    if (!ws->zbuf) CF_CUDA(cudaMalloc(&ws->zbuf, (size_t)ws->n * sizeof(double)));
+    if (!ws->wbuf) CF_CUDA(cudaMalloc(&ws->wbuf, (size_t)ws->n * sizeof(double)));
+    cf::DicData &dd = ws->dic;
+    dd.n = ws->n;
+    dd.lp = lp; dd.lc = lc; dd.lv = lv;
+    dd.up = up; dd.uc = uc; dd.uv = uv;
+    dd.d = d;
+    dd.rows = level_rows;
+    dd.level_ptr.assign(level_ptr_host, level_ptr_host + nlevels + 1);
+    ws->has_dic = true;
+    if (ws->exec[cf::PK_ZVEC]) {  // pointers changed: rebuild on the next solve
+        cudaGraphExecDestroy(ws->exec[cf::PK_ZVEC]);
+        cudaGraphDestroy(ws->graph[cf::PK_ZVEC]);
+        ws->exec[cf::PK_ZVEC] = nullptr;
+        ws->graph[cf::PK_ZVEC] = nullptr;
+    }
+    return CF_OK;
+}
+
+int cf_cg_last_loop_ms(cf_cg *ws, float *ms_host)
+{
+    CF_REQUIRE(ws && ms_host, "cf_cg_last_loop_ms: null argument");
+    *ms_host = ws->last_loop_ms;
+    return CF_OK;
+}
+
+}  // extern "C"

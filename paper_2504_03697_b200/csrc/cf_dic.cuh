@@ -1,0 +1,33 @@
+// cf_dic.cuh -- level-scheduled simplified-DIC preconditioner
+// (src/precond.py:24-54).  The reference's recurrence and sweeps are
+// sequential by row; a row only depends on rows of its strictly lower
+// (forward) or upper (backward) pattern, so rows are grouped into levels of
+// equal dependency depth (for the 7-point operator: hyperplanes i+j+k =
+// const, 3n-2 levels) and each level is one data-parallel launch.  Every row
+// performs the reference's operations in the reference's operand order, so
+// the factor and the applied preconditioner are bit-identical.
+#pragma once
+
+#include <vector>
+
+#include "cf_common.cuh"
+
+namespace cf {
+
+struct DicData {
+    long long n = 0;
+    const int32_t *lp = nullptr, *lc = nullptr;  // strict lower triangle (CSR)
+    const double *lv = nullptr;
+    const int32_t *up = nullptr, *uc = nullptr;  // strict upper triangle (CSR)
+    const double *uv = nullptr;
+    const double *d = nullptr;                   // modified diagonal
+    const int32_t *rows = nullptr;               // rows sorted by level
+    std::vector<long long> level_ptr;            // host: level l = rows[level_ptr[l]:level_ptr[l+1]]
+};
+
+// z = M^-1 r through w; if `done` is non-null every launch exits when *done
+// is set (used inside the CG graph once the solve has stopped).
+int dic_apply_launch(const DicData &dd, const double *r, double *w, double *z, const int *done,
+                     cudaStream_t s);
+
+}  // namespace cf

@@ -1,0 +1,347 @@
+// cf_step.cu -- the non-CG kernels of one cavity time step (src/sim.py:
+// 134-289, :352-449, src/grid.py:102-154), each the reference's per-element
+// arithmetic in the reference's order (-fmad=false), so results are
+// bit-identical to the reference.
+//
+// Velocity layout: component c has extents (na, nb, nc) = (n+[c==0],
+// n+[c==1], n+[c==2]) stored x-fastest with row pitch ld_c (padded to a
+// 32-double multiple by the host so every row starts 256-B aligned) and plane
+// pitch ld_c*nb.
+#include "cf_common.cuh"
+
+namespace cf {
+
+struct Comp {
+    const double *a;
+    int na, nb, nc, ld;
+    __device__ __forceinline__ double at(int i, int j, int k) const
+    {
+        return __ldg(a + (long long)i + (long long)ld * ((long long)j + (long long)nb * k));
+    }
+};
+
+__device__ __forceinline__ double clamp_hi(double a, double hi)
+{
+    if (a < 0.0) return 0.0;
+    if (a > hi) return hi;
+    return a;
+}
+
+__device__ __forceinline__ int base_index(double a, int na)
+{
+    int i0 = (int)a;
+    if (i0 > na - 2) i0 = na > 1 ? na - 2 : 0;
+    return i0;
+}
+
+// src/sim.py:156-190 (_tri): clamped trilinear interpolation at lattice
+// coordinates (a, b, c); blend order fixed.
+__device__ __forceinline__ double trilerp(const Comp &f, double a, double b, double c)
+{
+    a = clamp_hi(a, f.na - 1.0);
+    b = clamp_hi(b, f.nb - 1.0);
+    c = clamp_hi(c, f.nc - 1.0);
+    const int i0 = base_index(a, f.na), j0 = base_index(b, f.nb), k0 = base_index(c, f.nc);
+    const int i1 = min(i0 + 1, f.na - 1), j1 = min(j0 + 1, f.nb - 1), k1 = min(k0 + 1, f.nc - 1);
+    const double fa = a - (double)i0, fb = b - (double)j0, fc = c - (double)k0;
+    const double c00 = f.at(i0, j0, k0) * (1.0 - fa) + f.at(i1, j0, k0) * fa;
+    const double c10 = f.at(i0, j1, k0) * (1.0 - fa) + f.at(i1, j1, k0) * fa;
+    const double c01 = f.at(i0, j0, k1) * (1.0 - fa) + f.at(i1, j0, k1) * fa;
+    const double c11 = f.at(i0, j1, k1) * (1.0 - fa) + f.at(i1, j1, k1) * fa;
+    return (c00 * (1.0 - fb) + c10 * fb) * (1.0 - fc) + (c01 * (1.0 - fb) + c11 * fb) * fc;
+}
+
+struct Vel3 {
+    Comp c[3];
+};
+
+__host__ __device__ inline Comp make_comp(const double *a, int n, int comp, int ld)
+{
+    return Comp{a, n + (comp == 0), n + (comp == 1), n + (comp == 2), ld};
+}
+
+constexpr int kFaceThreads = 256;
+
+// src/sim.py:193-240 + :283-288.  blockIdx.y = component; a grid-stride
+// loop over the component's faces with i fastest (coalesced stores).
+__global__ void __launch_bounds__(kFaceThreads) advect_kernel(Vel3 in, double *nu, double *nv, double *nw,
+                                                              int n, double h, double dt, double length)
+{
+    const int comp = blockIdx.y;
+    const Comp me = in.c[comp];
+    double *out = comp == 0 ? nu : (comp == 1 ? nv : nw);
+    const long long total = (long long)me.na * me.nb * me.nc;
+    const long long stride = (long long)gridDim.x * kFaceThreads;
+    for (long long f = (long long)blockIdx.x * kFaceThreads + threadIdx.x; f < total; f += stride) {
+        const int i = (int)(f % me.na);
+        const long long rest = f / me.na;
+        const int j = (int)(rest % me.nb), k = (int)(rest / me.nb);
+        double *dst = out + (long long)i + (long long)me.ld * ((long long)j + (long long)me.nb * k);
+        const int wall = comp == 0 ? i : (comp == 1 ? j : k);
+        if (wall == 0 || wall == n) {  // wall-normal planes are zeroed (:283-288)
+            *dst = 0.0;
+            continue;
+        }
+        double x, y, z;
+        if (comp == 0) {
+            x = i * h; y = (j + 0.5) * h; z = (k + 0.5) * h;
+        } else if (comp == 1) {
+            x = (i + 0.5) * h; y = j * h; z = (k + 0.5) * h;
+        } else {
+            x = (i + 0.5) * h; y = (j + 0.5) * h; z = k * h;
+        }
+        const double su = trilerp(in.c[0], x / h, y / h - 0.5, z / h - 0.5);
+        const double sv = trilerp(in.c[1], x / h - 0.5, y / h, z / h - 0.5);
+        const double sw = trilerp(in.c[2], x / h - 0.5, y / h - 0.5, z / h);
+        const double xb = clamp_hi(x - dt * su, length);
+        const double yb = clamp_hi(y - dt * sv, length);
+        const double zb = clamp_hi(z - dt * sw, length);
+        double r;
+        if (comp == 0) r = trilerp(me, xb / h, yb / h - 0.5, zb / h - 0.5);
+        else if (comp == 1) r = trilerp(me, xb / h - 0.5, yb / h, zb / h - 0.5);
+        else r = trilerp(me, xb / h - 0.5, yb / h - 0.5, zb / h);
+        *dst = r;
+    }
+}
+
+// src/sim.py:134-149.  blockIdx.y selects the task: 0 = lid row
+// u[1:n, n-1, :] += lid_dv; 1..6 = the six wall-normal planes.
+__global__ void forces_bc_kernel(double *u, double *v, double *w, int n, int ldu, int ldv, int ldw,
+                                 double lid_dv, int apply_lid)
+{
+    const int task = blockIdx.y;
+    const long long m = (long long)(n + 1) * (n + 1);
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < m;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int a = (int)(t % (n + 1)), b = (int)(t / (n + 1));
+        if (task == 0) {
+            // a = i in [1, n-1], b = k in [0, n)
+            if (apply_lid && a >= 1 && a <= n - 1 && b < n) {
+                double *q = u + a + (long long)ldu * ((long long)(n - 1) + (long long)n * b);
+                *q = *q + lid_dv;
+            }
+        } else if (task <= 2) {  // u[0|n, j, k]: a = j, b = k
+            if (a < n && b < n) u[(task == 1 ? 0 : n) + (long long)ldu * (a + (long long)n * b)] = 0.0;
+        } else if (task <= 4) {  // v[i, 0|n, k]: a = i, b = k
+            if (a < n && b < n) v[a + (long long)ldv * ((task == 3 ? 0 : n) + (long long)(n + 1) * b)] = 0.0;
+        } else {  // w[i, j, 0|n]: a = i, b = j
+            if (a < n && b < n) w[a + (long long)ldw * (b + (long long)n * (task == 5 ? 0 : n))] = 0.0;
+        }
+    }
+}
+
+constexpr int kCellThreads = 256;
+
+// src/grid.py:145-154: ((((u1-u0)+v1)-v0)+w1)-w0, then /h, then * scale
+// (src/sim.py:360).  Partial max|out| per block.
+__global__ void __launch_bounds__(kCellThreads) divergence_kernel(Vel3 in, int n, double h, double scale,
+                                                                  int do_scale, double *out,
+                                                                  double *partials, unsigned int *ticket,
+                                                                  double *result)
+{
+    __shared__ double red[32];
+    __shared__ int is_last;
+    const long long total = (long long)n * n * n;
+    const long long stride = (long long)gridDim.x * kCellThreads;
+    double mx = 0.0;
+    for (long long c = (long long)blockIdx.x * kCellThreads + threadIdx.x; c < total; c += stride) {
+        const int i = (int)(c % n);
+        const long long rest = c / n;
+        const int j = (int)(rest % n), k = (int)(rest / n);
+        double t = in.c[0].at(i + 1, j, k) - in.c[0].at(i, j, k);
+        t = t + in.c[1].at(i, j + 1, k);
+        t = t - in.c[1].at(i, j, k);
+        t = t + in.c[2].at(i, j, k + 1);
+        t = t - in.c[2].at(i, j, k);
+        double d = t / h;
+        if (do_scale) d = scale * d;
+        out[c] = d;
+        mx = fmax(mx, fabs(d));
+    }
+    mx = block_max<kCellThreads>(mx, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = mx;
+    if (last_block(ticket, &is_last)) {
+        double v = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += kCellThreads) v = fmax(v, __ldcg(partials + b));
+        v = block_max<kCellThreads>(v, red);
+        if (threadIdx.x == 0) *result = v;
+    }
+}
+
+// src/sim.py:434-449.  One thread per cell: it recomputes the corrected
+// values of its six faces from the OLD field (reading p with a one-cell
+// halo, ghost p = 0 outside), takes the cell divergence of the corrected
+// faces for div_post, and writes the faces it owns (its three lower faces
+// and, on the high walls, the upper ones) to the output field with the
+// wall-normal faces clamped to zero.
+__global__ void __launch_bounds__(kCellThreads) correct_kernel(Vel3 in, double *nu, double *nv, double *nw,
+                                                               const double *__restrict__ p, int n,
+                                                               double h, double coef, double *partials,
+                                                               unsigned int *ticket, double *result)
+{
+    __shared__ double red[32];
+    __shared__ int is_last;
+    const long long total = (long long)n * n * n;
+    const long long stride = (long long)gridDim.x * kCellThreads;
+    const long long nn = (long long)n * n;
+    double mx = 0.0;
+    for (long long c = (long long)blockIdx.x * kCellThreads + threadIdx.x; c < total; c += stride) {
+        const int i = (int)(c % n);
+        const long long rest = c / n;
+        const int j = (int)(rest % n), k = (int)(rest / n);
+        const double pc = __ldg(p + c);
+        // lower face of each axis: interior -> coef*(p - p_prev); wall -> coef*p
+        // upper face: interior -> coef*(p_next - p); wall -> coef*(0.0 - p)
+        const double du0 = i > 0 ? pc - __ldg(p + c - 1) : pc;
+        const double du1 = i < n - 1 ? __ldg(p + c + 1) - pc : 0.0 - pc;
+        const double dv0 = j > 0 ? pc - __ldg(p + c - n) : pc;
+        const double dv1 = j < n - 1 ? __ldg(p + c + n) - pc : 0.0 - pc;
+        const double dw0 = k > 0 ? pc - __ldg(p + c - nn) : pc;
+        const double dw1 = k < n - 1 ? __ldg(p + c + nn) - pc : 0.0 - pc;
+        const double u0 = in.c[0].at(i, j, k) - coef * du0;
+        const double u1 = in.c[0].at(i + 1, j, k) - coef * du1;
+        const double v0 = in.c[1].at(i, j, k) - coef * dv0;
+        const double v1 = in.c[1].at(i, j + 1, k) - coef * dv1;
+        const double w0 = in.c[2].at(i, j, k) - coef * dw0;
+        const double w1 = in.c[2].at(i, j, k + 1) - coef * dw1;
+        double t = u1 - u0;
+        t = t + v1;
+        t = t - v0;
+        t = t + w1;
+        t = t - w0;
+        mx = fmax(mx, fabs(t / h));
+        const Comp &cu = in.c[0], &cv = in.c[1], &cw = in.c[2];
+        nu[(long long)i + (long long)cu.ld * (j + (long long)cu.nb * k)] = i == 0 ? 0.0 : u0;
+        nv[(long long)i + (long long)cv.ld * (j + (long long)cv.nb * k)] = j == 0 ? 0.0 : v0;
+        nw[(long long)i + (long long)cw.ld * (j + (long long)cw.nb * k)] = k == 0 ? 0.0 : w0;
+        if (i == n - 1) nu[(long long)n + (long long)cu.ld * (j + (long long)cu.nb * k)] = 0.0;
+        if (j == n - 1) nv[(long long)i + (long long)cv.ld * (n + (long long)cv.nb * k)] = 0.0;
+        if (k == n - 1) nw[(long long)i + (long long)cw.ld * (j + (long long)cw.nb * n)] = 0.0;
+    }
+    mx = block_max<kCellThreads>(mx, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = mx;
+    if (last_block(ticket, &is_last)) {
+        double v = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += kCellThreads) v = fmax(v, __ldcg(partials + b));
+        v = block_max<kCellThreads>(v, red);
+        if (threadIdx.x == 0) *result = v;
+    }
+}
+
+__global__ void sample_kernel(Vel3 in, double h, double px, double py, double pz, double *out)
+{
+    // src/grid.py:124-142 with the lattice offsets of :99
+    out[0] = trilerp(in.c[0], px / h - 0.0, py / h - 0.5, pz / h - 0.5);
+    out[1] = trilerp(in.c[1], px / h - 0.5, py / h - 0.0, pz / h - 0.5);
+    out[2] = trilerp(in.c[2], px / h - 0.5, py / h - 0.5, pz / h - 0.0);
+}
+
+static Vel3 make_vel(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw)
+{
+    return Vel3{{make_comp(u, n, 0, ldu), make_comp(v, n, 1, ldv), make_comp(w, n, 2, ldw)}};
+}
+
+static int grid_for(long long work, int threads, int per_sm)
+{
+    long long want = (work + threads - 1) / threads;
+    long long cap = (long long)num_sms() * per_sm;
+    return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+static bool pitches_ok(int n, int ldu, int ldv, int ldw) { return ldu >= n + 1 && ldv >= n && ldw >= n; }
+
+// One-shot max reduction through the shared scratch, result to host.
+template <class Launch>
+static int reduce_max_to_host(Launch launch, double *result_host, cudaStream_t s)
+{
+    double *scratch = scratch_partials();
+    double *slot = host_result_slot();
+    if (!scratch || !slot) { set_error("reduction scratch allocation failed"); return CF_ENOMEM; }
+    double *result = scratch + kScratchPartials;
+    unsigned int *ticket = reinterpret_cast<unsigned int *>(scratch + kScratchPartials + 1);
+    launch(scratch, ticket, result);
+    CF_CHECK_LAUNCH("reduction kernel");
+    if (result_host) {
+        CF_CUDA(cudaMemcpyAsync(slot, result, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CF_CUDA(cudaStreamSynchronize(s));
+        *result_host = *slot;
+    }
+    return CF_OK;
+}
+
+}  // namespace cf
+
+extern "C" {
+
+int cf_forces_bc(double *u, double *v, double *w, int n, int ldu, int ldv, int ldw, double lid_dv,
+                 int apply_lid, void *stream)
+{
+    CF_REQUIRE(n >= 1 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_forces_bc: bad grid/pitch");
+    long long m = (long long)(n + 1) * (n + 1);
+    dim3 grid((unsigned)((m + 255) / 256 < 1024 ? (m + 255) / 256 : 1024), 7);
+    cf::forces_bc_kernel<<<grid, 256, 0, cf::as_stream(stream)>>>(u, v, w, n, ldu, ldv, ldw, lid_dv,
+                                                                   apply_lid);
+    CF_CHECK_LAUNCH("forces_bc_kernel");
+    return CF_OK;
+}
+
+int cf_advect(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n,
+              int ldu, int ldv, int ldw, double h, double dt, void *stream)
+{
+    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_advect: bad grid/pitch");
+    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_advect: output aliases input");
+    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw);
+    long long faces = (long long)(n + 1) * n * n;
+    dim3 grid(cf::grid_for(faces, cf::kFaceThreads, 8), 3);
+    cf::advect_kernel<<<grid, cf::kFaceThreads, 0, cf::as_stream(stream)>>>(in, nu, nv, nw, n, h, dt, n * h);
+    CF_CHECK_LAUNCH("advect_kernel");
+    return CF_OK;
+}
+
+int cf_divergence(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw,
+                  double h, double scale, double *out, double *maxabs_host, void *stream)
+{
+    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_divergence: bad grid/pitch");
+    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw);
+    cudaStream_t s = cf::as_stream(stream);
+    int grid = cf::grid_for((long long)n * n * n, cf::kCellThreads, 8);
+    return cf::reduce_max_to_host(
+        [&](double *part, unsigned int *tk, double *res) {
+            cf::divergence_kernel<<<grid, cf::kCellThreads, 0, s>>>(in, n, h, scale, scale != 1.0, out, part,
+                                                                    tk, res);
+        },
+        maxabs_host, s);
+}
+
+int cf_pressure_correct(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
+                        const double *p, int n, int ldu, int ldv, int ldw, double h, double coef,
+                        double *div_post_host, void *stream)
+{
+    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_pressure_correct: bad grid/pitch");
+    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_pressure_correct: output aliases input");
+    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw);
+    cudaStream_t s = cf::as_stream(stream);
+    int grid = cf::grid_for((long long)n * n * n, cf::kCellThreads, 8);
+    return cf::reduce_max_to_host(
+        [&](double *part, unsigned int *tk, double *res) {
+            cf::correct_kernel<<<grid, cf::kCellThreads, 0, s>>>(in, nu, nv, nw, p, n, h, coef, part, tk, res);
+        },
+        div_post_host, s);
+}
+
+int cf_sample_velocity(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw,
+                       double h, double px, double py, double pz, double *out_host, void *stream)
+{
+    CF_REQUIRE(n >= 1 && h > 0 && out_host && cf::pitches_ok(n, ldu, ldv, ldw), "cf_sample_velocity: bad args");
+    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw);
+    cudaStream_t s = cf::as_stream(stream);
+    double *scratch = cf::scratch_partials();
+    if (!scratch) { cf::set_error("scratch allocation failed"); return CF_ENOMEM; }
+    cf::sample_kernel<<<1, 1, 0, s>>>(in, h, px, py, pz, scratch);
+    CF_CHECK_LAUNCH("sample_kernel");
+    CF_CUDA(cudaMemcpyAsync(out_host, scratch, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CF_CUDA(cudaStreamSynchronize(s));
+    return CF_OK;
+}
+
+}  // extern "C"
