@@ -25,6 +25,7 @@
 
 #include "cf_dic.cuh"
 #include "cf_stencil.cuh"
+#include "cf_tma_march.cuh"
 
 namespace cf {
 
@@ -266,6 +267,166 @@ __global__ void __launch_bounds__(kMarchThreads) cg_rz_kernel(long long n, const
     }
 }
 
+// ---------------------------------------------------------------- TMA-staged kernels
+// Same arithmetic as cg_dir_kernel / cg_update_kernel; operands arrive by
+// TMA into a 4-stage shared-memory ring (cf_tma_march.cuh).
+
+template <int PK>
+struct DirPolicy {
+    const CUtensorMap *mz, *mp;
+    double *sz, *sp;  // stage bases (kStages x kBoxStride each)
+    double zc, beta;
+    bool first;
+    int lo;  // plane offset of the tensor maps (lo halo)
+    double *p_new;
+    long long nx, plane;
+    double pap = 0.0;
+
+    __device__ void prefetch() const
+    {
+        prefetch_map(mz);
+        prefetch_map(mp);
+    }
+    __device__ void issue(int s, int bx0, int by0, int, int, int z, int, int, uint64_t *bar) const
+    {
+        mbar_expect_tx(bar, first ? kBoxBytes : 2 * kBoxBytes);
+        tma_load_3d(sz + s * kBoxStride, mz, bx0, by0, z + lo, bar);
+        if (!first) tma_load_3d(sp + s * kBoxStride, mp, bx0, by0, z + lo, bar);
+    }
+    __device__ __forceinline__ double value(int s, int o) const
+    {
+        const double rv = sz[s * kBoxStride + o];
+        const double z = PK == PK_JCONST ? rv * zc : rv;  // NONE and ZVEC stage z itself
+        return first ? z : z + beta * sp[s * kBoxStride + o];
+    }
+    __device__ __forceinline__ void epi(int, int, int, int i, int j, int z, double c, double ax)
+    {
+        p_new[i + nx * j + plane * z] = c;
+        pap = pap + c * ax;
+    }
+};
+
+template <int ORDER, int PK>
+__global__ void __launch_bounds__(kTThreads, 2) cg_dir_tma(const __grid_constant__ CUtensorMap mz,
+                                                           const __grid_constant__ CUtensorMap mp, TmaGeom g,
+                                                           double off, double diag, double *__restrict__ p_new,
+                                                           double zc, CgScalars *sc, double *partials, CgTickets *tk)
+{
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[kStages];
+    __shared__ double red[32];
+    __shared__ int is_last;
+    if (sc->done) return;
+    double *base = aligned_smem(smem_raw);
+    DirPolicy<PK> pol{&mz, &mp, base, base + kStages * kBoxStride, zc, sc->beta, sc->it == 0, g.lo_halo, p_new,
+                      g.nx, (long long)g.nx * g.ny};
+    staged_march<ORDER>(g, off, diag, pol, bars);
+    double pap = block_sum<kTThreads>(pol.pap, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = pap;
+    if (last_block(&tk->dir, &is_last)) {
+        pap = reduce_partials<kTThreads>(partials, gridDim.x, 1, red);
+        if (threadIdx.x == 0) {
+            sc->pap = pap;
+            if (pap <= 0.0) {
+                sc->status = ST_BREAKDOWN;
+                sc->done = 1;
+            } else {
+                sc->alpha = sc->rz / pap;
+            }
+        }
+    }
+}
+
+template <int PK>
+struct UpdPolicy {
+    const CUtensorMap *mp, *mr, *mx;
+    double *sp, *sr, *sx;
+    int lo;
+    double alpha, malpha, zc;
+    double *r, *x;
+    long long nx, plane;
+    double rr = 0.0, rz = 0.0;
+
+    __device__ void prefetch() const
+    {
+        prefetch_map(mp);
+        prefetch_map(mr);
+        prefetch_map(mx);
+    }
+    __device__ void issue(int s, int bx0, int by0, int x0, int y0, int z, int z0, int z1, uint64_t *bar) const
+    {
+        const bool own = z >= z0 && z < z1;  // r and x only for owned planes
+        mbar_expect_tx(bar, kBoxBytes + (own ? 2 * kIntBytes : 0));
+        tma_load_3d(sp + s * kBoxStride, mp, bx0, by0, z + lo, bar);
+        if (own) {
+            tma_load_3d(sr + s * kInt, mr, x0, y0, z + lo, bar);
+            tma_load_3d(sx + s * kInt, mx, x0, y0, z + lo, bar);
+        }
+    }
+    __device__ __forceinline__ double value(int s, int o) const { return sp[s * kBoxStride + o]; }
+    __device__ __forceinline__ void epi(int s, int tx, int ty, int i, int j, int z, double c, double ax)
+    {
+        const int k = ty * kTTX + tx;
+        const long long g = i + nx * j + plane * z;
+        x[g] = sx[s * kInt + k] + alpha * c;             // src/solver.py:155
+        const double rn = sr[s * kInt + k] + malpha * ax;  // :157
+        r[g] = rn;
+        rr = rr + rn * rn;
+        if (PK != PK_ZVEC) rz = rz + rn * zval<PK>(rn, nullptr, 0, zc);
+    }
+};
+
+template <int ORDER, int PK>
+__global__ void __launch_bounds__(kTThreads, 2) cg_update_tma(
+    const __grid_constant__ CUtensorMap mp, const __grid_constant__ CUtensorMap mr,
+    const __grid_constant__ CUtensorMap mx, TmaGeom g, double off, double diag, double *__restrict__ r,
+    double *__restrict__ x, double zc, CgScalars *sc, double *partials, CgTickets *tk, int use_cond,
+    cudaGraphConditionalHandle cond)
+{
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[kStages];
+    __shared__ double red[32];
+    __shared__ int is_last;
+    if (sc->done) {
+        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    double *base = aligned_smem(smem_raw);
+    const double alpha = sc->alpha;
+    UpdPolicy<PK> pol{&mp, &mr, &mx, base, base + kStages * kBoxStride, base + kStages * (kBoxStride + kInt),
+                      g.lo_halo, alpha, -alpha, zc, r, x, g.nx, (long long)g.nx * g.ny};
+    staged_march<ORDER>(g, off, diag, pol, bars);
+    double rr = block_sum<kTThreads>(pol.rr, red);
+    double rz = PK != PK_ZVEC ? block_sum<kTThreads>(pol.rz, red) : 0.0;
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = rr;
+        partials[2 * blockIdx.x + 1] = rz;
+    }
+    if (last_block(&tk->upd, &is_last)) {
+        rr = reduce_partials<kTThreads>(partials, gridDim.x, 2, red);
+        if (PK != PK_ZVEC) rz = reduce_partials<kTThreads>(partials + 1, gridDim.x, 2, red);
+        if (threadIdx.x == 0) {
+            sc->rr = rr;
+            sc->it += 1;
+            sc->res = sqrt(rr) / sc->norm_b;
+            if (sc->res <= sc->tol) {
+                sc->status = ST_CONVERGED;
+                sc->done = 1;
+            } else if (sc->it >= sc->max_iter) {
+                sc->status = ST_MAXITER;
+                sc->done = 1;
+            } else if (PK != PK_ZVEC) {
+                sc->beta = rz / sc->rz;
+                sc->rz = rz;
+            }
+            if (sc->done && use_cond) cudaGraphSetConditional(cond, 0);
+        }
+    }
+}
+
+constexpr size_t kDirSmem = 2 * kStages * kBoxStride * sizeof(double) + 128;
+constexpr size_t kUpdSmem = kStages * (kBoxStride + 2 * kInt) * sizeof(double) + 128;
+
 }  // namespace cf
 
 // ---------------------------------------------------------------- workspace
@@ -284,6 +445,13 @@ struct cf_cg {
     bool has_dic = false;
     cf::DicData dic;
     double *zbuf = nullptr, *wbuf = nullptr;
+    // CF_CG_DIRECT=<batch> in the environment: host-driven loop instead of
+    // the conditional graph (ncu cannot profile conditional-graph kernels)
+    int direct = 0, direct_batch = 8;
+    // TMA-staged kernels (even nx >= 32; CF_NO_TMA=1 forces the LDG march)
+    bool tma = false;
+    cf::TmaGeom geom_dir{}, geom_upd{};
+    CUtensorMap m_r{}, m_z{}, m_p[2]{}, m_ri{}, m_xi{};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_loop_ms = 0.f;
     // one instantiated while-graph per (preconditioner kind)
@@ -296,19 +464,31 @@ struct cf_cg {
 namespace cf {
 
 template <int ORDER, int PK>
-static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond)
+static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond, int use_cond = 1)
 {
     for (int half = 0; half < 2; ++half) {
         const double *p_old = ws->p[half];
         double *p_new = ws->p[half ^ 1];
+        if (PK != PK_JVEC && ws->tma) {
+            const TmaGeom &gd = ws->geom_dir, &gu = ws->geom_upd;
+            cg_dir_tma<ORDER, PK><<<gd.ntx * gd.nty * gd.nchunk, kTThreads, kDirSmem, s>>>(
+                PK == PK_ZVEC ? ws->m_z : ws->m_r, ws->m_p[half], gd, ws->off, ws->diag, p_new, zc, ws->sc,
+                ws->partials, ws->tk);
+            CF_CHECK_LAUNCH("cg_dir_tma");
+            cg_update_tma<ORDER, PK><<<gu.ntx * gu.nty * gu.nchunk, kTThreads, kUpdSmem, s>>>(
+                ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc,
+                ws->partials, ws->tk, use_cond, cond);
+            CF_CHECK_LAUNCH("cg_update_tma");
+        } else {
         cg_dir_kernel<ORDER, PK><<<ws->grid_dir, kMarchThreads, 0, s>>>(
             ws->bx, ws->off, ws->diag, ws->r, ws->jd, ws->zbuf, p_old, p_new, zc, ws->sc, ws->partials,
             ws->tk);
         CF_CHECK_LAUNCH("cg_dir_kernel");
         cg_update_kernel<ORDER, PK><<<ws->grid_upd, kMarchThreads, 0, s>>>(
-            ws->bx, ws->off, ws->diag, p_new, ws->r, ws->x, ws->jd, zc, ws->sc, ws->partials, ws->tk, 1,
+            ws->bx, ws->off, ws->diag, p_new, ws->r, ws->x, ws->jd, zc, ws->sc, ws->partials, ws->tk, use_cond,
             cond);
         CF_CHECK_LAUNCH("cg_update_kernel");
+        }
         if (PK == PK_ZVEC) {
             // z = M^-1 r by the level sweeps, then r.z and beta (src/solver.py:163-166)
             int rc = dic_apply_launch(ws->dic, ws->r, ws->wbuf, ws->zbuf, &ws->sc->done, s);
@@ -383,6 +563,23 @@ static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, c
 {
     int rc = launch_init<ORDER, PK>(ws, b, x0, zc, s);
     if (rc != CF_OK) return rc;
+    if (ws->direct) {
+        // Host-driven loop (profilers cannot see kernels inside conditional
+        // graphs; also the multi-rank path): batches of iterations, kernels
+        // early-exit on sc->done, one 4-byte poll per batch.
+        CF_CUDA(cudaEventRecord(ws->ev0, s));
+        for (;;) {
+            for (int b2 = 0; b2 < ws->direct_batch; ++b2) {
+                rc = capture_body<ORDER, PK>(ws, s, zc, 0, 0);
+                if (rc != CF_OK) return rc;
+            }
+            CF_CUDA(cudaMemcpyAsync(&ws->sc_host->done, &ws->sc->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CF_CUDA(cudaStreamSynchronize(s));
+            if (ws->sc_host->done) break;
+        }
+        CF_CUDA(cudaEventRecord(ws->ev1, s));
+        return CF_OK;
+    }
     if (!ws->exec[PK] || ws->zc_graph[PK] != zc) {
         if (ws->exec[PK]) {
             cudaGraphExecDestroy(ws->exec[PK]);
@@ -420,6 +617,32 @@ static void set_grids(cf_cg *ws)
     long long want = (ws->n + kMarchThreads - 1) / kMarchThreads;
     long long cap = (long long)num_sms() * blocks_per_sm((const void *)cg_init_flat<PK_JCONST>, kMarchThreads, 0);
     ws->grid_init = (int)(want < cap ? (want > 0 ? want : 1) : cap);
+    const char *no_tma = getenv("CF_NO_TMA");
+    ws->tma = ws->bx.nx >= 32 && ws->bx.nx % 2 == 0 && !(no_tma && atoi(no_tma) > 0);
+    if (ws->tma) {
+        int bd = 0, bu = 0;
+        // every instantiation the workspace may launch needs the dynamic smem opt-in
+        cudaFuncSetAttribute(cg_dir_tma<ORDER, PK_NONE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDirSmem);
+        cudaFuncSetAttribute(cg_dir_tma<ORDER, PK_JCONST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDirSmem);
+        cudaFuncSetAttribute(cg_dir_tma<ORDER, PK_ZVEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDirSmem);
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_NONE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem);
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_JCONST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kUpdSmem);
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_ZVEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bd, cg_dir_tma<ORDER, PK_JCONST>, kTThreads, kDirSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, cg_update_tma<ORDER, PK_JCONST>, kTThreads, kUpdSmem);
+        ws->geom_dir = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bd > 0 ? bd : 1);
+        ws->geom_upd = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bu > 0 ? bu : 1);
+    }
+}
+
+static bool build_maps(cf_cg *ws)
+{
+    const int nx = ws->bx.nx, ny = ws->bx.ny, nz = ws->bx.nz;
+    bool ok = make_map(&ws->m_r, ws->r, nx, ny, nz, kHX, kHY) && make_map(&ws->m_p[0], ws->p[0], nx, ny, nz, kHX, kHY) &&
+              make_map(&ws->m_p[1], ws->p[1], nx, ny, nz, kHX, kHY) &&
+              make_map(&ws->m_ri, ws->r, nx, ny, nz, kTTX, kTTY) && make_map(&ws->m_xi, ws->x, nx, ny, nz, kTTX, kTTY);
+    return ok;
 }
 
 }  // namespace cf
@@ -437,11 +660,24 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
     ws->diag = 6.0 / (h * h);
     ws->order = order;
     ws->n = (long long)nx * ny * nz;
+    if (const char *d = getenv("CF_CG_DIRECT")) {
+        int b = atoi(d);
+        if (b > 0) {
+            ws->direct = 1;
+            ws->direct_batch = b;
+        }
+    }
     if (order == CF_ORDER_CSR) cf::set_grids<CF_ORDER_CSR>(ws);
     else cf::set_grids<CF_ORDER_SYM>(ws);
     int maxg = ws->grid_dir > ws->grid_upd ? ws->grid_dir : ws->grid_upd;
     if (ws->grid_init > maxg) maxg = ws->grid_init;
     if (ws->grid_init_x0 > maxg) maxg = ws->grid_init_x0;
+    if (ws->tma) {
+        const cf::TmaGeom &gd = ws->geom_dir, &gu = ws->geom_upd;
+        int g1 = gd.ntx * gd.nty * gd.nchunk, g2 = gu.ntx * gu.nty * gu.nchunk;
+        if (g1 > maxg) maxg = g1;
+        if (g2 > maxg) maxg = g2;
+    }
     size_t vec = (size_t)ws->n * sizeof(double);
     cudaError_t e = cudaSuccess;
     for (double **b : {&ws->r, &ws->x, &ws->p[0], &ws->p[1]})
@@ -458,6 +694,7 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
         cf_cg_destroy(ws);
         return rc;
     }
+    if (ws->tma && !cf::build_maps(ws)) ws->tma = false;  // fall back to the LDG march
     *out = ws;
     return CF_OK;
 }
@@ -545,6 +782,8 @@ int cf_cg_set_dic(cf_cg *ws, const int32_t *lp, const int32_t *lc, const double 
     std::lock_guard<std::mutex> lk(ws->mu);
     if (!ws->zbuf) CF_CUDA(cudaMalloc(&ws->zbuf, (size_t)ws->n * sizeof(double)));
     if (!ws->wbuf) CF_CUDA(cudaMalloc(&ws->wbuf, (size_t)ws->n * sizeof(double)));
+    if (ws->tma && !cf::make_map(&ws->m_z, ws->zbuf, ws->bx.nx, ws->bx.ny, ws->bx.nz, cf::kHX, cf::kHY))
+        ws->tma = false;
     cf::DicData &dd = ws->dic;
     dd.n = ws->n;
     dd.lp = lp; dd.lc = lc; dd.lv = lv;

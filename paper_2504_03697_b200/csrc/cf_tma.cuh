@@ -1,0 +1,94 @@
+// cf_tma.cuh -- TMA-staged z-march for the 7-point operator on sm_100a.
+//
+// A block owns a TX x TY tile of the x-y plane and a contiguous z-chunk.
+// Planes of the operand(s) are brought into shared memory by the Tensor
+// Memory Accelerator (cp.async.bulk.tensor.3d) as (TX+2) x (TY+2) boxes --
+// the tile plus its one-cell halo; the domain edge is zero-filled by the TMA
+// unit and masked by existence flags -- through an S-stage ring of
+// mbarrier-tracked slots, so S-1 planes are in flight while the block
+// computes one.  This replaces per-thread loads (latency-bound at ~0.5
+// eligible warps/scheduler in the LDG version) with a few bulk copies per
+// plane, and the grid is sized to be resident in a single wave with every
+// z-chunk of a tile column marching in lockstep with its x-y neighbours, so
+// halo rows are served from L2 rather than re-read from HBM.
+#pragma once
+
+#include <cuda.h>
+
+#include "cf_common.cuh"
+
+namespace cf {
+
+constexpr int kTTX = 32;               // tile x (one warp per row)
+constexpr int kTTY = 16;               // tile y (16 warps)
+constexpr int kTThreads = kTTX * kTTY;  // 512
+// Halo box: x from x0-2 (the TMA unit faults unless a box's x origin is a
+// 16-byte multiple -- measured: any odd fp64 x origin traps -- so the box
+// starts two cells early and is 36 wide), y from y0-1, 18 tall.  Box origins
+// are clamped at 0: negative coordinates trap as well.
+constexpr int kHX = kTTX + 4, kHY = kTTY + 2;
+constexpr int kStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap *map)
+{
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// Geometry of the staged march: grid = ntx*nty tiles x nchunk z-chunks.
+struct TmaGeom {
+    int nx, ny, nz;
+    int lo_halo, hi_halo;  // plane -1 / plane nz exist in memory (z-slab halos)
+    int ntx, nty, nchunk;
+};
+
+// Host: encode a 3-D fp64 tensor map over an x-fastest block with `planes`
+// planes starting at `base`, box (bx, by, 1).  Returns false when TMA cannot
+// describe the array (row pitch not a multiple of 16 bytes, ...).
+bool make_map(CUtensorMap *map, const double *base, int nx, int ny, int planes, int bx, int by);
+
+// Host: chunk count and grid for a kernel with `blocks_per_sm` residency.
+TmaGeom tma_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, int blocks_per_sm);
+
+}  // namespace cf
