@@ -267,165 +267,7 @@ __global__ void __launch_bounds__(kMarchThreads) cg_rz_kernel(long long n, const
     }
 }
 
-// ---------------------------------------------------------------- TMA-staged kernels
-// Same arithmetic as cg_dir_kernel / cg_update_kernel; operands arrive by
-// TMA into a 4-stage shared-memory ring (cf_tma_march.cuh).
-
-template <int PK>
-struct DirPolicy {
-    const CUtensorMap *mz, *mp;
-    double *sz, *sp;  // stage bases (kStages x kBoxStride each)
-    double zc, beta;
-    bool first;
-    int lo;  // plane offset of the tensor maps (lo halo)
-    double *p_new;
-    long long nx, plane;
-    double pap = 0.0;
-
-    __device__ void prefetch() const
-    {
-        prefetch_map(mz);
-        prefetch_map(mp);
-    }
-    __device__ void issue(int s, int bx0, int by0, int, int, int z, int, int, uint64_t *bar) const
-    {
-        mbar_expect_tx(bar, first ? kBoxBytes : 2 * kBoxBytes);
-        tma_load_3d(sz + s * kBoxStride, mz, bx0, by0, z + lo, bar);
-        if (!first) tma_load_3d(sp + s * kBoxStride, mp, bx0, by0, z + lo, bar);
-    }
-    __device__ __forceinline__ double value(int s, int o) const
-    {
-        const double rv = sz[s * kBoxStride + o];
-        const double z = PK == PK_JCONST ? rv * zc : rv;  // NONE and ZVEC stage z itself
-        return first ? z : z + beta * sp[s * kBoxStride + o];
-    }
-    __device__ __forceinline__ void epi(int, int, int, int i, int j, int z, double c, double ax)
-    {
-        p_new[i + nx * j + plane * z] = c;
-        pap = pap + c * ax;
-    }
-};
-
-template <int ORDER, int PK>
-__global__ void __launch_bounds__(kTThreads, 2) cg_dir_tma(const __grid_constant__ CUtensorMap mz,
-                                                           const __grid_constant__ CUtensorMap mp, TmaGeom g,
-                                                           double off, double diag, double *__restrict__ p_new,
-                                                           double zc, CgScalars *sc, double *partials, CgTickets *tk)
-{
-    extern __shared__ unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t bars[kStages];
-    __shared__ double red[32];
-    __shared__ int is_last;
-    if (sc->done) return;
-    double *base = aligned_smem(smem_raw);
-    DirPolicy<PK> pol{&mz, &mp, base, base + kStages * kBoxStride, zc, sc->beta, sc->it == 0, g.lo_halo, p_new,
-                      g.nx, (long long)g.nx * g.ny};
-    staged_march<ORDER>(g, off, diag, pol, bars);
-    double pap = block_sum<kTThreads>(pol.pap, red);
-    if (threadIdx.x == 0) partials[blockIdx.x] = pap;
-    if (last_block(&tk->dir, &is_last)) {
-        pap = reduce_partials<kTThreads>(partials, gridDim.x, 1, red);
-        if (threadIdx.x == 0) {
-            sc->pap = pap;
-            if (pap <= 0.0) {
-                sc->status = ST_BREAKDOWN;
-                sc->done = 1;
-            } else {
-                sc->alpha = sc->rz / pap;
-            }
-        }
-    }
-}
-
-template <int PK>
-struct UpdPolicy {
-    const CUtensorMap *mp, *mr, *mx;
-    double *sp, *sr, *sx;
-    int lo;
-    double alpha, malpha, zc;
-    double *r, *x;
-    long long nx, plane;
-    double rr = 0.0, rz = 0.0;
-
-    __device__ void prefetch() const
-    {
-        prefetch_map(mp);
-        prefetch_map(mr);
-        prefetch_map(mx);
-    }
-    __device__ void issue(int s, int bx0, int by0, int x0, int y0, int z, int z0, int z1, uint64_t *bar) const
-    {
-        const bool own = z >= z0 && z < z1;  // r and x only for owned planes
-        mbar_expect_tx(bar, kBoxBytes + (own ? 2 * kIntBytes : 0));
-        tma_load_3d(sp + s * kBoxStride, mp, bx0, by0, z + lo, bar);
-        if (own) {
-            tma_load_3d(sr + s * kInt, mr, x0, y0, z + lo, bar);
-            tma_load_3d(sx + s * kInt, mx, x0, y0, z + lo, bar);
-        }
-    }
-    __device__ __forceinline__ double value(int s, int o) const { return sp[s * kBoxStride + o]; }
-    __device__ __forceinline__ void epi(int s, int tx, int ty, int i, int j, int z, double c, double ax)
-    {
-        const int k = ty * kTTX + tx;
-        const long long g = i + nx * j + plane * z;
-        x[g] = sx[s * kInt + k] + alpha * c;             // src/solver.py:155
-        const double rn = sr[s * kInt + k] + malpha * ax;  // :157
-        r[g] = rn;
-        rr = rr + rn * rn;
-        if (PK != PK_ZVEC) rz = rz + rn * zval<PK>(rn, nullptr, 0, zc);
-    }
-};
-
-template <int ORDER, int PK>
-__global__ void __launch_bounds__(kTThreads, 2) cg_update_tma(
-    const __grid_constant__ CUtensorMap mp, const __grid_constant__ CUtensorMap mr,
-    const __grid_constant__ CUtensorMap mx, TmaGeom g, double off, double diag, double *__restrict__ r,
-    double *__restrict__ x, double zc, CgScalars *sc, double *partials, CgTickets *tk, int use_cond,
-    cudaGraphConditionalHandle cond)
-{
-    extern __shared__ unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t bars[kStages];
-    __shared__ double red[32];
-    __shared__ int is_last;
-    if (sc->done) {
-        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
-        return;
-    }
-    double *base = aligned_smem(smem_raw);
-    const double alpha = sc->alpha;
-    UpdPolicy<PK> pol{&mp, &mr, &mx, base, base + kStages * kBoxStride, base + kStages * (kBoxStride + kInt),
-                      g.lo_halo, alpha, -alpha, zc, r, x, g.nx, (long long)g.nx * g.ny};
-    staged_march<ORDER>(g, off, diag, pol, bars);
-    double rr = block_sum<kTThreads>(pol.rr, red);
-    double rz = PK != PK_ZVEC ? block_sum<kTThreads>(pol.rz, red) : 0.0;
-    if (threadIdx.x == 0) {
-        partials[2 * blockIdx.x] = rr;
-        partials[2 * blockIdx.x + 1] = rz;
-    }
-    if (last_block(&tk->upd, &is_last)) {
-        rr = reduce_partials<kTThreads>(partials, gridDim.x, 2, red);
-        if (PK != PK_ZVEC) rz = reduce_partials<kTThreads>(partials + 1, gridDim.x, 2, red);
-        if (threadIdx.x == 0) {
-            sc->rr = rr;
-            sc->it += 1;
-            sc->res = sqrt(rr) / sc->norm_b;
-            if (sc->res <= sc->tol) {
-                sc->status = ST_CONVERGED;
-                sc->done = 1;
-            } else if (sc->it >= sc->max_iter) {
-                sc->status = ST_MAXITER;
-                sc->done = 1;
-            } else if (PK != PK_ZVEC) {
-                sc->beta = rz / sc->rz;
-                sc->rz = rz;
-            }
-            if (sc->done && use_cond) cudaGraphSetConditional(cond, 0);
-        }
-    }
-}
-
-constexpr size_t kDirSmem = 2 * kStages * kBoxStride * sizeof(double) + 128;
-constexpr size_t kUpdSmem = kStages * (kBoxStride + 2 * kInt) * sizeof(double) + 128;
+#include "cf_cg_tma.cuh"
 
 }  // namespace cf
 
@@ -471,11 +313,11 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
         double *p_new = ws->p[half ^ 1];
         if (PK != PK_JVEC && ws->tma) {
             const TmaGeom &gd = ws->geom_dir, &gu = ws->geom_upd;
-            cg_dir_tma<ORDER, PK><<<gd.ntx * gd.nty * gd.nchunk, kTThreads, kDirSmem, s>>>(
+            cg_dir_tma<ORDER, PK><<<gd.ntx * gd.nty * gd.nchunk, kPThreads, kDirSmem, s>>>(
                 PK == PK_ZVEC ? ws->m_z : ws->m_r, ws->m_p[half], gd, ws->off, ws->diag, p_new, zc, ws->sc,
                 ws->partials, ws->tk);
             CF_CHECK_LAUNCH("cg_dir_tma");
-            cg_update_tma<ORDER, PK><<<gu.ntx * gu.nty * gu.nchunk, kTThreads, kUpdSmem, s>>>(
+            cg_update_tma<ORDER, PK><<<gu.ntx * gu.nty * gu.nchunk, kPThreads, kUpdSmem, s>>>(
                 ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc,
                 ws->partials, ws->tk, use_cond, cond);
             CF_CHECK_LAUNCH("cg_update_tma");
@@ -629,8 +471,8 @@ static void set_grids(cf_cg *ws)
         cudaFuncSetAttribute(cg_update_tma<ORDER, PK_JCONST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kUpdSmem);
         cudaFuncSetAttribute(cg_update_tma<ORDER, PK_ZVEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bd, cg_dir_tma<ORDER, PK_JCONST>, kTThreads, kDirSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, cg_update_tma<ORDER, PK_JCONST>, kTThreads, kUpdSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bd, cg_dir_tma<ORDER, PK_JCONST>, kPThreads, kDirSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, cg_update_tma<ORDER, PK_JCONST>, kPThreads, kUpdSmem);
         ws->geom_dir = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bd > 0 ? bd : 1);
         ws->geom_upd = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bu > 0 ? bu : 1);
     }
