@@ -128,6 +128,28 @@ int cf_cg_set_dic(cf_cg *ws, const int32_t *lp, const int32_t *lc, const double 
                   const int32_t *uc, const double *uv, const double *d, const int32_t *level_rows,
                   const int64_t *level_ptr_host, int nlevels);
 
+/* ---- z-slab conjugate gradient (multi-GPU; SURVEY.md §5.8, §8 e) -------- */
+typedef struct cf_dcg cf_dcg;
+/* 128-byte NCCL unique id (rank 0 creates it and broadcasts it). */
+int cf_nccl_unique_id(void *out128);
+/* CG over z-slabs of an nx*ny*nz grid (nx even >= 32).  This process owns
+ * `nslabs` consecutive slabs with global plane bounds slab_bounds[0..nslabs]
+ * on the current device; lo_rank / hi_rank are the ranks owning the slabs
+ * below / above (-1: none).  nccl_id NULL (or nranks 1) runs without NCCL --
+ * several slabs in one process is the single-device emulation of the
+ * decomposition.  The reference has no distributed solver; the iterates are
+ * the reference's CG (src/solver.py:128-171) up to reduction order. */
+int cf_dcg_create(cf_dcg **ws, int nx, int ny, int nz, double h, int order, int nranks, int rank,
+                  const void *nccl_id, int nslabs, const int *slab_bounds, int lo_rank, int hi_rank,
+                  void *stream);
+int cf_dcg_destroy(cf_dcg *ws);
+/* b_slabs / x_slabs: per local slab, device pointers to its owned planes
+ * (nx*ny*(z1-z0) doubles, x fastest).  precond: CF_PRECOND_NONE or
+ * CF_PRECOND_JACOBI (constant diagonal).  Same return codes as cf_cg_solve. */
+int cf_dcg_solve(cf_dcg *ws, const double *const *b_slabs, double *const *x_slabs, double tol,
+                 int64_t max_iter, int precond, int64_t *iters_host, double *res_host, void *stream);
+int cf_dcg_last_loop_ms(cf_dcg *ws, float *ms_host);
+
 /* ---- time-step kernels (src/sim.py:134-289, :352-449) ------------------- */
 /* Lid forcing u[1:n, n-1, :] += lid_dv, then zero the six wall-normal face
  * planes.  Replaces apply_forces + enforce_boundaries (:134-149).

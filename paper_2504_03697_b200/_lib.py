@@ -61,6 +61,12 @@ _SIGNATURES = {
     "cf_cg_destroy": ([_vp], _int),
     "cf_cg_solve": ([_vp, _vp, _vp, _vp, _dbl, _i64, _int, _vp, _pi64, _pd, _vp], _int),
     "cf_cg_last_loop_ms": ([_vp, _pf], _int),
+    "cf_nccl_unique_id": ([_vp], _int),
+    "cf_dcg_create": ([ctypes.POINTER(_vp), _int, _int, _int, _dbl, _int, _int, _int, _vp, _int, _vp, _int, _int,
+                       _vp], _int),
+    "cf_dcg_destroy": ([_vp], _int),
+    "cf_dcg_solve": ([_vp, _vp, _vp, _dbl, _i64, _int, _pi64, _pd, _vp], _int),
+    "cf_dcg_last_loop_ms": ([_vp, _pf], _int),
     "cf_forces_bc": ([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _int, _vp], _int),
     "cf_advect": ([_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _vp], _int),
     "cf_divergence": ([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _vp, _pd, _vp], _int),

@@ -23,34 +23,12 @@
 #include <mutex>
 #include <vector>
 
+#include "cf_cg_common.cuh"
 #include "cf_dic.cuh"
 #include "cf_stencil.cuh"
 #include "cf_tma_march.cuh"
 
 namespace cf {
-
-enum PrecKind { PK_NONE = 0, PK_JCONST = 1, PK_JVEC = 2, PK_ZVEC = 3 };
-
-struct CgScalars {
-    double rz, alpha, beta, pap, rr, norm_b, res, tol;
-    long long it, max_iter;
-    int done, status;  // status: 0 running, 1 converged, 2 max_iter, 3 breakdown
-};
-
-enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_BREAKDOWN = 3 };
-
-struct CgTickets {
-    unsigned int init, dir, upd, pad;
-};
-
-template <int PK>
-__device__ __forceinline__ double zval(double r, const double *__restrict__ jd, long long i, double zc)
-{
-    // z = M^-1 r: src/solver.py:71-76 (none) and src/precond.py:94 (Jacobi)
-    if (PK == PK_NONE) return r;
-    if (PK == PK_JCONST) return r * zc;
-    return r * __ldg(jd + i);
-}
 
 // ---------------------------------------------------------------- init
 // r = b, x = 0, |b|^2 and r.z (src/solver.py:60-61, :130-143).
@@ -315,11 +293,11 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
             const TmaGeom &gd = ws->geom_dir, &gu = ws->geom_upd;
             cg_dir_tma<ORDER, PK><<<gd.ntx * gd.nty * gd.nchunk, kPThreads, kDirSmem, s>>>(
                 PK == PK_ZVEC ? ws->m_z : ws->m_r, ws->m_p[half], gd, ws->off, ws->diag, p_new, zc, ws->sc,
-                ws->partials, ws->tk);
+                ws->partials, ws->tk, nullptr);
             CF_CHECK_LAUNCH("cg_dir_tma");
             cg_update_tma<ORDER, PK><<<gu.ntx * gu.nty * gu.nchunk, kPThreads, kUpdSmem, s>>>(
                 ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc,
-                ws->partials, ws->tk, use_cond, cond);
+                ws->partials, ws->tk, use_cond, cond, nullptr);
             CF_CHECK_LAUNCH("cg_update_tma");
         } else {
         cg_dir_kernel<ORDER, PK><<<ws->grid_dir, kMarchThreads, 0, s>>>(

@@ -1,0 +1,80 @@
+// cf_cg_common.cuh -- device state shared by the single-domain CG
+// (cf_cg.cu) and the z-slab CG (cf_dist.cu).
+#pragma once
+
+#include "cf_common.cuh"
+
+namespace cf {
+
+enum PrecKind { PK_NONE = 0, PK_JCONST = 1, PK_JVEC = 2, PK_ZVEC = 3 };
+
+struct CgScalars {
+    double rz, alpha, beta, pap, rr, norm_b, res, tol;
+    long long it, max_iter;
+    int done, status;  // status: 0 running, 1 converged, 2 max_iter, 3 breakdown
+};
+
+enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_BREAKDOWN = 3 };
+
+struct CgTickets {
+    unsigned int init, dir, upd, pad;
+};
+
+template <int PK>
+__device__ __forceinline__ double zval(double r, const double *__restrict__ jd, long long i, double zc)
+{
+    // z = M^-1 r: src/solver.py:71-76 (none) and src/precond.py:94 (Jacobi)
+    if (PK == PK_NONE) return r;
+    if (PK == PK_JCONST) return r * zc;
+    return r * __ldg(jd + i);
+}
+
+// The scalar recurrences of src/solver.py, shared by the last block of the
+// single-domain kernels and by the z-slab scalar kernel (after the
+// all-reduce).
+__device__ __forceinline__ void scalar_after_dir(CgScalars *sc, double pap)
+{
+    sc->pap = pap;
+    if (pap <= 0.0) {  // src/solver.py:151-152
+        sc->status = ST_BREAKDOWN;
+        sc->done = 1;
+    } else {
+        sc->alpha = sc->rz / pap;  // :153
+    }
+}
+
+// returns true when the solve has stopped
+template <bool HAS_RZ>
+__device__ __forceinline__ bool scalar_after_update(CgScalars *sc, double rr, double rz)
+{
+    sc->rr = rr;
+    sc->it += 1;                          // :158
+    sc->res = sqrt(rr) / sc->norm_b;      // :159
+    if (sc->res <= sc->tol) {             // :160-162
+        sc->status = ST_CONVERGED;
+        sc->done = 1;
+    } else if (sc->it >= sc->max_iter) {  // :147
+        sc->status = ST_MAXITER;
+        sc->done = 1;
+    } else if (HAS_RZ) {
+        sc->beta = rz / sc->rz;  // :165-166
+        sc->rz = rz;
+    }
+    return sc->done != 0;
+}
+
+__device__ __forceinline__ void scalar_after_init(CgScalars *sc, double bb, double rz)
+{
+    sc->norm_b = sqrt(bb);  // src/solver.py:60-61
+    sc->rz = rz;            // :143
+    sc->beta = 0.0;
+    sc->it = 0;
+    sc->res = INFINITY;
+    if (sc->norm_b == 0.0) {  // :62-64
+        sc->done = 1;
+        sc->status = ST_CONVERGED;
+        sc->res = 0.0;
+    }
+}
+
+}  // namespace cf

@@ -15,7 +15,8 @@ template <int ORDER, int PK>
 __global__ void __launch_bounds__(kPThreads) cg_dir_tma(const __grid_constant__ CUtensorMap mz,
                                                         const __grid_constant__ CUtensorMap mp, TmaGeom g,
                                                         double off, double diag, double *__restrict__ p_new,
-                                                        double zc, CgScalars *sc, double *partials, CgTickets *tk)
+                                                        double zc, CgScalars *sc, double *partials, CgTickets *tk,
+                                                        double *red_out)
 {
     extern __shared__ unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[kStages];
@@ -69,6 +70,16 @@ __global__ void __launch_bounds__(kPThreads) cg_dir_tma(const __grid_constant__ 
         }
         __syncthreads();  // ring slot q complete; TMA slot q fully consumed
         if (threadIdx.x == 0 && q + kStages < m.nplanes) issue(q + kStages);
+        if (q < m.nplanes && m.valid) {
+            // z-slab halo planes: p there is recomputed from the exchanged r
+            // halo (bit-identical to the neighbour's owned p) and stored, so
+            // the update kernel's stencil can read it
+            const int zq = m.zs + q;
+            if (zq == -1 || zq == g.nz) {
+                const double2 v = ld2(ring + (q % kPnSlots) * kBoxStride + m.o);
+                st2(out + plane * zq, v.x, v.y);
+            }
+        }
         const int z = m.zs + q - 1;
         if (z >= m.z0 && z < m.z1 && m.valid) {
             const bool hzm = z - 1 >= m.zlo, hzp = z + 1 <= m.zhi;
@@ -96,13 +107,8 @@ __global__ void __launch_bounds__(kPThreads) cg_dir_tma(const __grid_constant__ 
     if (last_block(&tk->dir, &is_last)) {
         pap = reduce_partials<kPThreads>(partials, gridDim.x, 1, red);
         if (threadIdx.x == 0) {
-            sc->pap = pap;
-            if (pap <= 0.0) {  // src/solver.py:151-152
-                sc->status = ST_BREAKDOWN;
-                sc->done = 1;
-            } else {
-                sc->alpha = sc->rz / pap;
-            }
+            if (red_out) red_out[0] = pap;  // z-slab: summed across slabs/ranks first
+            else scalar_after_dir(sc, pap);
         }
     }
 }
@@ -157,7 +163,7 @@ __global__ void __launch_bounds__(kPThreads) cg_update_tma(
     const __grid_constant__ CUtensorMap mp, const __grid_constant__ CUtensorMap mr,
     const __grid_constant__ CUtensorMap mx, TmaGeom g, double off, double diag, double *__restrict__ r,
     double *__restrict__ x, double zc, CgScalars *sc, double *partials, CgTickets *tk, int use_cond,
-    cudaGraphConditionalHandle cond)
+    cudaGraphConditionalHandle cond, double *red_out)
 {
     extern __shared__ unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[kStages];
@@ -182,20 +188,12 @@ __global__ void __launch_bounds__(kPThreads) cg_update_tma(
         rr = reduce_partials<kPThreads>(partials, gridDim.x, 2, red);
         if (PK != PK_ZVEC) rz = reduce_partials<kPThreads>(partials + 1, gridDim.x, 2, red);
         if (threadIdx.x == 0) {
-            sc->rr = rr;
-            sc->it += 1;
-            sc->res = sqrt(rr) / sc->norm_b;
-            if (sc->res <= sc->tol) {
-                sc->status = ST_CONVERGED;
-                sc->done = 1;
-            } else if (sc->it >= sc->max_iter) {
-                sc->status = ST_MAXITER;
-                sc->done = 1;
-            } else if (PK != PK_ZVEC) {
-                sc->beta = rz / sc->rz;
-                sc->rz = rz;
+            if (red_out) {  // z-slab: summed across slabs/ranks first
+                red_out[0] = rr;
+                red_out[1] = rz;
+            } else if (scalar_after_update<PK != PK_ZVEC>(sc, rr, rz) && use_cond) {
+                cudaGraphSetConditional(cond, 0);
             }
-            if (sc->done && use_cond) cudaGraphSetConditional(cond, 0);
         }
     }
 }
