@@ -175,6 +175,24 @@ int cf_divergence(const double *u, const double *v, const double *w, int n, int 
 int cf_pressure_correct(const double *u, const double *v, const double *w, double *nu, double *nv,
                         double *nw, const double *p, int n, int ldu, int ldv, int ldw, double h,
                         double coef, double *div_post_host, void *stream);
+/* z-slab forms of the four step kernels (multi-GPU): the
+ * slab owns global planes [z0, z1) of the n-cube and its velocity arrays hold
+ * planes z0-halo .. (u, v: z1+halo-1; w: z1+halo), pointers at the first
+ * stored plane; scalar arrays (out, p) are slab-local with plane 0 = z0 and,
+ * for p, readable halo planes -1 / z1-z0 where neighbours exist.  Owned w
+ * faces are [z0, z1) plus face n on the last slab.  With z0 = 0, z1 = n,
+ * halo = 0 they are the single-domain kernels above. */
+int cf_forces_bc_slab(double *u, double *v, double *w, int n, int z0, int z1, int halo, int ldu, int ldv,
+                      int ldw, double lid_dv, int apply_lid, void *stream);
+int cf_advect_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
+                   int n, int z0, int z1, int halo, int ldu, int ldv, int ldw, double h, double dt,
+                   void *stream);
+int cf_divergence_slab(const double *u, const double *v, const double *w, int n, int z0, int z1, int halo,
+                       int ldu, int ldv, int ldw, double h, double scale, double *out, double *maxabs_host,
+                       void *stream);
+int cf_pressure_correct_slab(const double *u, const double *v, const double *w, double *nu, double *nv,
+                             double *nw, const double *p, int n, int z0, int z1, int halo, int ldu, int ldv,
+                             int ldw, double h, double coef, double *div_post_host, void *stream);
 /* Trilinear sample of all three components at one point (src/grid.py:124-142);
  * result (3 doubles) to out_host. */
 int cf_sample_velocity(const double *u, const double *v, const double *w, int n, int ldu,

@@ -72,7 +72,14 @@ _SIGNATURES = {
     "cf_divergence": ([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _vp, _pd, _vp], _int),
     "cf_pressure_correct": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl,
                              _pd, _vp], _int),
-    "cf_sample_velocity": ([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _dbl, _dbl, _pd, _vp],
+    "cf_forces_bc_slab": ([_vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _int, _dbl, _int, _vp], _int),
+    "cf_advect_slab": ([_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _int, _dbl, _dbl, _vp],
+                       _int),
+    "cf_divergence_slab": ([_vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _int, _dbl, _dbl, _vp, _pd, _vp],
+                           _int),
+    "cf_pressure_correct_slab": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _int, _dbl,
+                                  _dbl, _pd, _vp], _int),
+    "cf_sample_velocity":([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _dbl, _dbl, _pd, _vp],
                            _int),
 }
 

@@ -453,6 +453,8 @@ static void set_grids(cf_cg *ws)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, cg_update_tma<ORDER, PK_JCONST>, kPThreads, kUpdSmem);
         ws->geom_dir = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bd > 0 ? bd : 1);
         ws->geom_upd = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bu > 0 ? bu : 1);
+        if (const char *e = getenv("CF_TMA_CHUNKS_DIR")) ws->geom_dir.nchunk = atoi(e) > 0 ? atoi(e) : 1;
+        if (const char *e = getenv("CF_TMA_CHUNKS_UPD")) ws->geom_upd.nchunk = atoi(e) > 0 ? atoi(e) : 1;
     }
 }
 

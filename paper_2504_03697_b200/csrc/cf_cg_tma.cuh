@@ -68,7 +68,8 @@ __global__ void __launch_bounds__(kPThreads) cg_dir_tma(const __grid_constant__ 
                 st2(slot + pos, r2.x, r2.y);
             }
         }
-        __syncthreads();  // ring slot q complete; TMA slot q fully consumed
+        fence_proxy_async_smem();  // my reads of TMA slot q before its refill
+        __syncthreads();           // ring slot q complete; TMA slot q fully consumed
         if (threadIdx.x == 0 && q + kStages < m.nplanes) issue(q + kStages);
         if (q < m.nplanes && m.valid) {
             // z-slab halo planes: p there is recomputed from the exchanged r

@@ -3,21 +3,26 @@
 // arithmetic in the reference's order (-fmad=false), so results are
 // bit-identical to the reference.
 //
-// Velocity layout: component c has extents (na, nb, nc) = (n+[c==0],
+// Velocity layout: component c has global extents (na, nb, nc) = (n+[c==0],
 // n+[c==1], n+[c==2]) stored x-fastest with row pitch ld_c (padded to a
 // 32-double multiple by the host so every row starts 256-B aligned) and plane
-// pitch ld_c*nb.
+// pitch ld_c*nb.  Every kernel also runs on a z-slab: the arrays then hold the
+// global planes k_base .. (k_base + stored planes - 1) where k_base = z0 - H
+// (H halo planes below the slab's first owned plane z0); the single-domain
+// entry points are the slab [0, n) with H = 0.
 #include "cf_common.cuh"
 
 namespace cf {
 
 struct Comp {
     const double *a;
-    int na, nb, nc, ld;
-    __device__ __forceinline__ double at(int i, int j, int k) const
+    int na, nb, nc, ld;  // global extents, row pitch
+    int k_base;          // global plane index of a's first stored plane
+    __device__ __forceinline__ long long off(int i, int j, int k) const
     {
-        return __ldg(a + (long long)i + (long long)ld * ((long long)j + (long long)nb * k));
+        return (long long)i + (long long)ld * ((long long)j + (long long)nb * (k - k_base));
     }
+    __device__ __forceinline__ double at(int i, int j, int k) const { return __ldg(a + off(i, j, k)); }
 };
 
 __device__ __forceinline__ double clamp_hi(double a, double hi)
@@ -55,28 +60,43 @@ struct Vel3 {
     Comp c[3];
 };
 
-__host__ __device__ inline Comp make_comp(const double *a, int n, int comp, int ld)
+// Slab of the cube: owned planes [z0, z1) of n; H halo planes each side.
+struct SlabZ {
+    int n, z0, z1, H;
+    __host__ __device__ int k_base() const { return z0 - H; }
+    // owned w faces: [z0, z1), plus the top wall face when the slab ends at n
+    __host__ __device__ int w_end() const { return z1 == n ? n + 1 : z1; }
+};
+
+__host__ __device__ inline Comp make_comp(const double *a, int n, int comp, int ld, int k_base)
 {
-    return Comp{a, n + (comp == 0), n + (comp == 1), n + (comp == 2), ld};
+    return Comp{a, n + (comp == 0), n + (comp == 1), n + (comp == 2), ld, k_base};
+}
+
+static Vel3 make_vel(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw, int kb)
+{
+    return Vel3{{make_comp(u, n, 0, ldu, kb), make_comp(v, n, 1, ldv, kb), make_comp(w, n, 2, ldw, kb)}};
 }
 
 constexpr int kFaceThreads = 256;
 
 // src/sim.py:193-240 + :283-288.  blockIdx.y = component; a grid-stride
-// loop over the component's faces with i fastest (coalesced stores).
+// loop over the slab's owned faces with i fastest (coalesced stores).
 __global__ void __launch_bounds__(kFaceThreads) advect_kernel(Vel3 in, double *nu, double *nv, double *nw,
-                                                              int n, double h, double dt, double length)
+                                                              SlabZ sz, double h, double dt, double length)
 {
     const int comp = blockIdx.y;
+    const int n = sz.n;
     const Comp me = in.c[comp];
     double *out = comp == 0 ? nu : (comp == 1 ? nv : nw);
-    const long long total = (long long)me.na * me.nb * me.nc;
+    const int kend = comp == 2 ? sz.w_end() : sz.z1;
+    const long long total = (long long)me.na * me.nb * (kend - sz.z0);
     const long long stride = (long long)gridDim.x * kFaceThreads;
     for (long long f = (long long)blockIdx.x * kFaceThreads + threadIdx.x; f < total; f += stride) {
         const int i = (int)(f % me.na);
         const long long rest = f / me.na;
-        const int j = (int)(rest % me.nb), k = (int)(rest / me.nb);
-        double *dst = out + (long long)i + (long long)me.ld * ((long long)j + (long long)me.nb * k);
+        const int j = (int)(rest % me.nb), k = sz.z0 + (int)(rest / me.nb);
+        double *dst = out + me.off(i, j, k);
         const int wall = comp == 0 ? i : (comp == 1 ? j : k);
         if (wall == 0 || wall == n) {  // wall-normal planes are zeroed (:283-288)
             *dst = 0.0;
@@ -104,28 +124,31 @@ __global__ void __launch_bounds__(kFaceThreads) advect_kernel(Vel3 in, double *n
     }
 }
 
-// src/sim.py:134-149.  blockIdx.y selects the task: 0 = lid row
-// u[1:n, n-1, :] += lid_dv; 1..6 = the six wall-normal planes.
-__global__ void forces_bc_kernel(double *u, double *v, double *w, int n, int ldu, int ldv, int ldw,
-                                 double lid_dv, int apply_lid)
+// src/sim.py:134-149 on the slab.  blockIdx.y selects the task: 0 = lid row
+// u[1:n, n-1, k] += lid_dv; 1..6 = the six wall-normal planes.
+__global__ void forces_bc_kernel(double *u, double *v, double *w, SlabZ sz, int ldu, int ldv, int ldw, double lid_dv,
+                                 int apply_lid)
 {
     const int task = blockIdx.y;
+    const int n = sz.n, kb = sz.k_base(), nzl = sz.z1 - sz.z0;
     const long long m = (long long)(n + 1) * (n + 1);
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < m;
-         t += (long long)gridDim.x * blockDim.x) {
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += (long long)gridDim.x * blockDim.x) {
         const int a = (int)(t % (n + 1)), b = (int)(t / (n + 1));
-        if (task == 0) {
-            // a = i in [1, n-1], b = k in [0, n)
-            if (apply_lid && a >= 1 && a <= n - 1 && b < n) {
-                double *q = u + a + (long long)ldu * ((long long)(n - 1) + (long long)n * b);
+        if (task == 0) {  // a = i in [1, n-1], b = local k
+            if (apply_lid && a >= 1 && a <= n - 1 && b < nzl) {
+                double *q = u + a + (long long)ldu * ((long long)(n - 1) + (long long)n * (sz.z0 + b - kb));
                 *q = *q + lid_dv;
             }
-        } else if (task <= 2) {  // u[0|n, j, k]: a = j, b = k
-            if (a < n && b < n) u[(task == 1 ? 0 : n) + (long long)ldu * (a + (long long)n * b)] = 0.0;
-        } else if (task <= 4) {  // v[i, 0|n, k]: a = i, b = k
-            if (a < n && b < n) v[a + (long long)ldv * ((task == 3 ? 0 : n) + (long long)(n + 1) * b)] = 0.0;
-        } else {  // w[i, j, 0|n]: a = i, b = j
-            if (a < n && b < n) w[a + (long long)ldw * (b + (long long)n * (task == 5 ? 0 : n))] = 0.0;
+        } else if (task <= 2) {  // u[0|n, j, k]: a = j, b = local k
+            if (a < n && b < nzl)
+                u[(task == 1 ? 0 : n) + (long long)ldu * (a + (long long)n * (sz.z0 + b - kb))] = 0.0;
+        } else if (task <= 4) {  // v[i, 0|n, k]: a = i, b = local k
+            if (a < n && b < nzl)
+                v[a + (long long)ldv * ((task == 3 ? 0 : n) + (long long)(n + 1) * (sz.z0 + b - kb))] = 0.0;
+        } else {  // w[i, j, 0|n] where the slab owns the wall face: a = i, b = j
+            const int k = task == 5 ? 0 : n;
+            const bool owned = task == 5 ? sz.z0 == 0 : sz.z1 == n;
+            if (owned && a < n && b < n) w[a + (long long)ldw * (b + (long long)n * (k - kb))] = 0.0;
         }
     }
 }
@@ -133,21 +156,22 @@ __global__ void forces_bc_kernel(double *u, double *v, double *w, int n, int ldu
 constexpr int kCellThreads = 256;
 
 // src/grid.py:145-154: ((((u1-u0)+v1)-v0)+w1)-w0, then /h, then * scale
-// (src/sim.py:360).  Partial max|out| per block.
-__global__ void __launch_bounds__(kCellThreads) divergence_kernel(Vel3 in, int n, double h, double scale,
-                                                                  int do_scale, double *out,
-                                                                  double *partials, unsigned int *ticket,
-                                                                  double *result)
+// (src/sim.py:360), over the slab's owned cells; out is slab-local (plane
+// k - z0).  Partial max|out| per block.
+__global__ void __launch_bounds__(kCellThreads) divergence_kernel(Vel3 in, SlabZ sz, double h, double scale,
+                                                                  int do_scale, double *out, double *partials,
+                                                                  unsigned int *ticket, double *result)
 {
     __shared__ double red[32];
     __shared__ int is_last;
-    const long long total = (long long)n * n * n;
+    const int n = sz.n;
+    const long long total = (long long)n * n * (sz.z1 - sz.z0);
     const long long stride = (long long)gridDim.x * kCellThreads;
     double mx = 0.0;
     for (long long c = (long long)blockIdx.x * kCellThreads + threadIdx.x; c < total; c += stride) {
         const int i = (int)(c % n);
         const long long rest = c / n;
-        const int j = (int)(rest % n), k = (int)(rest / n);
+        const int j = (int)(rest % n), k = sz.z0 + (int)(rest / n);
         double t = in.c[0].at(i + 1, j, k) - in.c[0].at(i, j, k);
         t = t + in.c[1].at(i, j + 1, k);
         t = t - in.c[1].at(i, j, k);
@@ -168,29 +192,31 @@ __global__ void __launch_bounds__(kCellThreads) divergence_kernel(Vel3 in, int n
     }
 }
 
-// src/sim.py:434-449.  One thread per cell: it recomputes the corrected
-// values of its six faces from the OLD field (reading p with a one-cell
-// halo, ghost p = 0 outside), takes the cell divergence of the corrected
-// faces for div_post, and writes the faces it owns (its three lower faces
-// and, on the high walls, the upper ones) to the output field with the
-// wall-normal faces clamped to zero.
+// src/sim.py:434-449.  One thread per owned cell: it recomputes the
+// corrected values of its six faces from the OLD field (p with a one-plane
+// halo in z, ghost p = 0 outside the cube), takes the cell divergence of the
+// corrected faces for div_post, and writes the faces it owns (its three lower
+// faces and, on the high walls, the upper ones) to the output field with the
+// wall-normal faces clamped to zero.  p is slab-local (plane k - z0) and
+// readable at planes -1 and nzl when the slab has neighbours there.
 __global__ void __launch_bounds__(kCellThreads) correct_kernel(Vel3 in, double *nu, double *nv, double *nw,
-                                                               const double *__restrict__ p, int n,
-                                                               double h, double coef, double *partials,
-                                                               unsigned int *ticket, double *result)
+                                                               const double *__restrict__ p, SlabZ sz, double h,
+                                                               double coef, double *partials, unsigned int *ticket,
+                                                               double *result)
 {
     __shared__ double red[32];
     __shared__ int is_last;
-    const long long total = (long long)n * n * n;
+    const int n = sz.n;
+    const long long total = (long long)n * n * (sz.z1 - sz.z0);
     const long long stride = (long long)gridDim.x * kCellThreads;
     const long long nn = (long long)n * n;
     double mx = 0.0;
     for (long long c = (long long)blockIdx.x * kCellThreads + threadIdx.x; c < total; c += stride) {
         const int i = (int)(c % n);
         const long long rest = c / n;
-        const int j = (int)(rest % n), k = (int)(rest / n);
+        const int j = (int)(rest % n), k = sz.z0 + (int)(rest / n);
         const double pc = __ldg(p + c);
-        // lower face of each axis: interior -> coef*(p - p_prev); wall -> coef*p
+        // lower face: interior -> coef*(p - p_prev); wall -> coef*p
         // upper face: interior -> coef*(p_next - p); wall -> coef*(0.0 - p)
         const double du0 = i > 0 ? pc - __ldg(p + c - 1) : pc;
         const double du1 = i < n - 1 ? __ldg(p + c + 1) - pc : 0.0 - pc;
@@ -211,12 +237,12 @@ __global__ void __launch_bounds__(kCellThreads) correct_kernel(Vel3 in, double *
         t = t - w0;
         mx = fmax(mx, fabs(t / h));
         const Comp &cu = in.c[0], &cv = in.c[1], &cw = in.c[2];
-        nu[(long long)i + (long long)cu.ld * (j + (long long)cu.nb * k)] = i == 0 ? 0.0 : u0;
-        nv[(long long)i + (long long)cv.ld * (j + (long long)cv.nb * k)] = j == 0 ? 0.0 : v0;
-        nw[(long long)i + (long long)cw.ld * (j + (long long)cw.nb * k)] = k == 0 ? 0.0 : w0;
-        if (i == n - 1) nu[(long long)n + (long long)cu.ld * (j + (long long)cu.nb * k)] = 0.0;
-        if (j == n - 1) nv[(long long)i + (long long)cv.ld * (n + (long long)cv.nb * k)] = 0.0;
-        if (k == n - 1) nw[(long long)i + (long long)cw.ld * (j + (long long)cw.nb * n)] = 0.0;
+        nu[cu.off(i, j, k)] = i == 0 ? 0.0 : u0;
+        nv[cv.off(i, j, k)] = j == 0 ? 0.0 : v0;
+        nw[cw.off(i, j, k)] = k == 0 ? 0.0 : w0;
+        if (i == n - 1) nu[cu.off(n, j, k)] = 0.0;
+        if (j == n - 1) nv[cv.off(i, n, k)] = 0.0;
+        if (k == n - 1) nw[cw.off(i, j, n)] = 0.0;
     }
     mx = block_max<kCellThreads>(mx, red);
     if (threadIdx.x == 0) partials[blockIdx.x] = mx;
@@ -236,11 +262,6 @@ __global__ void sample_kernel(Vel3 in, double h, double px, double py, double pz
     out[2] = trilerp(in.c[2], px / h - 0.5, py / h - 0.5, pz / h - 0.0);
 }
 
-static Vel3 make_vel(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw)
-{
-    return Vel3{{make_comp(u, n, 0, ldu), make_comp(v, n, 1, ldv), make_comp(w, n, 2, ldw)}};
-}
-
 static int grid_for(long long work, int threads, int per_sm)
 {
     long long want = (work + threads - 1) / threads;
@@ -249,6 +270,8 @@ static int grid_for(long long work, int threads, int per_sm)
 }
 
 static bool pitches_ok(int n, int ldu, int ldv, int ldw) { return ldu >= n + 1 && ldv >= n && ldw >= n; }
+
+static bool slab_ok(int n, int z0, int z1, int H) { return n >= 1 && 0 <= z0 && z0 < z1 && z1 <= n && H >= 0; }
 
 // One-shot max reduction through the shared scratch, result to host.
 template <class Launch>
@@ -269,71 +292,128 @@ static int reduce_max_to_host(Launch launch, double *result_host, cudaStream_t s
     return CF_OK;
 }
 
-}  // namespace cf
-
-extern "C" {
-
-int cf_forces_bc(double *u, double *v, double *w, int n, int ldu, int ldv, int ldw, double lid_dv,
-                 int apply_lid, void *stream)
+static int forces_bc(double *u, double *v, double *w, SlabZ sz, int ldu, int ldv, int ldw, double lid_dv, int lid,
+                     void *stream)
 {
-    CF_REQUIRE(n >= 1 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_forces_bc: bad grid/pitch");
-    long long m = (long long)(n + 1) * (n + 1);
+    long long m = (long long)(sz.n + 1) * (sz.n + 1);
     dim3 grid((unsigned)((m + 255) / 256 < 1024 ? (m + 255) / 256 : 1024), 7);
-    cf::forces_bc_kernel<<<grid, 256, 0, cf::as_stream(stream)>>>(u, v, w, n, ldu, ldv, ldw, lid_dv,
-                                                                   apply_lid);
+    forces_bc_kernel<<<grid, 256, 0, as_stream(stream)>>>(u, v, w, sz, ldu, ldv, ldw, lid_dv, lid);
     CF_CHECK_LAUNCH("forces_bc_kernel");
     return CF_OK;
 }
 
-int cf_advect(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n,
-              int ldu, int ldv, int ldw, double h, double dt, void *stream)
+static int advect(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, SlabZ sz,
+                  int ldu, int ldv, int ldw, double h, double dt, void *stream)
 {
-    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_advect: bad grid/pitch");
-    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_advect: output aliases input");
-    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw);
-    long long faces = (long long)(n + 1) * n * n;
-    dim3 grid(cf::grid_for(faces, cf::kFaceThreads, 8), 3);
-    cf::advect_kernel<<<grid, cf::kFaceThreads, 0, cf::as_stream(stream)>>>(in, nu, nv, nw, n, h, dt, n * h);
+    Vel3 in = make_vel(u, v, w, sz.n, ldu, ldv, ldw, sz.k_base());
+    long long faces = (long long)(sz.n + 1) * sz.n * (sz.z1 - sz.z0 + 1);
+    dim3 grid(grid_for(faces, kFaceThreads, 8), 3);
+    advect_kernel<<<grid, kFaceThreads, 0, as_stream(stream)>>>(in, nu, nv, nw, sz, h, dt, sz.n * h);
     CF_CHECK_LAUNCH("advect_kernel");
     return CF_OK;
 }
 
-int cf_divergence(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw,
-                  double h, double scale, double *out, double *maxabs_host, void *stream)
+static int divergence(const double *u, const double *v, const double *w, SlabZ sz, int ldu, int ldv, int ldw,
+                      double h, double scale, double *out, double *maxabs_host, void *stream)
 {
-    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_divergence: bad grid/pitch");
-    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw);
-    cudaStream_t s = cf::as_stream(stream);
-    int grid = cf::grid_for((long long)n * n * n, cf::kCellThreads, 8);
-    return cf::reduce_max_to_host(
+    Vel3 in = make_vel(u, v, w, sz.n, ldu, ldv, ldw, sz.k_base());
+    cudaStream_t s = as_stream(stream);
+    int grid = grid_for((long long)sz.n * sz.n * (sz.z1 - sz.z0), kCellThreads, 8);
+    return reduce_max_to_host(
         [&](double *part, unsigned int *tk, double *res) {
-            cf::divergence_kernel<<<grid, cf::kCellThreads, 0, s>>>(in, n, h, scale, scale != 1.0, out, part,
-                                                                    tk, res);
+            divergence_kernel<<<grid, kCellThreads, 0, s>>>(in, sz, h, scale, scale != 1.0, out, part, tk, res);
         },
         maxabs_host, s);
 }
 
-int cf_pressure_correct(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
-                        const double *p, int n, int ldu, int ldv, int ldw, double h, double coef,
-                        double *div_post_host, void *stream)
+static int correct(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
+                   const double *p, SlabZ sz, int ldu, int ldv, int ldw, double h, double coef, double *div_post_host,
+                   void *stream)
 {
-    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_pressure_correct: bad grid/pitch");
-    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_pressure_correct: output aliases input");
-    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw);
-    cudaStream_t s = cf::as_stream(stream);
-    int grid = cf::grid_for((long long)n * n * n, cf::kCellThreads, 8);
-    return cf::reduce_max_to_host(
+    Vel3 in = make_vel(u, v, w, sz.n, ldu, ldv, ldw, sz.k_base());
+    cudaStream_t s = as_stream(stream);
+    int grid = grid_for((long long)sz.n * sz.n * (sz.z1 - sz.z0), kCellThreads, 8);
+    return reduce_max_to_host(
         [&](double *part, unsigned int *tk, double *res) {
-            cf::correct_kernel<<<grid, cf::kCellThreads, 0, s>>>(in, nu, nv, nw, p, n, h, coef, part, tk, res);
+            correct_kernel<<<grid, kCellThreads, 0, s>>>(in, nu, nv, nw, p, sz, h, coef, part, tk, res);
         },
         div_post_host, s);
 }
 
-int cf_sample_velocity(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw,
-                       double h, double px, double py, double pz, double *out_host, void *stream)
+}  // namespace cf
+
+extern "C" {
+
+int cf_forces_bc(double *u, double *v, double *w, int n, int ldu, int ldv, int ldw, double lid_dv, int apply_lid,
+                 void *stream)
+{
+    CF_REQUIRE(n >= 1 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_forces_bc: bad grid/pitch");
+    return cf::forces_bc(u, v, w, cf::SlabZ{n, 0, n, 0}, ldu, ldv, ldw, lid_dv, apply_lid, stream);
+}
+
+int cf_forces_bc_slab(double *u, double *v, double *w, int n, int z0, int z1, int halo, int ldu, int ldv, int ldw,
+                      double lid_dv, int apply_lid, void *stream)
+{
+    CF_REQUIRE(cf::slab_ok(n, z0, z1, halo) && cf::pitches_ok(n, ldu, ldv, ldw), "cf_forces_bc_slab: bad slab");
+    return cf::forces_bc(u, v, w, cf::SlabZ{n, z0, z1, halo}, ldu, ldv, ldw, lid_dv, apply_lid, stream);
+}
+
+int cf_advect(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n, int ldu,
+              int ldv, int ldw, double h, double dt, void *stream)
+{
+    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_advect: bad grid/pitch");
+    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_advect: output aliases input");
+    return cf::advect(u, v, w, nu, nv, nw, cf::SlabZ{n, 0, n, 0}, ldu, ldv, ldw, h, dt, stream);
+}
+
+int cf_advect_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n,
+                   int z0, int z1, int halo, int ldu, int ldv, int ldw, double h, double dt, void *stream)
+{
+    CF_REQUIRE(cf::slab_ok(n, z0, z1, halo) && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_advect_slab: bad slab");
+    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_advect_slab: output aliases input");
+    return cf::advect(u, v, w, nu, nv, nw, cf::SlabZ{n, z0, z1, halo}, ldu, ldv, ldw, h, dt, stream);
+}
+
+int cf_divergence(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw, double h,
+                  double scale, double *out, double *maxabs_host, void *stream)
+{
+    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_divergence: bad grid/pitch");
+    return cf::divergence(u, v, w, cf::SlabZ{n, 0, n, 0}, ldu, ldv, ldw, h, scale, out, maxabs_host, stream);
+}
+
+int cf_divergence_slab(const double *u, const double *v, const double *w, int n, int z0, int z1, int halo, int ldu,
+                       int ldv, int ldw, double h, double scale, double *out, double *maxabs_host, void *stream)
+{
+    CF_REQUIRE(cf::slab_ok(n, z0, z1, halo) && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw),
+               "cf_divergence_slab: bad slab");
+    return cf::divergence(u, v, w, cf::SlabZ{n, z0, z1, halo}, ldu, ldv, ldw, h, scale, out, maxabs_host, stream);
+}
+
+int cf_pressure_correct(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
+                        const double *p, int n, int ldu, int ldv, int ldw, double h, double coef, double *div_post_host,
+                        void *stream)
+{
+    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_pressure_correct: bad grid/pitch");
+    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_pressure_correct: output aliases input");
+    return cf::correct(u, v, w, nu, nv, nw, p, cf::SlabZ{n, 0, n, 0}, ldu, ldv, ldw, h, coef, div_post_host, stream);
+}
+
+int cf_pressure_correct_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
+                             const double *p, int n, int z0, int z1, int halo, int ldu, int ldv, int ldw, double h,
+                             double coef, double *div_post_host, void *stream)
+{
+    CF_REQUIRE(cf::slab_ok(n, z0, z1, halo) && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw),
+               "cf_pressure_correct_slab: bad slab");
+    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_pressure_correct_slab: output aliases input");
+    return cf::correct(u, v, w, nu, nv, nw, p, cf::SlabZ{n, z0, z1, halo}, ldu, ldv, ldw, h, coef, div_post_host,
+                       stream);
+}
+
+int cf_sample_velocity(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw, double h,
+                       double px, double py, double pz, double *out_host, void *stream)
 {
     CF_REQUIRE(n >= 1 && h > 0 && out_host && cf::pitches_ok(n, ldu, ldv, ldw), "cf_sample_velocity: bad args");
-    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw);
+    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw, 0);
     cudaStream_t s = cf::as_stream(stream);
     double *scratch = cf::scratch_partials();
     if (!scratch) { cf::set_error("scratch allocation failed"); return CF_ENOMEM; }

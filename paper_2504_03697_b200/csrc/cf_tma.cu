@@ -58,6 +58,10 @@ TmaGeom tma_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, int blocks_pe
     const long long max_c = nz / 8 > 0 ? nz / 8 : 1;  // keep >= 8 planes per chunk
     if (c > max_c) c = max_c;
     if (c < 1) c = 1;
+    if (const char *e = getenv("CF_TMA_CHUNKS")) {  // debugging / tuning override
+        const int v = atoi(e);
+        if (v >= 1 && v <= nz) c = v;
+    }
     g.nchunk = (int)c;
     return g;
 }

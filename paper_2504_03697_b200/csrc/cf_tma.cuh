@@ -45,6 +45,16 @@ __device__ __forceinline__ void fence_barrier_init()
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Order this thread's generic-proxy shared-memory accesses before later
+// async-proxy (TMA) writes to the same bytes.  bar.sync alone does not order
+// across proxies: without this fence a TMA refill of a stage slot raced the
+// slot's last LDS reads (measured: sporadic wrong stencil values at 4
+// blocks/SM, recurrence and true residual drifting apart).
+__device__ __forceinline__ void fence_proxy_async_smem()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
 {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)

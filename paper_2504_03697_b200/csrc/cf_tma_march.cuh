@@ -111,6 +111,7 @@ __device__ __forceinline__ void staged_pair_march(const TmaGeom &g, double off, 
     const bool inplane_fast = hxl && hxr && hym && hyp;
     auto wait = [&](int q) { mbar_wait(&bars[q % kStages], (uint32_t)((q / kStages) & 1)); };
     auto release = [&](int q) {
+        fence_proxy_async_smem();  // my reads of slot q before its TMA refill
         __syncthreads();
         if (threadIdx.x == 0 && q + kStages < m.nplanes)
             pol.issue(q % kStages, m, m.zs + q + kStages, &bars[q % kStages]);

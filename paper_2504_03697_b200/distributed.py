@@ -106,6 +106,226 @@ def emulated_pcg(op: StencilOperator, b, nslabs: int, tol: float = 1e-6, max_ite
     return (to_host(x) if host else x), st, scg
 
 
+HALO = 2  # velocity halo planes: the backtrace moves <= 1 cell (CFL <= 1) + the trilinear stencil
+
+
+class _SlabFields:
+    """One slab's device fields: velocity (two buffers) with HALO planes,
+    pressure with one halo plane each side, the Poisson RHS."""
+
+    def __init__(self, n: int, z0: int, z1: int, dev):
+        from .grid import padded_ld
+
+        self.n, self.z0, self.z1 = n, z0, z1
+        self.nzl = z1 - z0
+        self.ld = [padded_ld(n + 1), padded_ld(n), padded_ld(n)]
+        self.nb = [n, n + 1, n]
+        planes = [self.nzl + 2 * HALO, self.nzl + 2 * HALO, self.nzl + 1 + 2 * HALO]
+        self.vel = [[torch.zeros((planes[c], self.nb[c], self.ld[c]), dtype=torch.float64, device=dev)
+                     for c in range(3)] for _ in range(2)]
+        self.cur = 0
+        self.p = torch.zeros((self.nzl + 2) * n * n, dtype=torch.float64, device=dev)
+        self.rhs = torch.zeros(self.nzl * n * n, dtype=torch.float64, device=dev)
+
+    def planes(self, c: int, buf: int, k0: int, k1: int) -> torch.Tensor:
+        """Stored planes for global planes [k0, k1) of component c."""
+        kb = self.z0 - HALO
+        return self.vel[buf][c][k0 - kb:k1 - kb]
+
+    def p_owned(self) -> torch.Tensor:
+        pl = self.n * self.n
+        return self.p[pl:pl * (self.nzl + 1)]
+
+    def ptrs(self, buf: int):
+        return tuple(t.data_ptr() for t in self.vel[buf])
+
+
+class SlabSim:
+    """The cavity time step (src/sim.py:452-474) over z-slabs.
+
+    ``bounds`` are the global plane bounds of this process's consecutive slabs
+    (several slabs = single-device emulation; one slab per rank under
+    torch.distributed with ``distributed=True``).  Reference physics,
+    Jacobi/none PCG (DIC does not shard), cold-start pressure solves.
+    Halo exchanges: velocity (HALO planes) before advection and after it (for
+    the divergence's top w face), pressure (1 plane) before the correction;
+    the CG exchanges its own r halos inside cf_dcg.
+    """
+
+    def __init__(self, cfg, bounds, distributed: bool = False):
+        import torch.distributed as dist
+
+        if cfg.preconditioner != "jacobi":
+            raise ValueError("the z-slab solver shards Jacobi-PCG only (DIC's sweeps do not shard)")
+        if cfg.warm_start:
+            raise ValueError("warm_start is not supported by the z-slab solver")
+        lib = _lib.load_library()
+        self.cfg, self.n = cfg, cfg.n
+        self.bounds = [int(b) for b in bounds]
+        self.dist = distributed
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.slabs = [_SlabFields(self.n, self.bounds[k], self.bounds[k + 1], dev) for k in range(len(bounds) - 1)]
+        for s in self.slabs:
+            if s.nzl < HALO + 1:
+                raise ValueError(f"slab [{s.z0}, {s.z1}) is thinner than {HALO + 1} planes")
+        order = "sym" if cfg.variant == "optimized" else "csr"
+        if distributed:
+            self.rank, self.world = dist.get_rank(), dist.get_world_size()
+            obj = [nccl_unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            lo = self.rank - 1 if self.rank > 0 else -1
+            hi = self.rank + 1 if self.rank < self.world - 1 else -1
+            self.cg = SlabCG(self.n, self.n, self.n, cfg.h, order, bounds=self.bounds, nranks=self.world,
+                             rank=self.rank, uid=obj[0], lo_rank=lo, hi_rank=hi)
+        else:
+            self.rank, self.world = 0, 1
+            self.cg = SlabCG(self.n, self.n, self.n, cfg.h, order, bounds=self.bounds)
+        self.step_count = 0
+        self._lib = lib
+
+    # ------------------------------------------------------------ state I/O
+    def load_global(self, u, v, w, p=None):
+        """Scatter reference-layout global arrays (C order [i, j, k]) into the slabs."""
+        comps = [np.asarray(u), np.asarray(v), np.asarray(w)]
+        for s in self.slabs:
+            for c, arr in enumerate(comps):
+                k1 = s.z1 + (1 if (c == 2 and s.z1 == self.n) else 0)
+                blk = torch.as_tensor(np.ascontiguousarray(arr[:, :, s.z0:k1].transpose(2, 1, 0)))
+                s.planes(c, s.cur, s.z0, k1)[:, :, :arr.shape[0]].copy_(blk)
+            if p is not None:
+                pl = self.n * self.n
+                s.p_owned().copy_(torch.as_tensor(np.asarray(p)[s.z0 * pl:s.z1 * pl]))
+
+    def gather(self):
+        """Global reference-layout (u, v, w, p) of the local slabs (emulation: the whole cube)."""
+        n = self.n
+        out = [np.zeros((n + 1, n, n)), np.zeros((n, n + 1, n)), np.zeros((n, n, n + 1))]
+        p = np.zeros(n ** 3)
+        for s in self.slabs:
+            for c in range(3):
+                k1 = s.z1 + (1 if (c == 2 and s.z1 == n) else 0)
+                blk = s.planes(c, s.cur, s.z0, k1)[:, :, :out[c].shape[0]].cpu().numpy()
+                out[c][:, :, s.z0:k1] = blk.transpose(2, 1, 0)
+            p[s.z0 * n * n:s.z1 * n * n] = s.p_owned().cpu().numpy()
+        return out[0], out[1], out[2], p
+
+    # ------------------------------------------------------------ halos
+    def _exchange_vel(self, buf_attr="cur"):
+        """Velocity halo planes from the neighbouring slabs' owned planes."""
+        for a, b in zip(self.slabs, self.slabs[1:]):
+            ba, bb = getattr(a, buf_attr), getattr(b, buf_attr)
+            for c in range(3):
+                # a's hi halo <- b's owned [z, z + HALO (+1 for w)]
+                top = HALO + (1 if c == 2 else 0)
+                a.planes(c, ba, b.z0, b.z0 + top).copy_(b.planes(c, bb, b.z0, b.z0 + top))
+                # b's lo halo <- a's owned [z - HALO, z)
+                b.planes(c, bb, b.z0 - HALO, b.z0).copy_(a.planes(c, ba, b.z0 - HALO, b.z0))
+        if self.dist and self.world > 1:
+            self._exchange_vel_ranks(buf_attr)
+
+    def _exchange_vel_ranks(self, buf_attr):
+        import torch.distributed as dist
+
+        s = self.slabs[0]
+        buf = getattr(s, buf_attr)
+        ops = []
+        for c in range(3):
+            top = HALO + (1 if c == 2 else 0)
+            if self.rank > 0:
+                ops.append(dist.P2POp(dist.isend, s.planes(c, buf, s.z0, s.z0 + top).contiguous(), self.rank - 1))
+                ops.append(dist.P2POp(dist.irecv, s.planes(c, buf, s.z0 - HALO, s.z0), self.rank - 1))
+            if self.rank < self.world - 1:
+                ops.append(dist.P2POp(dist.isend, s.planes(c, buf, s.z1 - HALO, s.z1).contiguous(), self.rank + 1))
+                ops.append(dist.P2POp(dist.irecv, s.planes(c, buf, s.z1, s.z1 + top), self.rank + 1))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+    def _exchange_p(self):
+        pl = self.n * self.n
+        for a, b in zip(self.slabs, self.slabs[1:]):
+            a.p[pl * (a.nzl + 1):pl * (a.nzl + 2)].copy_(b.p[pl:2 * pl])
+            b.p[0:pl].copy_(a.p[pl * a.nzl:pl * (a.nzl + 1)])
+        if self.dist and self.world > 1:
+            import torch.distributed as dist
+
+            s = self.slabs[0]
+            ops = []
+            if self.rank > 0:
+                ops.append(dist.P2POp(dist.isend, s.p[pl:2 * pl], self.rank - 1))
+                ops.append(dist.P2POp(dist.irecv, s.p[0:pl], self.rank - 1))
+            if self.rank < self.world - 1:
+                ops.append(dist.P2POp(dist.isend, s.p[pl * s.nzl:pl * (s.nzl + 1)], self.rank + 1))
+                ops.append(dist.P2POp(dist.irecv, s.p[pl * (s.nzl + 1):pl * (s.nzl + 2)], self.rank + 1))
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+    def _max(self, vals):
+        m = max(vals)
+        if self.dist and self.world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([m], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            m = float(t.item())
+        return m
+
+    # ------------------------------------------------------------ the step
+    def step(self):
+        """Advance one time step; returns StepStats (src/sim.py:452-474)."""
+        from .sim import StepStats
+
+        cfg, n, lib, st = self.cfg, self.n, self._lib, _lib.stream()
+        for s in self.slabs:  # forces + walls (src/sim.py:134-149)
+            u, v, w = s.ptrs(s.cur)
+            _lib.check(lib.cf_forces_bc_slab(u, v, w, n, s.z0, s.z1, HALO, *s.ld, cfg.lid_accel * cfg.dt, 1, st),
+                       "forces_bc_slab")
+        self._exchange_vel()
+        # the HALO-plane halo covers a backtrace of <= 1 cell in z
+        wmax = []
+        for s in self.slabs:
+            r = ctypes.c_double()
+            w = s.vel[s.cur][2]
+            _lib.check(lib.cf_max_abs(w.data_ptr(), w.numel(), ctypes.byref(r), st), "max|w|")
+            wmax.append(r.value)
+        if self._max(wmax) * cfg.dt / cfg.h > HALO - 1:
+            raise ValueError("CFL in z exceeds the slab halo (max|w| dt/h > 1)")
+        for s in self.slabs:  # advection into the spare buffer (src/sim.py:259-289)
+            u, v, w = s.ptrs(s.cur)
+            nu, nv, nw = s.ptrs(1 - s.cur)
+            _lib.check(lib.cf_advect_slab(u, v, w, nu, nv, nw, n, s.z0, s.z1, HALO, *s.ld, cfg.h, cfg.dt, st),
+                       "advect_slab")
+            s.cur = 1 - s.cur
+        self._exchange_vel()  # the divergence reads the neighbour's first w face
+        maxb = []
+        for s in self.slabs:  # b = -(rho/dt) div (src/sim.py:359-360)
+            u, v, w = s.ptrs(s.cur)
+            mx = ctypes.c_double()
+            _lib.check(lib.cf_divergence_slab(u, v, w, n, s.z0, s.z1, HALO, *s.ld, cfg.h, -cfg.density / cfg.dt,
+                                              s.rhs.data_ptr(), ctypes.byref(mx), st), "divergence_slab")
+            maxb.append(mx.value)
+        div_pre = self._max(maxb) * cfg.dt / cfg.density
+        xs, stats = self.cg.solve([s.rhs for s in self.slabs], cfg.tol, cfg.max_iter, "jacobi")
+        for s, x in zip(self.slabs, xs):
+            s.p_owned().copy_(x)
+        self._exchange_p()
+        coef = cfg.dt / (cfg.density * cfg.h)
+        posts = []
+        for s in self.slabs:  # correction + div_post + walls (src/sim.py:426-449)
+            u, v, w = s.ptrs(s.cur)
+            nu, nv, nw = s.ptrs(1 - s.cur)
+            out = ctypes.c_double()
+            pl = n * n
+            _lib.check(lib.cf_pressure_correct_slab(u, v, w, nu, nv, nw, s.p.data_ptr() + 8 * pl, n, s.z0, s.z1,
+                                                    HALO, *s.ld, cfg.h, coef, ctypes.byref(out), st),
+                       "pressure_correct_slab")
+            posts.append(out.value)
+            s.cur = 1 - s.cur
+        div_post = self._max(posts)
+        self.step_count += 1
+        return StepStats(solve=stats, div_pre=div_pre, div_post=div_post)
+
+
 def init_slab_cg(n: int, h: float, order: str = "sym", nz: int | None = None) -> tuple:
     """Per-rank z-slab solver over torch.distributed (one GPU per rank).
     Returns (SlabCG, SlabDecomposition)."""

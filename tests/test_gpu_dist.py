@@ -66,6 +66,57 @@ def test_slabs_edge_cases(cuda):
     assert rel(x, xo) <= 1e-12
 
 
+@pytest.mark.parametrize("nslabs", [2, 3, 5])
+def test_slab_time_steps_match_single_domain(cuda, nslabs):
+    """Whole time steps (forces, advection with velocity halos, divergence,
+    z-slab CG, correction with pressure halos) on emulated slabs vs the
+    single-domain step.  Everything but the CG's reduction order is the same
+    per-element arithmetic, so at CG tol 1e-12 the fields agree to ~1e-10."""
+    from paper_2504_03697_b200.distributed import SlabSim
+    from paper_2504_03697_b200.parallel import SlabDecomposition
+
+    n = 32
+    kw = dict(n=n, h=1.0 / n, dt=0.01, t_end=0.03, tol=1e-12, max_iter=20000, variant="optimized",
+              preconditioner="jacobi")
+    cfg = cuda.SimConfig(**kw)
+    rng = np.random.default_rng(nslabs)
+    u0 = 0.5 * rng.standard_normal((n + 1, n, n))
+    v0 = 0.5 * rng.standard_normal((n, n + 1, n))
+    w0 = 0.5 * rng.standard_normal((n, n, n + 1))
+    u0[0] = u0[n] = 0.0
+    v0[:, 0] = v0[:, n] = 0.0
+    w0[:, :, 0] = w0[:, :, n] = 0.0
+    ref = cuda.initial_state(cfg)
+    ref.vel.load_host(u0, v0, w0)
+    cache = cuda.PoissonCache()
+    sim = SlabSim(cfg, SlabDecomposition.bounds(n, nslabs).tolist())
+    sim.load_global(u0, v0, w0)
+    for _ in range(cfg.num_steps):
+        a = cuda.step(ref, cfg, cache)
+        b = sim.step()
+        assert abs(a.solve.iterations - b.solve.iterations) <= 2
+        assert b.div_pre == pytest.approx(a.div_pre, rel=1e-12)
+        assert b.div_post == pytest.approx(a.div_post, rel=1e-4, abs=1e-12)
+    su, sv, sw, sp = sim.gather()
+    ru, rv, rw = ref.vel.numpy()
+    assert rel(np.concatenate([su.ravel(), sv.ravel(), sw.ravel()]),
+               np.concatenate([ru.ravel(), rv.ravel(), rw.ravel()])) <= 1e-10
+    assert rel(sp, ref.p.numpy()) <= 1e-9
+
+
+def test_slab_first_step_bitwise_before_solve(cuda):
+    """From rest the first step's advected field and RHS do not depend on the
+    CG: div_pre must be bit-identical across decompositions."""
+    from paper_2504_03697_b200.distributed import SlabSim
+
+    n = 32
+    cfg = cuda.SimConfig(n=n, h=1.0 / n, dt=0.01, t_end=0.01, tol=1e-8, max_iter=20000, variant="optimized",
+                         preconditioner="jacobi")
+    a = cuda.step(cuda.initial_state(cfg), cfg)
+    b = SlabSim(cfg, [0, 10, 21, 32]).step()
+    assert a.div_pre == b.div_pre
+
+
 def test_slabs_full_size(cuda):
     """256^3 split in 4 slabs: same iterations as the single-domain solve, true residual at tol."""
     from paper_2504_03697_b200.distributed import emulated_pcg
