@@ -115,6 +115,8 @@ struct cf_dcg {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_ms = 0.f;
     int batch = 8;
+    cudaGraphExec_t exec = nullptr;  // two captured iterations
+    int exec_key = -1;
 };
 
 namespace cf {
@@ -201,15 +203,47 @@ static int iteration(cf_dcg *ws, int half, double zc, cudaStream_t s)
     return exchange_r(ws, s);
 }
 
+// Two iterations (p buffers back to their original roles) captured once into
+// a CUDA graph -- kernels, D2D halo copies and the NCCL collectives alike --
+// then replayed; CF_DCG_GRAPH=0 launches them directly.
 template <int ORDER, int PK>
 static int solve_loop(cf_dcg *ws, double zc, cudaStream_t s)
 {
+    const char *ge = getenv("CF_DCG_GRAPH");
+    const bool use_graph = !(ge && atoi(ge) == 0);
+    const int key = ORDER * 4 + PK;
+    if (use_graph && (!ws->exec || ws->exec_key != key)) {
+        if (ws->exec) {
+            cudaGraphExecDestroy(ws->exec);
+            ws->exec = nullptr;
+        }
+        // capture on a private stream (the caller's may be the legacy default
+        // stream, which cannot be captured); the graph is launched on `s`
+        cudaGraph_t g;
+        cudaStream_t cs;
+        CF_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+        int rc = iteration<ORDER, PK>(ws, 0, zc, cs);
+        if (rc == CF_OK) rc = iteration<ORDER, PK>(ws, 1, zc, cs);
+        cudaError_t e = cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        if (rc != CF_OK) return rc;
+        CF_CUDA(e);
+        e = cudaGraphInstantiate(&ws->exec, g, 0);
+        cudaGraphDestroy(g);
+        CF_CUDA(e);
+        ws->exec_key = key;
+    }
     int half = 0;
     for (;;) {
-        for (int b = 0; b < ws->batch; ++b) {
-            int rc = iteration<ORDER, PK>(ws, half, zc, s);
-            if (rc != CF_OK) return rc;
-            half ^= 1;
+        for (int b = 0; b < ws->batch; b += 2) {
+            if (use_graph) {
+                CF_CUDA(cudaGraphLaunch(ws->exec, s));
+            } else {
+                int rc = iteration<ORDER, PK>(ws, half, zc, s);
+                if (rc == CF_OK) rc = iteration<ORDER, PK>(ws, half ^ 1, zc, s);
+                if (rc != CF_OK) return rc;
+            }
         }
         CF_CUDA(cudaMemcpyAsync(&ws->sc_host->done, &ws->sc->done, sizeof(int), cudaMemcpyDeviceToHost, s));
         CF_CUDA(cudaStreamSynchronize(s));
@@ -264,6 +298,7 @@ int cf_dcg_destroy(cf_dcg *ws)
     if (ws->red_sum) cudaFree(ws->red_sum);
     if (ws->ev0) cudaEventDestroy(ws->ev0);
     if (ws->ev1) cudaEventDestroy(ws->ev1);
+    if (ws->exec) cudaGraphExecDestroy(ws->exec);
     if (ws->comm) ncclCommDestroy(ws->comm);
     delete ws;
     return CF_OK;
