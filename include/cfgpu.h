@@ -193,6 +193,18 @@ int cf_divergence_slab(const double *u, const double *v, const double *w, int n,
 int cf_pressure_correct_slab(const double *u, const double *v, const double *w, double *nu, double *nv,
                              double *nw, const double *p, int n, int z0, int z1, int halo, int ldu, int ldv,
                              int ldw, double h, double coef, double *div_post_host, void *stream);
+/* Physics extension beyond the (inviscid) reference, SURVEY.md §8 f2:
+ * explicit viscous diffusion of every non-wall-normal face,
+ *   new = c + kdt*((((((xm + xp) + ym) + yp) + zm) + zp) - 6c),  kdt = nu*dt/h^2,
+ * tangential ghosts mirrored (free slip) or negated (no_slip), the lid
+ * (y = L) a Dirichlet wall when lid_dirichlet (ghost u = 2*lid_u - c,
+ * ghost w = -c).  Out of place.  Stable for kdt <= 1/6. */
+int cf_diffuse(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n,
+               int ldu, int ldv, int ldw, double kdt, double lid_u, int lid_dirichlet, int no_slip,
+               void *stream);
+int cf_diffuse_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
+                    int n, int z0, int z1, int halo, int ldu, int ldv, int ldw, double kdt, double lid_u,
+                    int lid_dirichlet, int no_slip, void *stream);
 /* Trilinear sample of all three components at one point (src/grid.py:124-142);
  * result (3 doubles) to out_host. */
 int cf_sample_velocity(const double *u, const double *v, const double *w, int n, int ldu,

@@ -254,6 +254,78 @@ __global__ void __launch_bounds__(kCellThreads) correct_kernel(Vel3 in, double *
     }
 }
 
+// Physics extension (the reference is inviscid): explicit
+// viscous diffusion of every non-wall-normal face,
+//   new = c + kdt * (((((( xm + xp) + ym) + yp) + zm) + zp) - 6*c),  kdt = nu*dt/h^2,
+// on the component's own lattice.  Neighbours across a wall are ghosts:
+// mirrored (+c, free slip) or antisymmetric (-c, no slip) for tangential
+// components; the lid (y = L) with a set velocity U is a Dirichlet wall:
+// ghost u = 2U - c, ghost w = -c.  Wall-normal faces stay zero.  The oracle
+// restates the same order (oracle/physics_ext.py).
+struct DiffBC {
+    double lid_u;
+    int lid_dirichlet, no_slip;
+};
+
+__device__ __forceinline__ double ghost(double c, bool anti) { return anti ? -c : c; }
+
+__global__ void __launch_bounds__(kFaceThreads) diffuse_kernel(Vel3 in, double *nu, double *nv, double *nw, SlabZ sz,
+                                                               double kdt, DiffBC bc)
+{
+    const int comp = blockIdx.y;
+    const int n = sz.n;
+    const Comp me = in.c[comp];
+    double *out = comp == 0 ? nu : (comp == 1 ? nv : nw);
+    const int kend = comp == 2 ? sz.w_end() : sz.z1;
+    const long long total = (long long)me.na * me.nb * (kend - sz.z0);
+    const long long stride = (long long)gridDim.x * kFaceThreads;
+    const bool ns = bc.no_slip != 0;
+    for (long long f = (long long)blockIdx.x * kFaceThreads + threadIdx.x; f < total; f += stride) {
+        const int i = (int)(f % me.na);
+        const long long rest = f / me.na;
+        const int j = (int)(rest % me.nb), k = sz.z0 + (int)(rest / me.nb);
+        double *dst = out + me.off(i, j, k);
+        const int wall = comp == 0 ? i : (comp == 1 ? j : k);
+        if (wall == 0 || wall == n) {
+            *dst = 0.0;
+            continue;
+        }
+        const double c = me.at(i, j, k);
+        // neighbours along the component's own axis always exist (walls are 0)
+        double xm, xp, ym, yp, zm, zp;
+        if (comp == 0) {
+            xm = me.at(i - 1, j, k);
+            xp = me.at(i + 1, j, k);
+        } else {
+            xm = i > 0 ? me.at(i - 1, j, k) : ghost(c, ns);
+            xp = i < n - 1 ? me.at(i + 1, j, k) : ghost(c, ns);
+        }
+        if (comp == 1) {
+            ym = me.at(i, j - 1, k);
+            yp = me.at(i, j + 1, k);
+        } else {
+            ym = j > 0 ? me.at(i, j - 1, k) : ghost(c, ns);
+            if (j < n - 1) yp = me.at(i, j + 1, k);
+            else if (bc.lid_dirichlet) yp = comp == 0 ? 2.0 * bc.lid_u - c : -c;
+            else yp = ghost(c, ns);
+        }
+        if (comp == 2) {
+            zm = me.at(i, j, k - 1);
+            zp = me.at(i, j, k + 1);
+        } else {
+            zm = k > 0 ? me.at(i, j, k - 1) : ghost(c, ns);
+            zp = k < n - 1 ? me.at(i, j, k + 1) : ghost(c, ns);
+        }
+        double s = xm + xp;
+        s = s + ym;
+        s = s + yp;
+        s = s + zm;
+        s = s + zp;
+        s = s - 6.0 * c;
+        *dst = c + kdt * s;
+    }
+}
+
 __global__ void sample_kernel(Vel3 in, double h, double px, double py, double pz, double *out)
 {
     // src/grid.py:124-142 with the lattice offsets of :99
@@ -407,6 +479,28 @@ int cf_pressure_correct_slab(const double *u, const double *v, const double *w, 
     CF_REQUIRE(nu != u && nv != v && nw != w, "cf_pressure_correct_slab: output aliases input");
     return cf::correct(u, v, w, nu, nv, nw, p, cf::SlabZ{n, z0, z1, halo}, ldu, ldv, ldw, h, coef, div_post_host,
                        stream);
+}
+
+int cf_diffuse_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n,
+                    int z0, int z1, int halo, int ldu, int ldv, int ldw, double kdt, double lid_u, int lid_dirichlet,
+                    int no_slip, void *stream)
+{
+    CF_REQUIRE(cf::slab_ok(n, z0, z1, halo) && cf::pitches_ok(n, ldu, ldv, ldw), "cf_diffuse: bad slab");
+    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_diffuse: output aliases input");
+    cf::SlabZ sz{n, z0, z1, halo};
+    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw, sz.k_base());
+    long long faces = (long long)(n + 1) * n * (z1 - z0 + 1);
+    dim3 grid(cf::grid_for(faces, cf::kFaceThreads, 8), 3);
+    cf::diffuse_kernel<<<grid, cf::kFaceThreads, 0, cf::as_stream(stream)>>>(in, nu, nv, nw, sz, kdt,
+                                                                              cf::DiffBC{lid_u, lid_dirichlet, no_slip});
+    CF_CHECK_LAUNCH("diffuse_kernel");
+    return CF_OK;
+}
+
+int cf_diffuse(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n, int ldu,
+               int ldv, int ldw, double kdt, double lid_u, int lid_dirichlet, int no_slip, void *stream)
+{
+    return cf_diffuse_slab(u, v, w, nu, nv, nw, n, 0, n, 0, ldu, ldv, ldw, kdt, lid_u, lid_dirichlet, no_slip, stream);
 }
 
 int cf_sample_velocity(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw, double h,

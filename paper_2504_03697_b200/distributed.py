@@ -296,7 +296,18 @@ class SlabSim:
             _lib.check(lib.cf_advect_slab(u, v, w, nu, nv, nw, n, s.z0, s.z1, HALO, *s.ld, cfg.h, cfg.dt, st),
                        "advect_slab")
             s.cur = 1 - s.cur
-        self._exchange_vel()  # the divergence reads the neighbour's first w face
+        self._exchange_vel()  # the divergence (and diffusion) read neighbour planes
+        if cfg.viscosity > 0.0:  # extension: explicit diffusion
+            kdt = cfg.viscosity * cfg.dt / (cfg.h * cfg.h)
+            lid = cfg.lid_velocity
+            for s in self.slabs:
+                u, v, w = s.ptrs(s.cur)
+                nu, nv, nw = s.ptrs(1 - s.cur)
+                _lib.check(lib.cf_diffuse_slab(u, v, w, nu, nv, nw, n, s.z0, s.z1, HALO, *s.ld, kdt,
+                                               0.0 if lid is None else float(lid), 0 if lid is None else 1,
+                                               1 if cfg.no_slip else 0, st), "diffuse_slab")
+                s.cur = 1 - s.cur
+            self._exchange_vel()
         maxb = []
         for s in self.slabs:  # b = -(rho/dt) div (src/sim.py:359-360)
             u, v, w = s.ptrs(s.cur)

@@ -57,8 +57,19 @@ class SimConfig:
     threads: int = 1
     advect_block: int = 8
     warm_start: bool = False
+    # --- physics extension beyond the (inviscid) reference, SURVEY.md §8 f2;
+    # the defaults reproduce the reference physics exactly
+    viscosity: float = 0.0               # kinematic nu: explicit diffusion after advection
+    lid_velocity: float | None = None    # Dirichlet lid u = U at y = L (via the diffusion ghosts)
+    no_slip: bool = False                # tangential ghosts negated on the walls
+    initial_pressure: float = 1.0        # the reference starts from p = 1 (dynamically inert)
 
     def __post_init__(self):
+        if self.viscosity < 0:
+            raise ValueError(f"viscosity must be >= 0, got {self.viscosity}")
+        if self.viscosity > 0 and self.viscosity * self.dt / (self.h * self.h) > 1.0 / 6.0:
+            raise ValueError(
+                f"explicit diffusion is unstable: nu*dt/h^2 = {self.viscosity * self.dt / self.h ** 2:.3f} > 1/6")
         if self.n < 2:
             raise ValueError(f"n must be >= 2, got {self.n}")
         if not self.dt > 0:
@@ -116,7 +127,7 @@ def initial_state(cfg: SimConfig) -> SimState:
     """Fluid at rest under uniform unit pressure (src/sim.py:126-131)."""
     spec = cfg.spec
     p = ScalarField(spec)
-    p.data.fill_(1.0)
+    p.data.fill_(cfg.initial_pressure)
     return SimState(vel=VelocityField(spec), p=p)
 
 
@@ -149,6 +160,23 @@ def _advect_into(src: VelocityField, dst: VelocityField, cfg: SimConfig):
     nu, nv, nw = dst.ptrs()
     _lib.check(lib.cf_advect(u, v, w, nu, nv, nw, n, lu, lv, lw, src.spec.h, cfg.dt, _lib.stream()),
                "advect")
+
+
+def _diffuse_into(src: VelocityField, dst: VelocityField, cfg: SimConfig):
+    lib = _lib.load_library()
+    u, v, w, n, lu, lv, lw = _vel_args(src)
+    nu, nv, nw = dst.ptrs()
+    kdt = cfg.viscosity * cfg.dt / (cfg.h * cfg.h)
+    lid = cfg.lid_velocity
+    _lib.check(lib.cf_diffuse(u, v, w, nu, nv, nw, n, lu, lv, lw, kdt, 0.0 if lid is None else float(lid),
+                              0 if lid is None else 1, 1 if cfg.no_slip else 0, _lib.stream()), "diffuse")
+
+
+def solve_diffusion(state: SimState, cfg: SimConfig) -> VelocityField:
+    """Extension: one explicit viscous diffusion step into a new field."""
+    new = VelocityField(state.vel.spec)
+    _diffuse_into(state.vel, new, cfg)
+    return new
 
 
 def solve_advection(state: SimState, cfg: SimConfig, pool=None) -> VelocityField:
@@ -311,6 +339,11 @@ def step(state: SimState, cfg: SimConfig, cache: PoissonCache | None = None, poo
         new = cache.spare_field(spec)
         _advect_into(state.vel, new, cfg)  # wall planes zeroed in-kernel
         cache.spare, state.vel = state.vel, new
+    if cfg.viscosity > 0.0:  # extension: explicit diffusion
+        with prof.region("solveDiffusion"):
+            new = cache.spare_field(spec)
+            _diffuse_into(state.vel, new, cfg)
+            cache.spare, state.vel = state.vel, new
     with prof.region("solvePressureCorrection"):
         p, stats, div_pre = solve_pressure_correction(state, cfg, cache, pool, prof)
     with prof.region("applyPressureCorrection"):

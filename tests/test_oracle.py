@@ -145,3 +145,26 @@ def test_known_answers():
     assert st.iterations == 0 and st.converged and not x.any()
     with pytest.raises(orc.Breakdown):
         orc.pcg(lambda v, o: np.dot(-np.eye(4), v, out=o), np.ones(4))
+
+
+def test_extension_diffusion_known_answers():
+    """The extension's restatement (oracle/physics_ext.py): a unit spike spreads
+    kdt to its six neighbours and keeps 1 - 6 kdt; a uniform tangential field is
+    invariant under mirror ghosts away from the normal walls; the moving lid
+    pulls u towards U."""
+    from oracle import physics_ext as ext
+
+    n, kdt = 6, 0.1
+    u = np.zeros((n + 1, n, n)); v = np.zeros((n, n + 1, n)); w = np.zeros((n, n, n + 1))
+    u[3, 2, 2] = 1.0
+    nu, nv, nw = ext.diffuse(u, v, w, n, kdt)
+    assert nu[3, 2, 2] == 1.0 - 6 * kdt
+    for d in ((1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)):
+        assert nu[3 + d[0], 2 + d[1], 2 + d[2]] == kdt
+    assert not nv.any() and not nw.any()
+    v[:] = 0.7
+    v[:, 0] = v[:, n] = 0.0
+    _, nv, _ = ext.diffuse(u * 0, v, w, n, kdt)
+    assert np.allclose(nv[:, 2:n - 1], 0.7, rtol=0, atol=1e-15)
+    nu, _, _ = ext.diffuse(u * 0, v * 0, w, n, kdt, lid_u=1.0, no_slip=True)
+    assert np.all(nu[1:n, n - 1, :] == kdt * 2.0)
