@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcfgpu.so")
+LIB_PATH = os.environ.get("CF_LIB", os.path.join(_HERE, "libcfgpu.so"))  # CF_LIB: tuning experiments only
 
 CF_OK = 0
 CF_BREAKDOWN = 1

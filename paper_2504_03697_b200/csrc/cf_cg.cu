@@ -291,11 +291,11 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
         double *p_new = ws->p[half ^ 1];
         if (PK != PK_JVEC && ws->tma) {
             const TmaGeom &gd = ws->geom_dir, &gu = ws->geom_upd;
-            cg_dir_tma<ORDER, PK><<<gd.ntx * gd.nty * gd.nchunk, kPThreads, kDirSmem, s>>>(
+            cg_dir_tma<ORDER, PK><<<gd.ntx * gd.nty * gd.nchunk, kWSThreads, kDirSmem, s>>>(
                 PK == PK_ZVEC ? ws->m_z : ws->m_r, ws->m_p[half], gd, ws->off, ws->diag, p_new, zc, ws->sc,
                 ws->partials, ws->tk, nullptr);
             CF_CHECK_LAUNCH("cg_dir_tma");
-            cg_update_tma<ORDER, PK><<<gu.ntx * gu.nty * gu.nchunk, kPThreads, kUpdSmem, s>>>(
+            cg_update_tma<ORDER, PK><<<gu.ntx * gu.nty * gu.nchunk, kWSThreads, kUpdSmem, s>>>(
                 ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc,
                 ws->partials, ws->tk, use_cond, cond, nullptr);
             CF_CHECK_LAUNCH("cg_update_tma");
@@ -449,8 +449,8 @@ static void set_grids(cf_cg *ws)
         cudaFuncSetAttribute(cg_update_tma<ORDER, PK_JCONST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kUpdSmem);
         cudaFuncSetAttribute(cg_update_tma<ORDER, PK_ZVEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bd, cg_dir_tma<ORDER, PK_JCONST>, kPThreads, kDirSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, cg_update_tma<ORDER, PK_JCONST>, kPThreads, kUpdSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bd, cg_dir_tma<ORDER, PK_JCONST>, kWSThreads, kDirSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, cg_update_tma<ORDER, PK_JCONST>, kWSThreads, kUpdSmem);
         ws->geom_dir = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bd > 0 ? bd : 1);
         ws->geom_upd = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bu > 0 ? bu : 1);
         if (const char *e = getenv("CF_TMA_CHUNKS_DIR")) ws->geom_dir.nchunk = atoi(e) > 0 ? atoi(e) : 1;

@@ -183,7 +183,7 @@ static int iteration(cf_dcg *ws, int half, double zc, cudaStream_t s)
     for (size_t k = 0; k < ws->slabs.size(); ++k) {
         Slab &sb = ws->slabs[k];
         const TmaGeom &g = sb.gd;
-        cg_dir_tma<ORDER, PK><<<g.ntx * g.nty * g.nchunk, kPThreads, kDirSmem, s>>>(
+        cg_dir_tma<ORDER, PK><<<g.ntx * g.nty * g.nchunk, kWSThreads, kDirSmem, s>>>(
             sb.m_r, sb.m_p[half], g, ws->off, ws->diag, sb.p[half ^ 1], zc, ws->sc, sb.partials, sb.tk,
             ws->red + 2 * k);
         CF_CHECK_LAUNCH("cg_dir_tma (slab)");
@@ -193,7 +193,7 @@ static int iteration(cf_dcg *ws, int half, double zc, cudaStream_t s)
     for (size_t k = 0; k < ws->slabs.size(); ++k) {
         Slab &sb = ws->slabs[k];
         const TmaGeom &g = sb.gu;
-        cg_update_tma<ORDER, PK><<<g.ntx * g.nty * g.nchunk, kPThreads, kUpdSmem, s>>>(
+        cg_update_tma<ORDER, PK><<<g.ntx * g.nty * g.nchunk, kWSThreads, kUpdSmem, s>>>(
             sb.m_p[half ^ 1], sb.m_ri, sb.m_xi, g, ws->off, ws->diag, sb.r, sb.x, zc, ws->sc, sb.partials, sb.tk, 0,
             0, ws->red + 2 * k);
         CF_CHECK_LAUNCH("cg_update_tma (slab)");
@@ -265,8 +265,8 @@ static void set_smem_attrs()
 template <int ORDER>
 static void occupancy(int *bd, int *bu)
 {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(bd, cg_dir_tma<ORDER, PK_JCONST>, kPThreads, kDirSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(bu, cg_update_tma<ORDER, PK_JCONST>, kPThreads, kUpdSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(bd, cg_dir_tma<ORDER, PK_JCONST>, kWSThreads, kDirSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(bu, cg_update_tma<ORDER, PK_JCONST>, kWSThreads, kUpdSmem);
 }
 
 }  // namespace cf

@@ -27,7 +27,7 @@ constexpr int kTThreads = kTTX * kTTY;  // 512
 // starts two cells early and is 36 wide), y from y0-1, 18 tall.  Box origins
 // are clamped at 0: negative coordinates trap as well.
 constexpr int kHX = kTTX + 4, kHY = kTTY + 2;
-constexpr int kStages = 4;
+constexpr int kStages = 3;  // measured 3/4/6: depth is not the limiter; 3 frees smem
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -53,6 +53,11 @@ __device__ __forceinline__ void fence_barrier_init()
 __device__ __forceinline__ void fence_proxy_async_smem()
 {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)

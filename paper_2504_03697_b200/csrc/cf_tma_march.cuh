@@ -156,4 +156,98 @@ __device__ __forceinline__ void staged_pair_march(const TmaGeom &g, double off, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised form: warps 0..7 consume (one cell pair per thread as
+// above), warp 8 is the TMA producer.  Each stage slot has a `full` barrier
+// (TMA transaction bytes) and an `empty` barrier (one arrival per consumer
+// warp, after a proxy fence), so consumer warps never wait for each other --
+// there is no block-wide barrier inside the plane loop.
+constexpr int kConsumerWarps = kPThreads / 32;
+constexpr int kWSThreads = kPThreads + 32;
+
+__device__ __forceinline__ void init_ws_bars(uint64_t *full, uint64_t *empty)
+{
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+}
+
+// Producer loop (run by one elected lane of warp 8).
+template <class Issue>
+__device__ __forceinline__ void ws_produce(int nplanes, uint64_t *full, uint64_t *empty, Issue issue)
+{
+    for (int q = 0; q < nplanes; ++q) {
+        const int s = q % kStages;
+        if (q >= kStages) mbar_wait(&empty[s], (uint32_t)(((q / kStages) - 1) & 1));
+        issue(q, s, &full[s]);
+    }
+}
+
+// Consumer: this warp is done with slot q.
+__device__ __forceinline__ void ws_release(uint64_t *empty, int q)
+{
+    fence_proxy_async_smem();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[q % kStages]);
+}
+
+// Consumer march over the block's planes.  Pol: value(slot, offset) ->
+// operand at a box offset (may compute it), box geometry as in
+// staged_pair_march; epi(slot, m, z, centre pair, a0, a1).
+template <int ORDER, class Pol>
+__device__ __forceinline__ void ws_consume(const TmaGeom &g, const MarchCoords &m, double off, double diag, Pol &pol,
+                                           uint64_t *full, uint64_t *empty)
+{
+    const bool hxl = m.i > 0, hxr = m.i + 2 < g.nx, hym = m.j > 0, hyp = m.j < g.ny - 1;
+    const bool inplane_fast = hxl && hxr && hym && hyp;
+    auto wait = [&](int q) { mbar_wait(&full[q % kStages], (uint32_t)((q / kStages) & 1)); };
+    int q = 0;
+    double2 cprev = make_double2(0.0, 0.0);
+    wait(0);
+    if (m.zs < m.z0) {
+        cprev = pol.value2(0, m.o);
+        pol.halo(m, m.zs, cprev);
+        ws_release(empty, 0);
+        q = 1;
+        wait(1);
+    }
+    double2 ccur = pol.value2(q % kStages, m.o);
+    const double2 zero = make_double2(0.0, 0.0);
+    for (int z = m.z0; z < m.z1; ++z, ++q) {
+        const bool hzm = z - 1 >= m.zlo, hzp = z + 1 <= m.zhi;
+        double2 cnext = zero;
+        if (hzp) {
+            wait(q + 1);
+            cnext = pol.value2((q + 1) % kStages, m.o);
+            if (z + 1 == m.z1) pol.halo(m, z + 1, cnext);
+        }
+        const int s = q % kStages;
+        if (m.valid) {
+            double a0, a1;
+            if (inplane_fast && hzm && hzp) {
+                stencil_pair<ORDER, true>(ccur, pol.value(s, m.o - 1), pol.value(s, m.o + 2),
+                                          pol.value2(s, m.o - kHX), pol.value2(s, m.o + kHX), cprev, cnext, true,
+                                          true, true, true, true, true, off, diag, a0, a1);
+            } else {
+                stencil_pair<ORDER, false>(ccur, hxl ? pol.value(s, m.o - 1) : 0.0,
+                                           hxr ? pol.value(s, m.o + 2) : 0.0,
+                                           hym ? pol.value2(s, m.o - kHX) : zero,
+                                           hyp ? pol.value2(s, m.o + kHX) : zero, cprev, cnext, hxl, hxr, hym, hyp,
+                                           hzm, hzp, off, diag, a0, a1);
+            }
+            pol.epi(s, m, z, ccur, a0, a1);
+        }
+        ws_release(empty, q);
+        cprev = ccur;
+        ccur = cnext;
+    }
+    // the last staged plane (z1, read as cnext) is released too
+    if (q < m.nplanes) ws_release(empty, q);
+}
+
 }  // namespace cf
