@@ -247,6 +247,97 @@ __global__ void __launch_bounds__(kMarchThreads) cg_rz_kernel(long long n, const
 
 #include "cf_cg_tma.cuh"
 
+// ---------------------------------------------------------------- small grids
+// Whole solve in ONE block: r, p, x live in shared memory (16^3: 96 KB), the
+// two grid-wide reductions per iteration become block reductions, and a
+// solve is a single launch -- the latency-bound regime of BASELINE config 1,
+// where the grid kernels cost ~19 us per iteration in launch/sync overhead.
+// Same per-element arithmetic and stop rule as the fused grid kernels.
+constexpr int kSmallThreads = 1024;
+constexpr long long kSmallMaxCells = 5120;  // 3 vectors <= 120 KB of shared memory
+
+template <int ORDER>
+__device__ __forceinline__ double small_ap(const double *v, int c, const Box &bx, double off, double diag)
+{
+    const int nx = bx.nx, ny = bx.ny;
+    const int i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+    const int pl = nx * ny;
+    const bool hxm = i > 0, hxp = i < nx - 1, hym = j > 0, hyp = j < ny - 1, hzm = k > 0, hzp = k < bx.nz - 1;
+    return stencil7<ORDER>(v[c], hxm ? v[c - 1] : 0.0, hxp ? v[c + 1] : 0.0, hym ? v[c - nx] : 0.0,
+                           hyp ? v[c + nx] : 0.0, hzm ? v[c - pl] : 0.0, hzp ? v[c + pl] : 0.0, hxm, hxp, hym, hyp,
+                           hzm, hzp, off, diag);
+}
+
+template <int ORDER, int PK>
+__global__ void __launch_bounds__(kSmallThreads) cg_small_kernel(Box bx, double off, double diag,
+                                                                 const double *__restrict__ b,
+                                                                 const double *__restrict__ x0, double *__restrict__ xout,
+                                                                 const double *__restrict__ jd, double zc, CgScalars *sc)
+{
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    __shared__ double bc[2];
+    const int n = (int)bx.cells();
+    double *r = sm, *p = sm + n, *x = sm + 2 * n;
+    const int t = threadIdx.x;
+    // r = b (or b - A x0), x = 0 (or x0); |b|^2 and r.z  (src/solver.py:60-61, :130-143)
+    for (int c = t; c < n; c += kSmallThreads) x[c] = x0 ? x0[c] : 0.0;
+    __syncthreads();
+    double bb = 0.0, rz = 0.0;
+    for (int c = t; c < n; c += kSmallThreads) {
+        const double bi = b[c];
+        const double rn = x0 ? bi + -1.0 * small_ap<ORDER>(x, c, bx, off, diag) : bi;
+        r[c] = rn;
+        bb = bb + bi * bi;
+        rz = rz + rn * zval<PK>(rn, jd, c, zc);
+    }
+    bb = block_sum<kSmallThreads>(bb, red);
+    rz = block_sum<kSmallThreads>(rz, red);
+    if (t == 0) {
+        bc[0] = bb;
+        bc[1] = rz;
+    }
+    __syncthreads();
+    CgScalars s = *sc;  // tol, max_iter from the host
+    scalar_after_init(&s, bc[0], bc[1]);
+    while (!s.done) {
+        // p = z + beta p (in place: each element depends on itself only)
+        for (int c = t; c < n; c += kSmallThreads) {
+            const double z = zval<PK>(r[c], jd, c, zc);
+            p[c] = s.it == 0 ? z : z + s.beta * p[c];
+        }
+        __syncthreads();
+        double pap = 0.0;
+        for (int c = t; c < n; c += kSmallThreads) pap = pap + p[c] * small_ap<ORDER>(p, c, bx, off, diag);
+        pap = block_sum<kSmallThreads>(pap, red);
+        if (t == 0) bc[0] = pap;
+        __syncthreads();
+        scalar_after_dir(&s, bc[0]);
+        if (s.done) break;
+        const double alpha = s.alpha, malpha = -alpha;
+        double rr = 0.0;
+        rz = 0.0;
+        for (int c = t; c < n; c += kSmallThreads) {
+            const double pc = p[c];
+            x[c] = x[c] + alpha * pc;
+            const double rn = r[c] + malpha * small_ap<ORDER>(p, c, bx, off, diag);
+            r[c] = rn;
+            rr = rr + rn * rn;
+            rz = rz + rn * zval<PK>(rn, jd, c, zc);
+        }
+        rr = block_sum<kSmallThreads>(rr, red);
+        rz = block_sum<kSmallThreads>(rz, red);
+        if (t == 0) {
+            bc[0] = rr;
+            bc[1] = rz;
+        }
+        __syncthreads();
+        scalar_after_update<true>(&s, bc[0], bc[1]);
+    }
+    for (int c = t; c < n; c += kSmallThreads) xout[c] = x[c];
+    if (t == 0) *sc = s;
+}
+
 }  // namespace cf
 
 // ---------------------------------------------------------------- workspace
@@ -381,6 +472,17 @@ static int launch_init(cf_cg *ws, const double *b, const double *x0, double zc, 
 template <int ORDER, int PK>
 static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, cudaStream_t s)
 {
+    const char *ns = getenv("CF_NO_SMALL");
+    if (PK != PK_ZVEC && ws->n <= kSmallMaxCells && !(ns && atoi(ns) > 0)) {
+        const size_t smem = 3 * (size_t)ws->n * sizeof(double);
+        CF_CUDA(cudaFuncSetAttribute(cg_small_kernel<ORDER, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CF_CUDA(cudaEventRecord(ws->ev0, s));
+        cg_small_kernel<ORDER, PK><<<1, kSmallThreads, smem, s>>>(ws->bx, ws->off, ws->diag, b, x0, ws->x, ws->jd, zc,
+                                                                  ws->sc);
+        CF_CHECK_LAUNCH("cg_small_kernel");
+        CF_CUDA(cudaEventRecord(ws->ev1, s));
+        return CF_OK;
+    }
     int rc = launch_init<ORDER, PK>(ws, b, x0, zc, s);
     if (rc != CF_OK) return rc;
     if (ws->direct) {

@@ -5,8 +5,72 @@
 //   * the matrix-free 7-point stencil (cf_stencil.cuh), 16 B/cell of HBM
 //     traffic against 12*nnz/N + 20 B/cell for CSR.
 #include "cf_stencil.cuh"
+#include "cf_tma_march.cuh"
 
 namespace cf {
+
+// y = A x through the warp-specialised TMA march (halo boxes of x staged by a
+// producer warp; the consumer warps' stencil reads shared memory only).
+struct ApplyPolicy {
+    const double *sx;
+    double *y;  // at (i, j) of plane 0
+    long long plane;
+    __device__ __forceinline__ double2 value2(int s, int o) const { return ld2(sx + s * kBoxStride + o); }
+    __device__ __forceinline__ double value(int s, int o) const { return sx[s * kBoxStride + o]; }
+    __device__ __forceinline__ void epi(int, const MarchCoords &, int z, double2, double a0, double a1)
+    {
+        st2(y + plane * z, a0, a1);
+    }
+    __device__ __forceinline__ void halo(const MarchCoords &, int, double2) {}
+};
+
+template <int ORDER>
+__global__ void __launch_bounds__(kWSThreads) stencil_apply_tma(const __grid_constant__ CUtensorMap mx, TmaGeom g,
+                                                                double off, double diag, double *__restrict__ y)
+{
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    double *const sx = aligned_smem(smem_raw);
+    const MarchCoords m = march_coords(g);
+    const long long plane = (long long)g.nx * g.ny;
+    ApplyPolicy pol{sx, y + m.i + (long long)g.nx * m.j, plane};
+    init_ws_bars(full, empty);
+    if (threadIdx.x >= kPThreads) {
+        if (threadIdx.x == kPThreads) {
+            prefetch_map(&mx);
+            ws_produce(m.nplanes, full, empty, [&](int q, int s, uint64_t *bar) {
+                mbar_expect_tx(bar, kBoxBytes);
+                tma_load_3d(sx + s * kBoxStride, &mx, m.bx0, m.by0, m.zs + q + g.lo_halo, bar);
+            });
+        }
+    } else {
+        ws_consume<ORDER>(g, m, off, diag, pol, full, empty);
+    }
+}
+
+constexpr size_t kApplySmem = kStages * kBoxStride * sizeof(double) + 128;
+
+template <int ORDER>
+static int stencil_apply_tma_launch(int nx, int ny, int nz, double off, double diag, const double *x, double *y,
+                                    cudaStream_t s, bool *used)
+{
+    *used = false;
+    if (nx < 32 || nx % 2 != 0) return CF_OK;
+    CUtensorMap map;
+    if (!make_map(&map, x, nx, ny, nz, kHX, kHY)) return CF_OK;
+    static bool attr[2] = {false, false};
+    if (!attr[ORDER]) {
+        cudaFuncSetAttribute(stencil_apply_tma<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem);
+        attr[ORDER] = true;
+    }
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, stencil_apply_tma<ORDER>, kWSThreads, kApplySmem);
+    TmaGeom g = tma_geom(nx, ny, nz, 0, 0, b > 0 ? b : 1);
+    stencil_apply_tma<ORDER><<<g.ntx * g.nty * g.nchunk, kWSThreads, kApplySmem, s>>>(map, g, off, diag, y);
+    CF_CHECK_LAUNCH("stencil_apply_tma");
+    *used = true;
+    return CF_OK;
+}
 
 constexpr int kRowThreads = 256;
 
@@ -103,6 +167,11 @@ int cf_stencil7_apply(int nx, int ny, int nz, double h, int order, const double 
     // the same literals the reference assembles (src/sim.py:303-304)
     const double off = -1.0 / (h * h), diag = 6.0 / (h * h);
     cudaStream_t s = cf::as_stream(stream);
+    bool used = false;
+    int rc = order == CF_ORDER_CSR
+                 ? cf::stencil_apply_tma_launch<CF_ORDER_CSR>(nx, ny, nz, off, diag, x, y, s, &used)
+                 : cf::stencil_apply_tma_launch<CF_ORDER_SYM>(nx, ny, nz, off, diag, x, y, s, &used);
+    if (rc != CF_OK || used) return rc;
     if (order == CF_ORDER_CSR) {
         auto k = cf::stencil_apply_kernel<CF_ORDER_CSR>;
         k<<<cf::march_grid((const void *)k, bx), cf::kMarchThreads, 0, s>>>(bx, off, diag, x, y);
