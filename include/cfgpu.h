@@ -205,6 +205,13 @@ int cf_diffuse(const double *u, const double *v, const double *w, double *nu, do
 int cf_diffuse_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
                     int n, int z0, int z1, int halo, int ldu, int ldv, int ldw, double kdt, double lid_u,
                     int lid_dirichlet, int no_slip, void *stream);
+/* Implicit (backward-Euler) diffusion operator of one component (comp 0/1/2
+ * = u/v/w) on its physical padded array (row pitch ld): (I - kdt L) with the
+ * ghost rules of cf_diffuse folded into the diagonal and, for the moving lid,
+ * the right-hand side.  mode 0: y = A x; mode 1: y = diag(A); mode 2: y = the
+ * right-hand side for x = u*.  Fixed faces and padding are identity rows. */
+int cf_helmholtz(int mode, int comp, const double *x, double *y, int n, int ld, double kdt, double lid_u,
+                 int lid_dirichlet, int no_slip, void *stream);
 /* Trilinear sample of all three components at one point (src/grid.py:124-142);
  * result (3 doubles) to out_host. */
 int cf_sample_velocity(const double *u, const double *v, const double *w, int n, int ldu,

@@ -77,11 +77,71 @@ def diffuse(u, v, w, n, kdt, lid_u=None, no_slip=False):
     return tuple(out)
 
 
+def helmholtz_apply(comp, x, n, kdt, lid_u=None, no_slip=False):
+    """(I - kdt L) x for one component array (reference C-order layout).
+    Ghosts fold into the diagonal (+1 mirror / -1 negate; the moving lid is a
+    -1); along the component's own axis the wall faces are fixed zeros (no
+    term).  Wall-normal faces are identity rows."""
+    g = -1.0 if no_slip else 1.0
+    shape = x.shape
+    idx = np.indices(shape)
+    s = np.zeros_like(x)
+    gsum = np.zeros_like(x)
+    for axis in range(3):
+        pos = idx[axis]
+        hi_lim = shape[axis] - 1
+        if axis == comp:  # own axis: real neighbours only between the walls
+            has_m, has_p = pos > 1, pos < hi_lim - 1
+        else:
+            has_m, has_p = pos > 0, pos < hi_lim
+        xm = np.zeros_like(x)
+        xp = np.zeros_like(x)
+        sl_lo = [slice(None)] * 3
+        sl_hi = [slice(None)] * 3
+        sl_lo[axis], sl_hi[axis] = slice(1, None), slice(None, -1)
+        xm[tuple(sl_lo)] = x[tuple(sl_hi)]
+        xp[tuple(sl_hi)] = x[tuple(sl_lo)]
+        s = s + np.where(has_m, xm, 0.0) + np.where(has_p, xp, 0.0)
+        if axis != comp:
+            gsum = gsum + np.where(has_m, 0.0, g)
+            if axis == 1 and lid_u is not None:
+                gsum = gsum + np.where(has_p, 0.0, -1.0)
+            else:
+                gsum = gsum + np.where(has_p, 0.0, g)
+    y = (1.0 + kdt * (6.0 - gsum)) * x - kdt * s
+    wall = idx[comp]
+    fixed = (wall == 0) | (wall == shape[comp] - 1)
+    return np.where(fixed, x, y), np.where(fixed, 1.0, 1.0 + kdt * (6.0 - gsum))
+
+
+def diffuse_implicit(u, v, w, n, kdt, lid_u=None, no_slip=False, tol=1e-10):
+    """Backward Euler per component with the oracle's Jacobi-PCG (src/solver.py)."""
+    from . import Jacobi, pcg
+
+    out = []
+    for comp, a in enumerate((u, v, w)):
+        shape = a.shape
+
+        def op(vec, o, comp=comp, shape=shape):
+            o[:] = helmholtz_apply(comp, vec.reshape(shape), n, kdt, lid_u, no_slip)[0].ravel()
+            return o
+
+        _, dia = helmholtz_apply(comp, a, n, kdt, lid_u, no_slip)
+        b = a.copy()
+        if lid_u is not None and comp == 0:
+            b[1:n, n - 1, :] += kdt * (2.0 * lid_u)
+        x, _ = pcg(op, b.ravel(), x0=a.ravel(), precond=Jacobi(dia.ravel()), tol=tol, max_iter=10000)
+        out.append(x.reshape(shape))
+    return tuple(out)
+
+
 @dataclass
 class ExtCfg(Cfg):
     viscosity: float = 0.0
     lid_velocity: float | None = None
     no_slip: bool = False
+    diffusion: str = "explicit"
+    diffusion_tol: float = 1e-10
 
 
 def step(s, cfg: ExtCfg, cache=None) -> StepResult:
@@ -92,7 +152,11 @@ def step(s, cfg: ExtCfg, cache=None) -> StepResult:
     enforce_boundaries(s)
     if cfg.viscosity > 0.0:
         kdt = cfg.viscosity * cfg.dt / (cfg.h * cfg.h)
-        s.u, s.v, s.w = diffuse(s.u, s.v, s.w, cfg.n, kdt, cfg.lid_velocity, cfg.no_slip)
+        if cfg.diffusion == "implicit":
+            s.u, s.v, s.w = diffuse_implicit(s.u, s.v, s.w, cfg.n, kdt, cfg.lid_velocity, cfg.no_slip,
+                                             cfg.diffusion_tol)
+        else:
+            s.u, s.v, s.w = diffuse(s.u, s.v, s.w, cfg.n, kdt, cfg.lid_velocity, cfg.no_slip)
     st, div_pre = solve_pressure(s, cfg, cache)
     div_post = correct(s, cfg)
     enforce_boundaries(s)

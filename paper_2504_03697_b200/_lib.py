@@ -79,6 +79,7 @@ _SIGNATURES = {
                            _int),
     "cf_pressure_correct_slab": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _int, _dbl,
                                   _dbl, _pd, _vp], _int),
+    "cf_helmholtz": ([_int, _int, _vp, _vp, _int, _int, _dbl, _dbl, _int, _int, _vp], _int),
     "cf_diffuse": ([_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _int, _int, _vp], _int),
     "cf_diffuse_slab": ([_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _int, _dbl, _dbl, _int,
                          _int, _vp], _int),

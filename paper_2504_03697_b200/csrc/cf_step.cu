@@ -326,6 +326,71 @@ __global__ void __launch_bounds__(kFaceThreads) diffuse_kernel(Vel3 in, double *
     }
 }
 
+// Implicit (backward-Euler) diffusion of one component: (I - kdt L) u = u*,
+// L the same ghost-aware Laplacian as diffuse_kernel.  A mirrored ghost (+c)
+// or negated ghost (-c) folds into the diagonal, the lid's Dirichlet ghost
+// 2U - c folds +kdt*c into the diagonal and 2U*kdt into the right-hand side.
+// Unknowns are the component's physical (padded) array; wall-normal faces and
+// row padding are identity rows with a zero right-hand side.
+// MODE 0: y = A x   MODE 1: y = diag(A)   MODE 2: y = rhs from x = u*
+template <int MODE>
+__global__ void __launch_bounds__(kFaceThreads) helmholtz_kernel(const double *__restrict__ xin, double *__restrict__ y,
+                                                                 int comp, int n, int ld, double kdt, DiffBC bc)
+{
+    const int na = n + (comp == 0), nb = n + (comp == 1), nc = n + (comp == 2);
+    const long long total = (long long)ld * nb * nc;
+    const long long stride = (long long)gridDim.x * kFaceThreads;
+    const bool ns = bc.no_slip != 0;
+    const long long pj = ld, pk = (long long)ld * nb;
+    for (long long f = (long long)blockIdx.x * kFaceThreads + threadIdx.x; f < total; f += stride) {
+        const int i = (int)(f % ld);
+        const long long rest = f / ld;
+        const int j = (int)(rest % nb), k = (int)(rest / nb);
+        const int wall = comp == 0 ? i : (comp == 1 ? j : k);
+        if (i >= na || wall == 0 || wall == n) {  // fixed faces, padding: identity
+            y[f] = MODE == 1 ? 1.0 : (MODE == 0 ? xin[f] : 0.0);
+            continue;
+        }
+        // Along the component's own axis a missing neighbour is a fixed wall
+        // face (value 0: no term, keeps A symmetric); across the other axes it
+        // is a ghost folded into the diagonal (+1 mirror, -1 negate).
+        const double g = ns ? -1.0 : 1.0;
+        double gsum = 0.0;  // sum of ghost coefficients multiplying c
+        double lid = 0.0;   // Dirichlet lid contribution to the rhs
+        const bool ex_xm = comp == 0 ? i > 1 : i > 0, ex_xp = i < n - 1;
+        const bool ex_ym = comp == 1 ? j > 1 : j > 0, ex_yp = j < n - 1;
+        const bool ex_zm = comp == 2 ? k > 1 : k > 0, ex_zp = k < n - 1;
+        if (comp != 0 && !ex_xm) gsum += g;
+        if (comp != 0 && !ex_xp) gsum += g;
+        if (comp != 1 && !ex_ym) gsum += g;
+        if (comp != 1 && !ex_yp) {
+            if (bc.lid_dirichlet) {
+                gsum += -1.0;
+                if (comp == 0) lid = 2.0 * bc.lid_u;
+            } else {
+                gsum += g;
+            }
+        }
+        if (comp != 2 && !ex_zm) gsum += g;
+        if (comp != 2 && !ex_zp) gsum += g;
+        const double dia = 1.0 + kdt * (6.0 - gsum);
+        if (MODE == 1) {
+            y[f] = dia;
+        } else if (MODE == 2) {
+            y[f] = xin[f] + kdt * lid;
+        } else {
+            double s = 0.0;
+            if (ex_xm) s = s + xin[f - 1];
+            if (ex_xp) s = s + xin[f + 1];
+            if (ex_ym) s = s + xin[f - pj];
+            if (ex_yp) s = s + xin[f + pj];
+            if (ex_zm) s = s + xin[f - pk];
+            if (ex_zp) s = s + xin[f + pk];
+            y[f] = dia * xin[f] - kdt * s;
+        }
+    }
+}
+
 __global__ void sample_kernel(Vel3 in, double h, double px, double py, double pz, double *out)
 {
     // src/grid.py:124-142 with the lattice offsets of :99
@@ -494,6 +559,22 @@ int cf_diffuse_slab(const double *u, const double *v, const double *w, double *n
     cf::diffuse_kernel<<<grid, cf::kFaceThreads, 0, cf::as_stream(stream)>>>(in, nu, nv, nw, sz, kdt,
                                                                               cf::DiffBC{lid_u, lid_dirichlet, no_slip});
     CF_CHECK_LAUNCH("diffuse_kernel");
+    return CF_OK;
+}
+
+int cf_helmholtz(int mode, int comp, const double *x, double *y, int n, int ld, double kdt, double lid_u,
+                 int lid_dirichlet, int no_slip, void *stream)
+{
+    CF_REQUIRE(n >= 1 && comp >= 0 && comp <= 2 && mode >= 0 && mode <= 2 && ld >= n + (comp == 0),
+               "cf_helmholtz: bad arguments");
+    long long total = (long long)ld * (n + (comp == 1)) * (n + (comp == 2));
+    int grid = cf::grid_for(total, cf::kFaceThreads, 8);
+    cf::DiffBC bc{lid_u, lid_dirichlet, no_slip};
+    cudaStream_t s = cf::as_stream(stream);
+    if (mode == 0) cf::helmholtz_kernel<0><<<grid, cf::kFaceThreads, 0, s>>>(x, y, comp, n, ld, kdt, bc);
+    else if (mode == 1) cf::helmholtz_kernel<1><<<grid, cf::kFaceThreads, 0, s>>>(x, y, comp, n, ld, kdt, bc);
+    else cf::helmholtz_kernel<2><<<grid, cf::kFaceThreads, 0, s>>>(x, y, comp, n, ld, kdt, bc);
+    CF_CHECK_LAUNCH("helmholtz_kernel");
     return CF_OK;
 }
 

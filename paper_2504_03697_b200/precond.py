@@ -31,8 +31,10 @@ class JacobiPreconditioner:
     def __init__(self, inv_diag):
         self.inv_diag, _ = as_device(inv_diag)
         self.inv_diag = self.inv_diag.contiguous()
-        host = to_host(self.inv_diag)
-        self.constant = float(host[0]) if len(host) and np.all(host == host[0]) else None
+        # constant diagonal (the cavity operator) -> the fused CG forms z in registers
+        n = self.inv_diag.shape[0]
+        first = self.inv_diag[:1]
+        self.constant = (float(first.item()) if n and bool(torch.all(self.inv_diag == first).item()) else None)
 
     @property
     def n(self) -> int:

@@ -63,13 +63,19 @@ class SimConfig:
     lid_velocity: float | None = None    # Dirichlet lid u = U at y = L (via the diffusion ghosts)
     no_slip: bool = False                # tangential ghosts negated on the walls
     initial_pressure: float = 1.0        # the reference starts from p = 1 (dynamically inert)
+    diffusion: str = "explicit"          # "explicit" | "implicit" (backward Euler, CG per component)
+    diffusion_tol: float = 1e-10
 
     def __post_init__(self):
         if self.viscosity < 0:
             raise ValueError(f"viscosity must be >= 0, got {self.viscosity}")
-        if self.viscosity > 0 and self.viscosity * self.dt / (self.h * self.h) > 1.0 / 6.0:
+        if self.diffusion not in ("explicit", "implicit"):
+            raise ValueError("diffusion must be 'explicit' or 'implicit'")
+        if (self.diffusion == "explicit" and self.viscosity > 0
+                and self.viscosity * self.dt / (self.h * self.h) > 1.0 / 6.0):
             raise ValueError(
-                f"explicit diffusion is unstable: nu*dt/h^2 = {self.viscosity * self.dt / self.h ** 2:.3f} > 1/6")
+                f"explicit diffusion is unstable: nu*dt/h^2 = {self.viscosity * self.dt / self.h ** 2:.3f} > 1/6 "
+                "(use diffusion='implicit')")
         if self.n < 2:
             raise ValueError(f"n must be >= 2, got {self.n}")
         if not self.dt > 0:
@@ -172,8 +178,58 @@ def _diffuse_into(src: VelocityField, dst: VelocityField, cfg: SimConfig):
                               0 if lid is None else 1, 1 if cfg.no_slip else 0, _lib.stream()), "diffuse")
 
 
+class HelmholtzOperator:
+    """(I - kdt L) for one velocity component on its physical padded array
+    (cf_helmholtz); an ``apply_a`` for pcg's per-op path."""
+
+    def __init__(self, comp: int, n: int, ld: int, kdt: float, lid_velocity, no_slip: bool):
+        self.comp, self.n, self.ld, self.kdt = comp, n, ld, float(kdt)
+        self.lid = 0.0 if lid_velocity is None else float(lid_velocity)
+        self.dirichlet = 0 if lid_velocity is None else 1
+        self.no_slip = 1 if no_slip else 0
+
+    def _run(self, mode, x, y):
+        lib = _lib.load_library()
+        _lib.check(lib.cf_helmholtz(mode, self.comp, x.data_ptr() if x is not None else None, y.data_ptr(), self.n,
+                                    self.ld, self.kdt, self.lid, self.dirichlet, self.no_slip, _lib.stream()),
+                   "helmholtz")
+        return y
+
+    def __call__(self, x, out=None):
+        return self._run(0, x, torch.empty_like(x) if out is None else out)
+
+    def diagonal_tensor(self, like):
+        return self._run(1, like, torch.empty_like(like))
+
+    def rhs(self, ustar):
+        return self._run(2, ustar, torch.empty_like(ustar))
+
+
+def _diffuse_implicit(vel: VelocityField, cfg: SimConfig):
+    """Backward-Euler diffusion in place: per component (I - kdt L) u = u*,
+    Jacobi-PCG on the device (per-op path), warm-started from u*."""
+    from .precond import JacobiPreconditioner
+
+    kdt = cfg.viscosity * cfg.dt / (cfg.h * cfg.h)
+    stats = []
+    for comp, phys in enumerate(vel._phys):
+        flat = phys.view(-1)
+        op = HelmholtzOperator(comp, cfg.n, vel.ld[comp], kdt, cfg.lid_velocity, cfg.no_slip)
+        b = op.rhs(flat)
+        pre = JacobiPreconditioner(1.0 / op.diagonal_tensor(flat))
+        x, st = pcg(op, b, x0=flat, precond=pre, tol=cfg.diffusion_tol, max_iter=10000, variant="optimized")
+        flat.copy_(x)
+        stats.append(st)
+    return stats
+
+
 def solve_diffusion(state: SimState, cfg: SimConfig) -> VelocityField:
-    """Extension: one explicit viscous diffusion step into a new field."""
+    """Extension: one viscous diffusion step into a new field
+    (explicit, or backward Euler when cfg.diffusion == 'implicit')."""
+    if cfg.diffusion == "implicit":
+        new = state.vel.copy()
+        _diffuse_implicit(new, cfg)
+        return new
     new = VelocityField(state.vel.spec)
     _diffuse_into(state.vel, new, cfg)
     return new
@@ -339,11 +395,14 @@ def step(state: SimState, cfg: SimConfig, cache: PoissonCache | None = None, poo
         new = cache.spare_field(spec)
         _advect_into(state.vel, new, cfg)  # wall planes zeroed in-kernel
         cache.spare, state.vel = state.vel, new
-    if cfg.viscosity > 0.0:  # extension: explicit diffusion
+    if cfg.viscosity > 0.0:  # extension: viscous diffusion
         with prof.region("solveDiffusion"):
-            new = cache.spare_field(spec)
-            _diffuse_into(state.vel, new, cfg)
-            cache.spare, state.vel = state.vel, new
+            if cfg.diffusion == "implicit":
+                _diffuse_implicit(state.vel, cfg)
+            else:
+                new = cache.spare_field(spec)
+                _diffuse_into(state.vel, new, cfg)
+                cache.spare, state.vel = state.vel, new
     with prof.region("solvePressureCorrection"):
         p, stats, div_pre = solve_pressure_correction(state, cfg, cache, pool, prof)
     with prof.region("applyPressureCorrection"):

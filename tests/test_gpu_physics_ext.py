@@ -94,3 +94,44 @@ def test_slab_run_with_extension_physics(cuda):
     ru, rv, rw = ref.vel.numpy()
     assert rel(np.concatenate([su.ravel(), sv.ravel(), sw.ravel()]),
                np.concatenate([ru.ravel(), rv.ravel(), rw.ravel()])) <= 1e-10
+
+
+@pytest.mark.parametrize("lid,no_slip", [(None, False), (1.0, True)])
+def test_implicit_diffusion_vs_restatement(cuda, lid, no_slip):
+    """Backward-Euler diffusion (CG per component, device per-op path) against
+    the oracle's restatement, both solved to tol 1e-12: rel-L2 <= 1e-9."""
+    from paper_2504_03697_b200.sim import solve_diffusion
+
+    n = 12
+    u, v, w = random_field(n, 5)
+    nu = 0.3 * (1.0 / n) ** 2 / 0.01  # nu*dt/h^2 = 0.3 > 1/6: explicit would be unstable
+    cfg = cuda.SimConfig(n=n, h=1.0 / n, dt=0.01, t_end=0.0, viscosity=nu, lid_velocity=lid, no_slip=no_slip,
+                         diffusion="implicit", diffusion_tol=1e-12)
+    st = cuda.SimState(vel=cuda.VelocityField(cfg.spec, u, v, w), p=cuda.ScalarField(cfg.spec))
+    got = solve_diffusion(st, cfg).numpy()
+    want = ext.diffuse_implicit(u, v, w, n, 0.3, lid, no_slip, tol=1e-12)
+    for g, wv in zip(got, want):
+        assert rel(g, wv) <= 1e-9
+
+
+def test_config5_ratio_implicit_run(cuda):
+    """Config-5 diffusion number (nu*dt/h^2 = 0.262) on a 32^3 run: implicit
+    diffusion, lid velocity, no-slip; matches the restatement step by step."""
+    n = 32
+    h, dt = 1.0 / n, 0.01
+    nu = 0.262 * h * h / dt
+    kw = dict(n=n, h=h, dt=dt, t_end=0.02, tol=1e-8, max_iter=20000, variant="optimized",
+              preconditioner="jacobi", lid_accel=0.0)
+    ekw = dict(viscosity=nu, lid_velocity=1.0, no_slip=True, diffusion="implicit", diffusion_tol=1e-12)
+    cfg = cuda.SimConfig(**kw, **ekw)
+    st = cuda.initial_state(cfg)
+    cache = cuda.PoissonCache()
+    ost = orc.initial_state(n)
+    ocfg = ext.ExtCfg(**kw, **ekw)
+    for _ in range(cfg.num_steps):
+        a = cuda.step(st, cfg, cache)
+        b = ext.step(ost, ocfg, orc.Cache())
+        assert abs(a.solve.iterations - b.solve.iterations) <= 2
+    u, v, w = st.vel.numpy()
+    assert rel(np.concatenate([u.ravel(), v.ravel(), w.ravel()]),
+               np.concatenate([ost.u.ravel(), ost.v.ravel(), ost.w.ravel()])) <= 1e-8

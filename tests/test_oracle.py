@@ -168,3 +168,34 @@ def test_extension_diffusion_known_answers():
     assert np.allclose(nv[:, 2:n - 1], 0.7, rtol=0, atol=1e-15)
     nu, _, _ = ext.diffuse(u * 0, v * 0, w, n, kdt, lid_u=1.0, no_slip=True)
     assert np.all(nu[1:n, n - 1, :] == kdt * 2.0)
+
+
+def test_extension_implicit_diffusion_restatement():
+    """Backward-Euler operator of the extension: symmetric (CG-safe), and the
+    solve satisfies (I - kdt L) u = u* (+ lid term); for small kdt it agrees
+    with the explicit step to O(kdt^2)."""
+    from oracle import physics_ext as ext
+
+    n, kdt = 6, 0.3
+    rng = np.random.default_rng(2)
+    for comp, shape in enumerate(((n + 1, n, n), (n, n + 1, n), (n, n, n + 1))):
+        a, b = rng.standard_normal(shape), rng.standard_normal(shape)
+        for arr in (a, b):  # wall-normal faces are fixed zeros
+            sl = [slice(None)] * 3
+            sl[comp] = 0
+            arr[tuple(sl)] = 0.0
+            sl[comp] = -1
+            arr[tuple(sl)] = 0.0
+        for lid, ns in ((None, False), (1.0, True)):
+            Aa = ext.helmholtz_apply(comp, a, n, kdt, lid, ns)[0]
+            Ab = ext.helmholtz_apply(comp, b, n, kdt, lid, ns)[0]
+            assert abs(np.sum(b * Aa) - np.sum(a * Ab)) <= 1e-12 * np.abs(np.sum(b * Aa))
+    u = 0.1 * rng.standard_normal((n + 1, n, n)); u[0] = u[n] = 0
+    v = 0.1 * rng.standard_normal((n, n + 1, n)); v[:, 0] = v[:, n] = 0
+    w = 0.1 * rng.standard_normal((n, n, n + 1)); w[:, :, 0] = w[:, :, n] = 0
+    iu, iv, iw = ext.diffuse_implicit(u, v, w, n, 1e-3, 1.0, True, tol=1e-13)
+    eu, ev, ew = ext.diffuse(u, v, w, n, 1e-3, 1.0, True)
+    assert np.abs(iu - eu).max() <= 1e-4 and np.abs(iw - ew).max() <= 1e-4
+    r = ext.helmholtz_apply(0, iu, n, 1e-3, 1.0, True)[0]
+    want = u.copy(); want[1:n, n - 1, :] += 1e-3 * 2.0
+    assert np.abs(r - want).max() <= 1e-11

@@ -1,6 +1,7 @@
 // Calibration tool: HBM throughput of simple fp64 kernels on this GPU.
 //  copy (double2 grid-stride), naive 7-point stencil (one thread per cell).
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 __global__ void copy2(const double2 *__restrict__ a, double2 *__restrict__ b, long long n2) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) b[i] = a[i];
@@ -18,8 +19,8 @@ __global__ void stencil_naive(const double *__restrict__ x, double *__restrict__
   if (i > 0) s += off * __ldg(x + c - 1);
   y[c] = s;
 }
-int main() {
-  const int n = 256; const long long N = (long long)n * n * n;
+int main(int argc, char **argv) {
+  const int n = argc > 1 ? atoi(argv[1]) : 256; const long long N = (long long)n * n * n;
   double *x, *y; cudaMalloc(&x, N * 8); cudaMalloc(&y, N * 8); cudaMemset(x, 0, N * 8);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b); float ms;
   for (int g : {148 * 4, 148 * 8, 148 * 16, 148 * 32}) {
@@ -29,7 +30,7 @@ int main() {
     printf("copy grid=%d: %.1f us %.0f GB/s\n", g, ms / 20 * 1e3, 16.0 * N / (ms / 20 * 1e-3) / 1e9);
   }
   for (int by : {4, 8}) {
-    dim3 blk(64, by), grd(n / 64, n / by, n);
+    dim3 blk(64, by), grd((n + 63) / 64, (n + by - 1) / by, n);
     for (int w = 0; w < 3; ++w) stencil_naive<<<grd, blk>>>(x, y, n, -1.0, 6.0);
     cudaEventRecord(a); for (int r = 0; r < 20; ++r) stencil_naive<<<grd, blk>>>(x, y, n, -1.0, 6.0); cudaEventRecord(b);
     cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
