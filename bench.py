@@ -134,7 +134,7 @@ def run_reference(args, rank):
     import oracle as orc
 
     threads = os.cpu_count() or 1
-    n = args.n
+    n = args.grid
     a = orc.poisson_sym(n, 1.0 / n)
     b = np.random.default_rng(0).uniform(-1, 1, n ** 3)
     pre = orc.jacobi_from(a)
@@ -184,7 +184,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     cf.load_library()
-    n = args.n
+    n = args.grid
     cfg = cf.SimConfig(n=n, h=1.0 / n, dt=args.dt, t_end=args.dt * (args.warmup + 2 * args.steps), tol=1e-8,
                        max_iter=20000, variant="optimized", preconditioner="jacobi")
     stream = torch.cuda.current_stream()
@@ -194,7 +194,7 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    if world > 1:
+    if world > 1 or args.force_slabs:
         return run_slabs(args, cfg, rank, world, local_rank, barrier)
     state = cf.initial_state(cfg)
     cache = cf.PoissonCache()
@@ -381,18 +381,21 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--grid", type=int, default=256)
     ap.add_argument("--dt", type=float, default=0.002)
     ap.add_argument("--cpu-iters", type=int, default=40)
     ap.add_argument("--ref-iters", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-slabs", action="store_true",
+                    help="run the z-slab/NCCL path even on one rank (plumbing check)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank)
-    if world > 1:
+    use_pg = world > 1 or args.force_slabs
+    if use_pg:
         import torch
         import torch.distributed as dist
 
@@ -401,7 +404,7 @@ def main():
     try:
         return run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if use_pg:
             import torch.distributed as dist
 
             dist.destroy_process_group()
