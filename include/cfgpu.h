@@ -175,43 +175,45 @@ int cf_divergence(const double *u, const double *v, const double *w, int n, int 
 int cf_pressure_correct(const double *u, const double *v, const double *w, double *nu, double *nv,
                         double *nw, const double *p, int n, int ldu, int ldv, int ldw, double h,
                         double coef, double *div_post_host, void *stream);
-/* z-slab forms of the four step kernels (multi-GPU): the
- * slab owns global planes [z0, z1) of the n-cube and its velocity arrays hold
- * planes z0-halo .. (u, v: z1+halo-1; w: z1+halo), pointers at the first
- * stored plane; scalar arrays (out, p) are slab-local with plane 0 = z0 and,
- * for p, readable halo planes -1 / z1-z0 where neighbours exist.  Owned w
- * faces are [z0, z1) plus face n on the last slab.  With z0 = 0, z1 = n,
- * halo = 0 they are the single-domain kernels above. */
-int cf_forces_bc_slab(double *u, double *v, double *w, int n, int z0, int z1, int halo, int ldu, int ldv,
-                      int ldw, double lid_dv, int apply_lid, void *stream);
+/* Box (nx x ny x nz; the reference's cube is nx = ny = nz = n, other boxes
+ * are the SURVEY.md §8 f2 extension) and z-slab forms of the step kernels
+ * (multi-GPU): the slab owns global planes [z0, z1) of nz and
+ * its velocity arrays hold planes z0-halo .. (u, v: z1+halo-1; w: z1+halo),
+ * pointers at the first stored plane; scalar arrays (out, p) are slab-local
+ * with plane 0 = z0 and, for p, readable halo planes -1 / z1-z0 where
+ * neighbours exist.  Owned w faces are [z0, z1) plus face nz on the last
+ * slab.  z0 = 0, z1 = nz, halo = 0 is the whole box. */
+int cf_forces_bc_slab(double *u, double *v, double *w, int nx, int ny, int nz, int z0, int z1, int halo,
+                      int ldu, int ldv, int ldw, double lid_dv, int apply_lid, void *stream);
 int cf_advect_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
-                   int n, int z0, int z1, int halo, int ldu, int ldv, int ldw, double h, double dt,
-                   void *stream);
-int cf_divergence_slab(const double *u, const double *v, const double *w, int n, int z0, int z1, int halo,
-                       int ldu, int ldv, int ldw, double h, double scale, double *out, double *maxabs_host,
-                       void *stream);
+                   int nx, int ny, int nz, int z0, int z1, int halo, int ldu, int ldv, int ldw, double h,
+                   double dt, void *stream);
+int cf_divergence_slab(const double *u, const double *v, const double *w, int nx, int ny, int nz, int z0,
+                       int z1, int halo, int ldu, int ldv, int ldw, double h, double scale, double *out,
+                       double *maxabs_host, void *stream);
 int cf_pressure_correct_slab(const double *u, const double *v, const double *w, double *nu, double *nv,
-                             double *nw, const double *p, int n, int z0, int z1, int halo, int ldu, int ldv,
-                             int ldw, double h, double coef, double *div_post_host, void *stream);
+                             double *nw, const double *p, int nx, int ny, int nz, int z0, int z1, int halo,
+                             int ldu, int ldv, int ldw, double h, double coef, double *div_post_host,
+                             void *stream);
 /* Physics extension beyond the (inviscid) reference, SURVEY.md §8 f2:
  * explicit viscous diffusion of every non-wall-normal face,
  *   new = c + kdt*((((((xm + xp) + ym) + yp) + zm) + zp) - 6c),  kdt = nu*dt/h^2,
  * tangential ghosts mirrored (free slip) or negated (no_slip), the lid
- * (y = L) a Dirichlet wall when lid_dirichlet (ghost u = 2*lid_u - c,
+ * (y = Ly) a Dirichlet wall when lid_dirichlet (ghost u = 2*lid_u - c,
  * ghost w = -c).  Out of place.  Stable for kdt <= 1/6. */
 int cf_diffuse(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n,
                int ldu, int ldv, int ldw, double kdt, double lid_u, int lid_dirichlet, int no_slip,
                void *stream);
 int cf_diffuse_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
-                    int n, int z0, int z1, int halo, int ldu, int ldv, int ldw, double kdt, double lid_u,
-                    int lid_dirichlet, int no_slip, void *stream);
+                    int nx, int ny, int nz, int z0, int z1, int halo, int ldu, int ldv, int ldw, double kdt,
+                    double lid_u, int lid_dirichlet, int no_slip, void *stream);
 /* Implicit (backward-Euler) diffusion operator of one component (comp 0/1/2
  * = u/v/w) on its physical padded array (row pitch ld): (I - kdt L) with the
  * ghost rules of cf_diffuse folded into the diagonal and, for the moving lid,
  * the right-hand side.  mode 0: y = A x; mode 1: y = diag(A); mode 2: y = the
  * right-hand side for x = u*.  Fixed faces and padding are identity rows. */
-int cf_helmholtz(int mode, int comp, const double *x, double *y, int n, int ld, double kdt, double lid_u,
-                 int lid_dirichlet, int no_slip, void *stream);
+int cf_helmholtz(int mode, int comp, const double *x, double *y, int nx, int ny, int nz, int ld, double kdt,
+                 double lid_u, int lid_dirichlet, int no_slip, void *stream);
 /* Trilinear sample of all three components at one point (src/grid.py:124-142);
  * result (3 doubles) to out_host. */
 int cf_sample_velocity(const double *u, const double *v, const double *w, int n, int ldu,

@@ -56,9 +56,10 @@ def lib():
         L.orc_dic_diag.argtypes = [_ip, _ip, _dp, _dp, _dp, ctypes.c_int64]
         L.orc_dic_diag.restype = ctypes.c_int64
         L.orc_dic_apply.argtypes = [_ip, _ip, _dp, _ip, _ip, _dp, _dp, _dp, _dp, _dp, ctypes.c_int64]
-        L.orc_advect.argtypes = [_dp, _dp, _dp, _dp, ctypes.c_int, ctypes.c_int64,
-                                 ctypes.c_double, ctypes.c_double, ctypes.c_double, _ip, ctypes.c_int]
-        L.orc_divergence.argtypes = [_dp, _dp, _dp, ctypes.c_int64, ctypes.c_double, _dp, ctypes.c_int]
+        L.orc_advect.argtypes = [_dp, _dp, _dp, _dp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                 ctypes.c_int64, ctypes.c_double, ctypes.c_double, _ip, ctypes.c_int]
+        L.orc_divergence.argtypes = [_dp, _dp, _dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_double, _dp, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -123,35 +124,44 @@ class SymCsr:
         self.t_perm = order.astype(np.int64)
 
 
-def _cell_ijk(n: int):
-    idx = np.arange(n ** 3, dtype=np.int64)
-    return idx, idx % n, (idx // n) % n, idx // (n * n)
+def _cell_ijk(nx: int, ny: int, nz: int):
+    idx = np.arange(nx * ny * nz, dtype=np.int64)
+    return idx, idx % nx, (idx // nx) % ny, idx // (nx * ny)
 
 
-def poisson_csr(n: int, h: float) -> Csr:
-    """src/sim.py:296-317 -- full CSR, columns ascending (k-1,j-1,i-1,d,i+1,j+1,k+1)."""
-    idx, i, j, k = _cell_ijk(n)
-    nn = n * n
-    cand = np.stack([idx - nn, idx - n, idx - 1, idx, idx + 1, idx + n, idx + nn], axis=1)
-    keep = np.stack([k > 0, j > 0, i > 0, np.ones_like(i, dtype=bool), i < n - 1, j < n - 1,
-                     k < n - 1], axis=1)
+def _box(n, shape):
+    return tuple(shape) if shape is not None else (n, n, n)
+
+
+def poisson_csr(n: int, h: float, shape=None) -> Csr:
+    """src/sim.py:296-317 -- full CSR, columns ascending (k-1,j-1,i-1,d,i+1,j+1,k+1).
+    ``shape`` (extension): an nx*ny*nz box instead of the cube."""
+    nx, ny, nz = _box(n, shape)
+    idx, i, j, k = _cell_ijk(nx, ny, nz)
+    pl = nx * ny
+    cand = np.stack([idx - pl, idx - nx, idx - 1, idx, idx + 1, idx + nx, idx + pl], axis=1)
+    keep = np.stack([k > 0, j > 0, i > 0, np.ones_like(i, dtype=bool), i < nx - 1, j < ny - 1,
+                     k < nz - 1], axis=1)
     vals = np.full(cand.shape, -1.0 / (h * h))
     vals[:, 3] = 6.0 / (h * h)
     row_ptr = np.concatenate(([0], np.cumsum(keep.sum(axis=1)))).astype(np.int64)
     m = keep.ravel()
-    return Csr(n ** 3, n ** 3, row_ptr, np.ascontiguousarray(cand.ravel()[m]),
+    num = nx * ny * nz
+    return Csr(num, num, row_ptr, np.ascontiguousarray(cand.ravel()[m]),
                np.ascontiguousarray(vals.ravel()[m]))
 
 
-def poisson_sym(n: int, h: float) -> SymCsr:
+def poisson_sym(n: int, h: float, shape=None) -> SymCsr:
     """src/sim.py:320-333 -- diagonal plus strict upper (i+1, j+1, k+1)."""
-    idx, i, j, k = _cell_ijk(n)
-    cand = np.stack([idx + 1, idx + n, idx + n * n], axis=1)
-    keep = np.stack([i < n - 1, j < n - 1, k < n - 1], axis=1)
+    nx, ny, nz = _box(n, shape)
+    idx, i, j, k = _cell_ijk(nx, ny, nz)
+    cand = np.stack([idx + 1, idx + nx, idx + nx * ny], axis=1)
+    keep = np.stack([i < nx - 1, j < ny - 1, k < nz - 1], axis=1)
     vals = np.full(cand.shape, -1.0 / (h * h))
     row_ptr = np.concatenate(([0], np.cumsum(keep.sum(axis=1)))).astype(np.int64)
     m = keep.ravel()
-    return SymCsr(n ** 3, np.full(n ** 3, 6.0 / (h * h)), row_ptr,
+    num = nx * ny * nz
+    return SymCsr(num, np.full(num, 6.0 / (h * h)), row_ptr,
                   np.ascontiguousarray(cand.ravel()[m]), np.ascontiguousarray(vals.ravel()[m]))
 
 
@@ -338,10 +348,15 @@ class Cfg:
     variant: str = "baseline"
     threads: int = 1
     warm_start: bool = False
+    shape: tuple | None = None  # extension: an nx*ny*nz box (the reference is the n-cube)
 
     @property
     def num_steps(self) -> int:
         return round(self.t_end / self.dt)
+
+    @property
+    def box(self):
+        return _box(self.n, self.shape)
 
 
 @dataclass
@@ -361,16 +376,17 @@ class StepResult:
     div_post: float
 
 
-def initial_state(n: int) -> State:
+def initial_state(n: int, shape=None) -> State:
     """src/sim.py:126-131 -- rest under unit pressure."""
-    return State(np.zeros((n + 1, n, n)), np.zeros((n, n + 1, n)), np.zeros((n, n, n + 1)),
-                 np.ones(n ** 3))
+    nx, ny, nz = _box(n, shape)
+    return State(np.zeros((nx + 1, ny, nz)), np.zeros((nx, ny + 1, nz)), np.zeros((nx, ny, nz + 1)),
+                 np.ones(nx * ny * nz))
 
 
 def apply_forces(s: State, cfg: Cfg) -> None:
     """src/sim.py:134-137 -- lid offset on the top-layer u faces."""
-    n = cfg.n
-    s.u[1:n, n - 1, :] += cfg.lid_accel * cfg.dt
+    nx, ny, _ = cfg.box
+    s.u[1:nx, ny - 1, :] += cfg.lid_accel * cfg.dt
 
 
 def enforce_boundaries(s: State) -> None:
@@ -381,27 +397,29 @@ def enforce_boundaries(s: State) -> None:
 
 
 def advect(u, v, w, n: int, h: float, dt: float, threads: int = 1):
-    """src/sim.py:259-289 -- new (u, v, w) with wall-normal planes zeroed."""
+    """src/sim.py:259-289 -- new (u, v, w) with wall-normal planes zeroed.
+    (The box extents come from the arrays; n is kept for the reference call shape.)"""
     u, v, w = (np.ascontiguousarray(a, dtype=np.float64) for a in (u, v, w))
+    nx, ny, nz = u.shape[0] - 1, u.shape[1], u.shape[2]
     outs = []
-    for comp, shape in enumerate(((n + 1, n, n), (n, n + 1, n), (n, n, n + 1))):
+    for comp, shape in enumerate(((nx + 1, ny, nz), (nx, ny + 1, nz), (nx, ny, nz + 1))):
         out = np.empty(shape)
         b = chunk_bounds(out.size, threads)
-        lib().orc_advect(_d(u), _d(v), _d(w), _d(out), comp, n, h, dt, n * h, _i(b), len(b) - 1)
+        lib().orc_advect(_d(u), _d(v), _d(w), _d(out), comp, nx, ny, nz, h, dt, _i(b), len(b) - 1)
         outs.append(out)
     nu, nv, nw = outs
-    nu[0], nu[n] = 0.0, 0.0
-    nv[:, 0], nv[:, n] = 0.0, 0.0
-    nw[:, :, 0], nw[:, :, n] = 0.0, 0.0
+    nu[0], nu[nx] = 0.0, 0.0
+    nv[:, 0], nv[:, ny] = 0.0, 0.0
+    nw[:, :, 0], nw[:, :, nz] = 0.0, 0.0
     return nu, nv, nw
 
 
 def divergence(u, v, w, h: float, threads: int = 1) -> np.ndarray:
     """src/grid.py:145-154 -- flat, i fastest."""
-    n = u.shape[1]
-    out = np.empty(n ** 3)
+    nx, ny, nz = u.shape[0] - 1, u.shape[1], u.shape[2]
+    out = np.empty(nx * ny * nz)
     lib().orc_divergence(_d(np.ascontiguousarray(u)), _d(np.ascontiguousarray(v)),
-                         _d(np.ascontiguousarray(w)), n, h, _d(out), threads)
+                         _d(np.ascontiguousarray(w)), nx, ny, nz, h, _d(out), threads)
     return out
 
 
@@ -417,11 +435,11 @@ def assemble(s: State, cfg: Cfg, cache: Cache | None = None):
     b = (-cfg.density / cfg.dt) * divergence(s.u, s.v, s.w, cfg.h, cfg.threads)
     if cfg.variant == "optimized":
         if cache is None:
-            return poisson_sym(cfg.n, cfg.h), b
+            return poisson_sym(cfg.n, cfg.h, cfg.shape), b
         if cache.matrix is None:
-            cache.matrix = poisson_sym(cfg.n, cfg.h)
+            cache.matrix = poisson_sym(cfg.n, cfg.h, cfg.shape)
         return cache.matrix, b
-    return poisson_csr(cfg.n, cfg.h), b
+    return poisson_csr(cfg.n, cfg.h, cfg.shape), b
 
 
 def solve_pressure(s: State, cfg: Cfg, cache: Cache | None = None, max_count=None):
@@ -444,18 +462,18 @@ def solve_pressure(s: State, cfg: Cfg, cache: Cache | None = None, max_count=Non
 
 def correct(s: State, cfg: Cfg) -> float:
     """src/sim.py:426-449 -- gradient subtract with ghost p = 0, div_post, walls."""
-    n = cfg.n
+    nx, ny, nz = cfg.box
     coef = cfg.dt / (cfg.density * cfg.h)
-    p3 = s.p.reshape((n, n, n), order="F")
-    s.u[1:n] -= coef * (p3[1:] - p3[:-1])
-    s.v[:, 1:n] -= coef * (p3[:, 1:] - p3[:, :-1])
-    s.w[:, :, 1:n] -= coef * (p3[:, :, 1:] - p3[:, :, :-1])
+    p3 = s.p.reshape((nx, ny, nz), order="F")
+    s.u[1:nx] -= coef * (p3[1:] - p3[:-1])
+    s.v[:, 1:ny] -= coef * (p3[:, 1:] - p3[:, :-1])
+    s.w[:, :, 1:nz] -= coef * (p3[:, :, 1:] - p3[:, :, :-1])
     s.u[0] -= coef * p3[0]
-    s.u[n] -= coef * (0.0 - p3[n - 1])
+    s.u[nx] -= coef * (0.0 - p3[nx - 1])
     s.v[:, 0] -= coef * p3[:, 0]
-    s.v[:, n] -= coef * (0.0 - p3[:, n - 1])
+    s.v[:, ny] -= coef * (0.0 - p3[:, ny - 1])
     s.w[:, :, 0] -= coef * p3[:, :, 0]
-    s.w[:, :, n] -= coef * (0.0 - p3[:, :, n - 1])
+    s.w[:, :, nz] -= coef * (0.0 - p3[:, :, nz - 1])
     div_post = float(np.abs(divergence(s.u, s.v, s.w, cfg.h, cfg.threads)).max())
     enforce_boundaries(s)
     return div_post
@@ -477,7 +495,7 @@ def step(s: State, cfg: Cfg, cache: Cache | None = None) -> StepResult:
 
 def run(cfg: Cfg):
     """src/sim.py:477-505 without snapshot output."""
-    s = initial_state(cfg.n)
+    s = initial_state(cfg.n, cfg.shape)
     cache = Cache()
     results = [step(s, cfg, cache) for _ in range(cfg.num_steps)]
     return s, results

@@ -173,10 +173,13 @@ static double trilerp(const double *arr, i64 na, i64 nb, i64 nc,
 
 /* src/sim.py:193-229 (_advect_face) and :232-240 (_advect_range). */
 void orc_advect(const double *u, const double *v, const double *w,
-                double *out, int comp, i64 n, double h, double dt,
-                double length, const i64 *bounds, int nch)
+                double *out, int comp, i64 nx, i64 ny, i64 nz, double h, double dt,
+                const i64 *bounds, int nch)
 {
-    i64 na = n + (comp == 0), nb = n + (comp == 1), nc = n + (comp == 2);
+    /* the reference's cube has nx = ny = nz = n and one side length n*h
+     * (src/grid.py:35-37); a box (extension) clamps each axis to its own */
+    const double lx = nx * h, ly = ny * h, lz = nz * h;
+    i64 na = nx + (comp == 0), nb = ny + (comp == 1), nc = nz + (comp == 2);
     CHUNK_LOOP(nch) {
         for (i64 idx = bounds[c_]; idx < bounds[c_ + 1]; ++idx) {
             i64 i = idx % na, j = (idx / na) % nb, k = idx / (na * nb);
@@ -188,19 +191,19 @@ void orc_advect(const double *u, const double *v, const double *w,
             } else {
                 x = (i + 0.5) * h; y = (j + 0.5) * h; z = k * h;
             }
-            double su = trilerp(u, n + 1, n, n, x / h, y / h - 0.5, z / h - 0.5);
-            double sv = trilerp(v, n, n + 1, n, x / h - 0.5, y / h, z / h - 0.5);
-            double sw = trilerp(w, n, n, n + 1, x / h - 0.5, y / h - 0.5, z / h);
-            double xb = clampd(x - dt * su, length);
-            double yb = clampd(y - dt * sv, length);
-            double zb = clampd(z - dt * sw, length);
+            double su = trilerp(u, nx + 1, ny, nz, x / h, y / h - 0.5, z / h - 0.5);
+            double sv = trilerp(v, nx, ny + 1, nz, x / h - 0.5, y / h, z / h - 0.5);
+            double sw = trilerp(w, nx, ny, nz + 1, x / h - 0.5, y / h - 0.5, z / h);
+            double xb = clampd(x - dt * su, lx);
+            double yb = clampd(y - dt * sv, ly);
+            double zb = clampd(z - dt * sw, lz);
             double r;
             if (comp == 0)
-                r = trilerp(u, n + 1, n, n, xb / h, yb / h - 0.5, zb / h - 0.5);
+                r = trilerp(u, nx + 1, ny, nz, xb / h, yb / h - 0.5, zb / h - 0.5);
             else if (comp == 1)
-                r = trilerp(v, n, n + 1, n, xb / h - 0.5, yb / h, zb / h - 0.5);
+                r = trilerp(v, nx, ny + 1, nz, xb / h - 0.5, yb / h, zb / h - 0.5);
             else
-                r = trilerp(w, n, n, n + 1, xb / h - 0.5, yb / h - 0.5, zb / h);
+                r = trilerp(w, nx, ny, nz + 1, xb / h - 0.5, yb / h - 0.5, zb / h);
             out[(i * nb + j) * nc + k] = r;
         }
     }
@@ -209,18 +212,18 @@ void orc_advect(const double *u, const double *v, const double *w,
 /* src/grid.py:145-154 (divergence): numpy evaluates the six-term flux
  * expression left to right, then divides by h; output flat, i fastest. */
 void orc_divergence(const double *u, const double *v, const double *w,
-                    i64 n, double h, double *out, int nthreads)
+                    i64 nx, i64 ny, i64 nz, double h, double *out, int nthreads)
 {
-    const i64 n1 = n + 1;
+    /* C-order arrays: u (nx+1, ny, nz), v (nx, ny+1, nz), w (nx, ny, nz+1) */
 #pragma omp parallel for num_threads(nthreads > 0 ? nthreads : 1)
-    for (i64 k = 0; k < n; ++k)
-        for (i64 j = 0; j < n; ++j)
-            for (i64 i = 0; i < n; ++i) {
-                double t = u[((i + 1) * n + j) * n + k] - u[(i * n + j) * n + k];
-                t = t + v[(i * n1 + j + 1) * n + k];
-                t = t - v[(i * n1 + j) * n + k];
-                t = t + w[(i * n + j) * n1 + k + 1];
-                t = t - w[(i * n + j) * n1 + k];
-                out[i + n * (j + n * k)] = t / h;
+    for (i64 k = 0; k < nz; ++k)
+        for (i64 j = 0; j < ny; ++j)
+            for (i64 i = 0; i < nx; ++i) {
+                double t = u[((i + 1) * ny + j) * nz + k] - u[(i * ny + j) * nz + k];
+                t = t + v[(i * (ny + 1) + j + 1) * nz + k];
+                t = t - v[(i * (ny + 1) + j) * nz + k];
+                t = t + w[(i * ny + j) * (nz + 1) + k + 1];
+                t = t - w[(i * ny + j) * (nz + 1) + k];
+                out[i + nx * (j + ny * k)] = t / h;
             }
 }

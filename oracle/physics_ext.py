@@ -68,11 +68,11 @@ def diffuse(u, v, w, n, kdt, lid_u=None, no_slip=False):
         s = s - 6.0 * a
         new = a + kdt * s
         if comp == 0:
-            new[0], new[n] = 0.0, 0.0
+            new[0], new[-1] = 0.0, 0.0
         elif comp == 1:
-            new[:, 0], new[:, n] = 0.0, 0.0
+            new[:, 0], new[:, -1] = 0.0, 0.0
         else:
-            new[:, :, 0], new[:, :, n] = 0.0, 0.0
+            new[:, :, 0], new[:, :, -1] = 0.0, 0.0
         out.append(new)
     return tuple(out)
 
@@ -129,7 +129,7 @@ def diffuse_implicit(u, v, w, n, kdt, lid_u=None, no_slip=False, tol=1e-10):
         _, dia = helmholtz_apply(comp, a, n, kdt, lid_u, no_slip)
         b = a.copy()
         if lid_u is not None and comp == 0:
-            b[1:n, n - 1, :] += kdt * (2.0 * lid_u)
+            b[1:shape[0] - 1, shape[1] - 1, :] += kdt * (2.0 * lid_u)
         x, _ = pcg(op, b.ravel(), x0=a.ravel(), precond=Jacobi(dia.ravel()), tol=tol, max_iter=10000)
         out.append(x.reshape(shape))
     return tuple(out)

@@ -72,17 +72,13 @@ _SIGNATURES = {
     "cf_divergence": ([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _vp, _pd, _vp], _int),
     "cf_pressure_correct": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl,
                              _pd, _vp], _int),
-    "cf_forces_bc_slab": ([_vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _int, _dbl, _int, _vp], _int),
-    "cf_advect_slab": ([_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _int, _dbl, _dbl, _vp],
-                       _int),
-    "cf_divergence_slab": ([_vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _int, _dbl, _dbl, _vp, _pd, _vp],
-                           _int),
-    "cf_pressure_correct_slab": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _int, _dbl,
-                                  _dbl, _pd, _vp], _int),
-    "cf_helmholtz": ([_int, _int, _vp, _vp, _int, _int, _dbl, _dbl, _int, _int, _vp], _int),
+    "cf_forces_bc_slab": ([_vp, _vp, _vp] + [_int] * 9 + [_dbl, _int, _vp], _int),
+    "cf_advect_slab": ([_vp] * 6 + [_int] * 9 + [_dbl, _dbl, _vp], _int),
+    "cf_divergence_slab": ([_vp] * 3 + [_int] * 9 + [_dbl, _dbl, _vp, _pd, _vp], _int),
+    "cf_pressure_correct_slab": ([_vp] * 7 + [_int] * 9 + [_dbl, _dbl, _pd, _vp], _int),
+    "cf_helmholtz": ([_int, _int, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _int, _int, _vp], _int),
     "cf_diffuse": ([_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _int, _int, _vp], _int),
-    "cf_diffuse_slab": ([_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _int, _dbl, _dbl, _int,
-                         _int, _vp], _int),
+    "cf_diffuse_slab": ([_vp] * 6 + [_int] * 9 + [_dbl, _dbl, _int, _int, _vp], _int),
     "cf_sample_velocity":([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _dbl, _dbl, _pd, _vp],
                            _int),
 }

@@ -3,13 +3,16 @@
 // arithmetic in the reference's order (-fmad=false), so results are
 // bit-identical to the reference.
 //
-// Velocity layout: component c has global extents (na, nb, nc) = (n+[c==0],
-// n+[c==1], n+[c==2]) stored x-fastest with row pitch ld_c (padded to a
-// 32-double multiple by the host so every row starts 256-B aligned) and plane
-// pitch ld_c*nb.  Every kernel also runs on a z-slab: the arrays then hold the
-// global planes k_base .. (k_base + stored planes - 1) where k_base = z0 - H
-// (H halo planes below the slab's first owned plane z0); the single-domain
-// entry points are the slab [0, n) with H = 0.
+// Geometry: an nx x ny x nz box of cells of edge h (the reference's cube is
+// nx = ny = nz = n; other boxes are the SURVEY.md §8 f2 extension).  Velocity
+// component c has extents (nx+[c==0], ny+[c==1], nz+[c==2]) stored x-fastest
+// with row pitch ld_c (padded to a 32-double multiple by the host so every row
+// starts 256-B aligned) and plane pitch ld_c * (ny+[c==1]).  Every kernel also
+// runs on a z-slab: the arrays then hold the global planes k_base .. where
+// k_base = z0 - H (H halo planes below the slab's first owned plane z0); the
+// single-domain entry points are the slab [0, nz) with H = 0.
+#include <algorithm>
+
 #include "cf_common.cuh"
 
 namespace cf {
@@ -60,22 +63,23 @@ struct Vel3 {
     Comp c[3];
 };
 
-// Slab of the cube: owned planes [z0, z1) of n; H halo planes each side.
+// Slab of the box: owned planes [z0, z1) of nz; H halo planes each side.
 struct SlabZ {
-    int n, z0, z1, H;
+    int nx, ny, nz, z0, z1, H;
     __host__ __device__ int k_base() const { return z0 - H; }
-    // owned w faces: [z0, z1), plus the top wall face when the slab ends at n
-    __host__ __device__ int w_end() const { return z1 == n ? n + 1 : z1; }
+    // owned w faces: [z0, z1), plus the top wall face when the slab ends at nz
+    __host__ __device__ int w_end() const { return z1 == nz ? nz + 1 : z1; }
+    __host__ __device__ int ext(int axis) const { return axis == 0 ? nx : (axis == 1 ? ny : nz); }
 };
 
-__host__ __device__ inline Comp make_comp(const double *a, int n, int comp, int ld, int k_base)
+__host__ __device__ inline Comp make_comp(const double *a, const SlabZ &sz, int comp, int ld)
 {
-    return Comp{a, n + (comp == 0), n + (comp == 1), n + (comp == 2), ld, k_base};
+    return Comp{a, sz.nx + (comp == 0), sz.ny + (comp == 1), sz.nz + (comp == 2), ld, sz.k_base()};
 }
 
-static Vel3 make_vel(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw, int kb)
+static Vel3 make_vel(const double *u, const double *v, const double *w, const SlabZ &sz, int ldu, int ldv, int ldw)
 {
-    return Vel3{{make_comp(u, n, 0, ldu, kb), make_comp(v, n, 1, ldv, kb), make_comp(w, n, 2, ldw, kb)}};
+    return Vel3{{make_comp(u, sz, 0, ldu), make_comp(v, sz, 1, ldv), make_comp(w, sz, 2, ldw)}};
 }
 
 constexpr int kFaceThreads = 256;
@@ -83,22 +87,23 @@ constexpr int kFaceThreads = 256;
 // src/sim.py:193-240 + :283-288.  blockIdx.y = component; a grid-stride
 // loop over the slab's owned faces with i fastest (coalesced stores).
 __global__ void __launch_bounds__(kFaceThreads) advect_kernel(Vel3 in, double *nu, double *nv, double *nw,
-                                                              SlabZ sz, double h, double dt, double length)
+                                                              SlabZ sz, double h, double dt)
 {
     const int comp = blockIdx.y;
-    const int n = sz.n;
     const Comp me = in.c[comp];
     double *out = comp == 0 ? nu : (comp == 1 ? nv : nw);
     const int kend = comp == 2 ? sz.w_end() : sz.z1;
     const long long total = (long long)me.na * me.nb * (kend - sz.z0);
     const long long stride = (long long)gridDim.x * kFaceThreads;
+    const int wall_n = sz.ext(comp);
+    const double lx = sz.nx * h, ly = sz.ny * h, lz = sz.nz * h;  // side lengths (length = n*h)
     for (long long f = (long long)blockIdx.x * kFaceThreads + threadIdx.x; f < total; f += stride) {
         const int i = (int)(f % me.na);
         const long long rest = f / me.na;
         const int j = (int)(rest % me.nb), k = sz.z0 + (int)(rest / me.nb);
         double *dst = out + me.off(i, j, k);
         const int wall = comp == 0 ? i : (comp == 1 ? j : k);
-        if (wall == 0 || wall == n) {  // wall-normal planes are zeroed (:283-288)
+        if (wall == 0 || wall == wall_n) {  // wall-normal planes are zeroed (:283-288)
             *dst = 0.0;
             continue;
         }
@@ -113,9 +118,9 @@ __global__ void __launch_bounds__(kFaceThreads) advect_kernel(Vel3 in, double *n
         const double su = trilerp(in.c[0], x / h, y / h - 0.5, z / h - 0.5);
         const double sv = trilerp(in.c[1], x / h - 0.5, y / h, z / h - 0.5);
         const double sw = trilerp(in.c[2], x / h - 0.5, y / h - 0.5, z / h);
-        const double xb = clamp_hi(x - dt * su, length);
-        const double yb = clamp_hi(y - dt * sv, length);
-        const double zb = clamp_hi(z - dt * sw, length);
+        const double xb = clamp_hi(x - dt * su, lx);
+        const double yb = clamp_hi(y - dt * sv, ly);
+        const double zb = clamp_hi(z - dt * sw, lz);
         double r;
         if (comp == 0) r = trilerp(me, xb / h, yb / h - 0.5, zb / h - 0.5);
         else if (comp == 1) r = trilerp(me, xb / h - 0.5, yb / h, zb / h - 0.5);
@@ -125,30 +130,32 @@ __global__ void __launch_bounds__(kFaceThreads) advect_kernel(Vel3 in, double *n
 }
 
 // src/sim.py:134-149 on the slab.  blockIdx.y selects the task: 0 = lid row
-// u[1:n, n-1, k] += lid_dv; 1..6 = the six wall-normal planes.
+// u[1:nx, ny-1, k] += lid_dv; 1..6 = the six wall-normal planes.
 __global__ void forces_bc_kernel(double *u, double *v, double *w, SlabZ sz, int ldu, int ldv, int ldw, double lid_dv,
                                  int apply_lid)
 {
     const int task = blockIdx.y;
-    const int n = sz.n, kb = sz.k_base(), nzl = sz.z1 - sz.z0;
-    const long long m = (long long)(n + 1) * (n + 1);
+    const int nx = sz.nx, ny = sz.ny, nz = sz.nz, kb = sz.k_base(), nzl = sz.z1 - sz.z0;
+    long long m;  // items of this task
+    if (task == 0) m = apply_lid ? (long long)(nx - 1) * nzl : 0;
+    else if (task <= 2) m = (long long)ny * nzl;
+    else if (task <= 4) m = (long long)nx * nzl;
+    else m = ((task == 5 && sz.z0 == 0) || (task == 6 && sz.z1 == nz)) ? (long long)nx * ny : 0;
     for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += (long long)gridDim.x * blockDim.x) {
-        const int a = (int)(t % (n + 1)), b = (int)(t / (n + 1));
-        if (task == 0) {  // a = i in [1, n-1], b = local k
-            if (apply_lid && a >= 1 && a <= n - 1 && b < nzl) {
-                double *q = u + a + (long long)ldu * ((long long)(n - 1) + (long long)n * (sz.z0 + b - kb));
-                *q = *q + lid_dv;
-            }
-        } else if (task <= 2) {  // u[0|n, j, k]: a = j, b = local k
-            if (a < n && b < nzl)
-                u[(task == 1 ? 0 : n) + (long long)ldu * (a + (long long)n * (sz.z0 + b - kb))] = 0.0;
-        } else if (task <= 4) {  // v[i, 0|n, k]: a = i, b = local k
-            if (a < n && b < nzl)
-                v[a + (long long)ldv * ((task == 3 ? 0 : n) + (long long)(n + 1) * (sz.z0 + b - kb))] = 0.0;
-        } else {  // w[i, j, 0|n] where the slab owns the wall face: a = i, b = j
-            const int k = task == 5 ? 0 : n;
-            const bool owned = task == 5 ? sz.z0 == 0 : sz.z1 == n;
-            if (owned && a < n && b < n) w[a + (long long)ldw * (b + (long long)n * (k - kb))] = 0.0;
+        if (task == 0) {  // u[i, ny-1, k], i in [1, nx-1]
+            const int i = 1 + (int)(t % (nx - 1)), k = sz.z0 + (int)(t / (nx - 1));
+            double *q = u + i + (long long)ldu * ((long long)(ny - 1) + (long long)ny * (k - kb));
+            *q = *q + lid_dv;
+        } else if (task <= 2) {  // u[0|nx, j, k]
+            const int j = (int)(t % ny), k = sz.z0 + (int)(t / ny);
+            u[(task == 1 ? 0 : nx) + (long long)ldu * (j + (long long)ny * (k - kb))] = 0.0;
+        } else if (task <= 4) {  // v[i, 0|ny, k]
+            const int i = (int)(t % nx), k = sz.z0 + (int)(t / nx);
+            v[i + (long long)ldv * ((task == 3 ? 0 : ny) + (long long)(ny + 1) * (k - kb))] = 0.0;
+        } else {  // w[i, j, 0|nz], owned by the slab holding that wall
+            const int i = (int)(t % nx), j = (int)(t / nx);
+            const int k = task == 5 ? 0 : nz;
+            w[i + (long long)ldw * (j + (long long)ny * (k - kb))] = 0.0;
         }
     }
 }
@@ -164,14 +171,14 @@ __global__ void __launch_bounds__(kCellThreads) divergence_kernel(Vel3 in, SlabZ
 {
     __shared__ double red[32];
     __shared__ int is_last;
-    const int n = sz.n;
-    const long long total = (long long)n * n * (sz.z1 - sz.z0);
+    const int nx = sz.nx, ny = sz.ny;
+    const long long total = (long long)nx * ny * (sz.z1 - sz.z0);
     const long long stride = (long long)gridDim.x * kCellThreads;
     double mx = 0.0;
     for (long long c = (long long)blockIdx.x * kCellThreads + threadIdx.x; c < total; c += stride) {
-        const int i = (int)(c % n);
-        const long long rest = c / n;
-        const int j = (int)(rest % n), k = sz.z0 + (int)(rest / n);
+        const int i = (int)(c % nx);
+        const long long rest = c / nx;
+        const int j = (int)(rest % ny), k = sz.z0 + (int)(rest / ny);
         double t = in.c[0].at(i + 1, j, k) - in.c[0].at(i, j, k);
         t = t + in.c[1].at(i, j + 1, k);
         t = t - in.c[1].at(i, j, k);
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(kCellThreads) divergence_kernel(Vel3 in, SlabZ
 
 // src/sim.py:434-449.  One thread per owned cell: it recomputes the
 // corrected values of its six faces from the OLD field (p with a one-plane
-// halo in z, ghost p = 0 outside the cube), takes the cell divergence of the
+// halo in z, ghost p = 0 outside the box), takes the cell divergence of the
 // corrected faces for div_post, and writes the faces it owns (its three lower
 // faces and, on the high walls, the upper ones) to the output field with the
 // wall-normal faces clamped to zero.  p is slab-local (plane k - z0) and
@@ -206,24 +213,24 @@ __global__ void __launch_bounds__(kCellThreads) correct_kernel(Vel3 in, double *
 {
     __shared__ double red[32];
     __shared__ int is_last;
-    const int n = sz.n;
-    const long long total = (long long)n * n * (sz.z1 - sz.z0);
+    const int nx = sz.nx, ny = sz.ny, nz = sz.nz;
+    const long long total = (long long)nx * ny * (sz.z1 - sz.z0);
     const long long stride = (long long)gridDim.x * kCellThreads;
-    const long long nn = (long long)n * n;
+    const long long pl = (long long)nx * ny;
     double mx = 0.0;
     for (long long c = (long long)blockIdx.x * kCellThreads + threadIdx.x; c < total; c += stride) {
-        const int i = (int)(c % n);
-        const long long rest = c / n;
-        const int j = (int)(rest % n), k = sz.z0 + (int)(rest / n);
+        const int i = (int)(c % nx);
+        const long long rest = c / nx;
+        const int j = (int)(rest % ny), k = sz.z0 + (int)(rest / ny);
         const double pc = __ldg(p + c);
         // lower face: interior -> coef*(p - p_prev); wall -> coef*p
         // upper face: interior -> coef*(p_next - p); wall -> coef*(0.0 - p)
         const double du0 = i > 0 ? pc - __ldg(p + c - 1) : pc;
-        const double du1 = i < n - 1 ? __ldg(p + c + 1) - pc : 0.0 - pc;
-        const double dv0 = j > 0 ? pc - __ldg(p + c - n) : pc;
-        const double dv1 = j < n - 1 ? __ldg(p + c + n) - pc : 0.0 - pc;
-        const double dw0 = k > 0 ? pc - __ldg(p + c - nn) : pc;
-        const double dw1 = k < n - 1 ? __ldg(p + c + nn) - pc : 0.0 - pc;
+        const double du1 = i < nx - 1 ? __ldg(p + c + 1) - pc : 0.0 - pc;
+        const double dv0 = j > 0 ? pc - __ldg(p + c - nx) : pc;
+        const double dv1 = j < ny - 1 ? __ldg(p + c + nx) - pc : 0.0 - pc;
+        const double dw0 = k > 0 ? pc - __ldg(p + c - pl) : pc;
+        const double dw1 = k < nz - 1 ? __ldg(p + c + pl) - pc : 0.0 - pc;
         const double u0 = in.c[0].at(i, j, k) - coef * du0;
         const double u1 = in.c[0].at(i + 1, j, k) - coef * du1;
         const double v0 = in.c[1].at(i, j, k) - coef * dv0;
@@ -240,9 +247,9 @@ __global__ void __launch_bounds__(kCellThreads) correct_kernel(Vel3 in, double *
         nu[cu.off(i, j, k)] = i == 0 ? 0.0 : u0;
         nv[cv.off(i, j, k)] = j == 0 ? 0.0 : v0;
         nw[cw.off(i, j, k)] = k == 0 ? 0.0 : w0;
-        if (i == n - 1) nu[cu.off(n, j, k)] = 0.0;
-        if (j == n - 1) nv[cv.off(i, n, k)] = 0.0;
-        if (k == n - 1) nw[cw.off(i, j, n)] = 0.0;
+        if (i == nx - 1) nu[cu.off(nx, j, k)] = 0.0;
+        if (j == ny - 1) nv[cv.off(i, ny, k)] = 0.0;
+        if (k == nz - 1) nw[cw.off(i, j, nz)] = 0.0;
     }
     mx = block_max<kCellThreads>(mx, red);
     if (threadIdx.x == 0) partials[blockIdx.x] = mx;
@@ -259,7 +266,7 @@ __global__ void __launch_bounds__(kCellThreads) correct_kernel(Vel3 in, double *
 //   new = c + kdt * (((((( xm + xp) + ym) + yp) + zm) + zp) - 6*c),  kdt = nu*dt/h^2,
 // on the component's own lattice.  Neighbours across a wall are ghosts:
 // mirrored (+c, free slip) or antisymmetric (-c, no slip) for tangential
-// components; the lid (y = L) with a set velocity U is a Dirichlet wall:
+// components; the lid (y = Ly) with a set velocity U is a Dirichlet wall:
 // ghost u = 2U - c, ghost w = -c.  Wall-normal faces stay zero.  The oracle
 // restates the same order (oracle/physics_ext.py).
 struct DiffBC {
@@ -273,20 +280,20 @@ __global__ void __launch_bounds__(kFaceThreads) diffuse_kernel(Vel3 in, double *
                                                                double kdt, DiffBC bc)
 {
     const int comp = blockIdx.y;
-    const int n = sz.n;
     const Comp me = in.c[comp];
     double *out = comp == 0 ? nu : (comp == 1 ? nv : nw);
     const int kend = comp == 2 ? sz.w_end() : sz.z1;
     const long long total = (long long)me.na * me.nb * (kend - sz.z0);
     const long long stride = (long long)gridDim.x * kFaceThreads;
     const bool ns = bc.no_slip != 0;
+    const int nx = sz.nx, ny = sz.ny, nz = sz.nz, wall_n = sz.ext(comp);
     for (long long f = (long long)blockIdx.x * kFaceThreads + threadIdx.x; f < total; f += stride) {
         const int i = (int)(f % me.na);
         const long long rest = f / me.na;
         const int j = (int)(rest % me.nb), k = sz.z0 + (int)(rest / me.nb);
         double *dst = out + me.off(i, j, k);
         const int wall = comp == 0 ? i : (comp == 1 ? j : k);
-        if (wall == 0 || wall == n) {
+        if (wall == 0 || wall == wall_n) {
             *dst = 0.0;
             continue;
         }
@@ -298,14 +305,14 @@ __global__ void __launch_bounds__(kFaceThreads) diffuse_kernel(Vel3 in, double *
             xp = me.at(i + 1, j, k);
         } else {
             xm = i > 0 ? me.at(i - 1, j, k) : ghost(c, ns);
-            xp = i < n - 1 ? me.at(i + 1, j, k) : ghost(c, ns);
+            xp = i < nx - 1 ? me.at(i + 1, j, k) : ghost(c, ns);
         }
         if (comp == 1) {
             ym = me.at(i, j - 1, k);
             yp = me.at(i, j + 1, k);
         } else {
             ym = j > 0 ? me.at(i, j - 1, k) : ghost(c, ns);
-            if (j < n - 1) yp = me.at(i, j + 1, k);
+            if (j < ny - 1) yp = me.at(i, j + 1, k);
             else if (bc.lid_dirichlet) yp = comp == 0 ? 2.0 * bc.lid_u - c : -c;
             else yp = ghost(c, ns);
         }
@@ -314,7 +321,7 @@ __global__ void __launch_bounds__(kFaceThreads) diffuse_kernel(Vel3 in, double *
             zp = me.at(i, j, k + 1);
         } else {
             zm = k > 0 ? me.at(i, j, k - 1) : ghost(c, ns);
-            zp = k < n - 1 ? me.at(i, j, k + 1) : ghost(c, ns);
+            zp = k < nz - 1 ? me.at(i, j, k + 1) : ghost(c, ns);
         }
         double s = xm + xp;
         s = s + ym;
@@ -335,19 +342,21 @@ __global__ void __launch_bounds__(kFaceThreads) diffuse_kernel(Vel3 in, double *
 // MODE 0: y = A x   MODE 1: y = diag(A)   MODE 2: y = rhs from x = u*
 template <int MODE>
 __global__ void __launch_bounds__(kFaceThreads) helmholtz_kernel(const double *__restrict__ xin, double *__restrict__ y,
-                                                                 int comp, int n, int ld, double kdt, DiffBC bc)
+                                                                 int comp, int nx, int ny, int nz, int ld, double kdt,
+                                                                 DiffBC bc)
 {
-    const int na = n + (comp == 0), nb = n + (comp == 1), nc = n + (comp == 2);
+    const int na = nx + (comp == 0), nb = ny + (comp == 1), nc = nz + (comp == 2);
     const long long total = (long long)ld * nb * nc;
     const long long stride = (long long)gridDim.x * kFaceThreads;
     const bool ns = bc.no_slip != 0;
     const long long pj = ld, pk = (long long)ld * nb;
+    const int wall_n = comp == 0 ? nx : (comp == 1 ? ny : nz);
     for (long long f = (long long)blockIdx.x * kFaceThreads + threadIdx.x; f < total; f += stride) {
         const int i = (int)(f % ld);
         const long long rest = f / ld;
         const int j = (int)(rest % nb), k = (int)(rest / nb);
         const int wall = comp == 0 ? i : (comp == 1 ? j : k);
-        if (i >= na || wall == 0 || wall == n) {  // fixed faces, padding: identity
+        if (i >= na || wall == 0 || wall == wall_n) {  // fixed faces, padding: identity
             y[f] = MODE == 1 ? 1.0 : (MODE == 0 ? xin[f] : 0.0);
             continue;
         }
@@ -357,9 +366,9 @@ __global__ void __launch_bounds__(kFaceThreads) helmholtz_kernel(const double *_
         const double g = ns ? -1.0 : 1.0;
         double gsum = 0.0;  // sum of ghost coefficients multiplying c
         double lid = 0.0;   // Dirichlet lid contribution to the rhs
-        const bool ex_xm = comp == 0 ? i > 1 : i > 0, ex_xp = i < n - 1;
-        const bool ex_ym = comp == 1 ? j > 1 : j > 0, ex_yp = j < n - 1;
-        const bool ex_zm = comp == 2 ? k > 1 : k > 0, ex_zp = k < n - 1;
+        const bool ex_xm = comp == 0 ? i > 1 : i > 0, ex_xp = i < nx - 1;
+        const bool ex_ym = comp == 1 ? j > 1 : j > 0, ex_yp = j < ny - 1;
+        const bool ex_zm = comp == 2 ? k > 1 : k > 0, ex_zp = k < nz - 1;
         if (comp != 0 && !ex_xm) gsum += g;
         if (comp != 0 && !ex_xp) gsum += g;
         if (comp != 1 && !ex_ym) gsum += g;
@@ -406,9 +415,15 @@ static int grid_for(long long work, int threads, int per_sm)
     return (int)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
-static bool pitches_ok(int n, int ldu, int ldv, int ldw) { return ldu >= n + 1 && ldv >= n && ldw >= n; }
+static bool pitches_ok(const SlabZ &sz, int ldu, int ldv, int ldw)
+{
+    return ldu >= sz.nx + 1 && ldv >= sz.nx && ldw >= sz.nx;
+}
 
-static bool slab_ok(int n, int z0, int z1, int H) { return n >= 1 && 0 <= z0 && z0 < z1 && z1 <= n && H >= 0; }
+static bool slab_ok(const SlabZ &s)
+{
+    return s.nx >= 1 && s.ny >= 1 && s.nz >= 1 && 0 <= s.z0 && s.z0 < s.z1 && s.z1 <= s.nz && s.H >= 0;
+}
 
 // One-shot max reduction through the shared scratch, result to host.
 template <class Launch>
@@ -432,7 +447,9 @@ static int reduce_max_to_host(Launch launch, double *result_host, cudaStream_t s
 static int forces_bc(double *u, double *v, double *w, SlabZ sz, int ldu, int ldv, int ldw, double lid_dv, int lid,
                      void *stream)
 {
-    long long m = (long long)(sz.n + 1) * (sz.n + 1);
+    CF_REQUIRE(slab_ok(sz) && pitches_ok(sz, ldu, ldv, ldw), "forces_bc: bad slab/pitch");
+    long long m = std::max((long long)(sz.nx + 1) * (sz.ny + 1),
+                           (long long)std::max(sz.nx, sz.ny) * (sz.z1 - sz.z0));
     dim3 grid((unsigned)((m + 255) / 256 < 1024 ? (m + 255) / 256 : 1024), 7);
     forces_bc_kernel<<<grid, 256, 0, as_stream(stream)>>>(u, v, w, sz, ldu, ldv, ldw, lid_dv, lid);
     CF_CHECK_LAUNCH("forces_bc_kernel");
@@ -442,10 +459,12 @@ static int forces_bc(double *u, double *v, double *w, SlabZ sz, int ldu, int ldv
 static int advect(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, SlabZ sz,
                   int ldu, int ldv, int ldw, double h, double dt, void *stream)
 {
-    Vel3 in = make_vel(u, v, w, sz.n, ldu, ldv, ldw, sz.k_base());
-    long long faces = (long long)(sz.n + 1) * sz.n * (sz.z1 - sz.z0 + 1);
+    CF_REQUIRE(slab_ok(sz) && h > 0 && pitches_ok(sz, ldu, ldv, ldw), "advect: bad slab/pitch");
+    CF_REQUIRE(nu != u && nv != v && nw != w, "advect: output aliases input");
+    Vel3 in = make_vel(u, v, w, sz, ldu, ldv, ldw);
+    long long faces = (long long)(sz.nx + 1) * (sz.ny + 1) * (sz.z1 - sz.z0 + 1);
     dim3 grid(grid_for(faces, kFaceThreads, 8), 3);
-    advect_kernel<<<grid, kFaceThreads, 0, as_stream(stream)>>>(in, nu, nv, nw, sz, h, dt, sz.n * h);
+    advect_kernel<<<grid, kFaceThreads, 0, as_stream(stream)>>>(in, nu, nv, nw, sz, h, dt);
     CF_CHECK_LAUNCH("advect_kernel");
     return CF_OK;
 }
@@ -453,9 +472,10 @@ static int advect(const double *u, const double *v, const double *w, double *nu,
 static int divergence(const double *u, const double *v, const double *w, SlabZ sz, int ldu, int ldv, int ldw,
                       double h, double scale, double *out, double *maxabs_host, void *stream)
 {
-    Vel3 in = make_vel(u, v, w, sz.n, ldu, ldv, ldw, sz.k_base());
+    CF_REQUIRE(slab_ok(sz) && h > 0 && pitches_ok(sz, ldu, ldv, ldw), "divergence: bad slab/pitch");
+    Vel3 in = make_vel(u, v, w, sz, ldu, ldv, ldw);
     cudaStream_t s = as_stream(stream);
-    int grid = grid_for((long long)sz.n * sz.n * (sz.z1 - sz.z0), kCellThreads, 8);
+    int grid = grid_for((long long)sz.nx * sz.ny * (sz.z1 - sz.z0), kCellThreads, 8);
     return reduce_max_to_host(
         [&](double *part, unsigned int *tk, double *res) {
             divergence_kernel<<<grid, kCellThreads, 0, s>>>(in, sz, h, scale, scale != 1.0, out, part, tk, res);
@@ -467,9 +487,11 @@ static int correct(const double *u, const double *v, const double *w, double *nu
                    const double *p, SlabZ sz, int ldu, int ldv, int ldw, double h, double coef, double *div_post_host,
                    void *stream)
 {
-    Vel3 in = make_vel(u, v, w, sz.n, ldu, ldv, ldw, sz.k_base());
+    CF_REQUIRE(slab_ok(sz) && h > 0 && pitches_ok(sz, ldu, ldv, ldw), "pressure_correct: bad slab/pitch");
+    CF_REQUIRE(nu != u && nv != v && nw != w, "pressure_correct: output aliases input");
+    Vel3 in = make_vel(u, v, w, sz, ldu, ldv, ldw);
     cudaStream_t s = as_stream(stream);
-    int grid = grid_for((long long)sz.n * sz.n * (sz.z1 - sz.z0), kCellThreads, 8);
+    int grid = grid_for((long long)sz.nx * sz.ny * (sz.z1 - sz.z0), kCellThreads, 8);
     return reduce_max_to_host(
         [&](double *part, unsigned int *tk, double *res) {
             correct_kernel<<<grid, kCellThreads, 0, s>>>(in, nu, nv, nw, p, sz, h, coef, part, tk, res);
@@ -477,118 +499,117 @@ static int correct(const double *u, const double *v, const double *w, double *nu
         div_post_host, s);
 }
 
+static int diffuse(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, SlabZ sz,
+                   int ldu, int ldv, int ldw, double kdt, DiffBC bc, void *stream)
+{
+    CF_REQUIRE(slab_ok(sz) && pitches_ok(sz, ldu, ldv, ldw), "diffuse: bad slab/pitch");
+    CF_REQUIRE(nu != u && nv != v && nw != w, "diffuse: output aliases input");
+    Vel3 in = make_vel(u, v, w, sz, ldu, ldv, ldw);
+    long long faces = (long long)(sz.nx + 1) * (sz.ny + 1) * (sz.z1 - sz.z0 + 1);
+    dim3 grid(grid_for(faces, kFaceThreads, 8), 3);
+    diffuse_kernel<<<grid, kFaceThreads, 0, as_stream(stream)>>>(in, nu, nv, nw, sz, kdt, bc);
+    CF_CHECK_LAUNCH("diffuse_kernel");
+    return CF_OK;
+}
+
 }  // namespace cf
 
 extern "C" {
 
+// ---- the reference's cube (nx = ny = nz = n) -----------------------------
 int cf_forces_bc(double *u, double *v, double *w, int n, int ldu, int ldv, int ldw, double lid_dv, int apply_lid,
                  void *stream)
 {
-    CF_REQUIRE(n >= 1 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_forces_bc: bad grid/pitch");
-    return cf::forces_bc(u, v, w, cf::SlabZ{n, 0, n, 0}, ldu, ldv, ldw, lid_dv, apply_lid, stream);
-}
-
-int cf_forces_bc_slab(double *u, double *v, double *w, int n, int z0, int z1, int halo, int ldu, int ldv, int ldw,
-                      double lid_dv, int apply_lid, void *stream)
-{
-    CF_REQUIRE(cf::slab_ok(n, z0, z1, halo) && cf::pitches_ok(n, ldu, ldv, ldw), "cf_forces_bc_slab: bad slab");
-    return cf::forces_bc(u, v, w, cf::SlabZ{n, z0, z1, halo}, ldu, ldv, ldw, lid_dv, apply_lid, stream);
+    return cf::forces_bc(u, v, w, cf::SlabZ{n, n, n, 0, n, 0}, ldu, ldv, ldw, lid_dv, apply_lid, stream);
 }
 
 int cf_advect(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n, int ldu,
               int ldv, int ldw, double h, double dt, void *stream)
 {
-    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_advect: bad grid/pitch");
-    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_advect: output aliases input");
-    return cf::advect(u, v, w, nu, nv, nw, cf::SlabZ{n, 0, n, 0}, ldu, ldv, ldw, h, dt, stream);
-}
-
-int cf_advect_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n,
-                   int z0, int z1, int halo, int ldu, int ldv, int ldw, double h, double dt, void *stream)
-{
-    CF_REQUIRE(cf::slab_ok(n, z0, z1, halo) && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_advect_slab: bad slab");
-    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_advect_slab: output aliases input");
-    return cf::advect(u, v, w, nu, nv, nw, cf::SlabZ{n, z0, z1, halo}, ldu, ldv, ldw, h, dt, stream);
+    return cf::advect(u, v, w, nu, nv, nw, cf::SlabZ{n, n, n, 0, n, 0}, ldu, ldv, ldw, h, dt, stream);
 }
 
 int cf_divergence(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw, double h,
                   double scale, double *out, double *maxabs_host, void *stream)
 {
-    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_divergence: bad grid/pitch");
-    return cf::divergence(u, v, w, cf::SlabZ{n, 0, n, 0}, ldu, ldv, ldw, h, scale, out, maxabs_host, stream);
-}
-
-int cf_divergence_slab(const double *u, const double *v, const double *w, int n, int z0, int z1, int halo, int ldu,
-                       int ldv, int ldw, double h, double scale, double *out, double *maxabs_host, void *stream)
-{
-    CF_REQUIRE(cf::slab_ok(n, z0, z1, halo) && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw),
-               "cf_divergence_slab: bad slab");
-    return cf::divergence(u, v, w, cf::SlabZ{n, z0, z1, halo}, ldu, ldv, ldw, h, scale, out, maxabs_host, stream);
+    return cf::divergence(u, v, w, cf::SlabZ{n, n, n, 0, n, 0}, ldu, ldv, ldw, h, scale, out, maxabs_host, stream);
 }
 
 int cf_pressure_correct(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
                         const double *p, int n, int ldu, int ldv, int ldw, double h, double coef, double *div_post_host,
                         void *stream)
 {
-    CF_REQUIRE(n >= 1 && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw), "cf_pressure_correct: bad grid/pitch");
-    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_pressure_correct: output aliases input");
-    return cf::correct(u, v, w, nu, nv, nw, p, cf::SlabZ{n, 0, n, 0}, ldu, ldv, ldw, h, coef, div_post_host, stream);
-}
-
-int cf_pressure_correct_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
-                             const double *p, int n, int z0, int z1, int halo, int ldu, int ldv, int ldw, double h,
-                             double coef, double *div_post_host, void *stream)
-{
-    CF_REQUIRE(cf::slab_ok(n, z0, z1, halo) && h > 0 && cf::pitches_ok(n, ldu, ldv, ldw),
-               "cf_pressure_correct_slab: bad slab");
-    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_pressure_correct_slab: output aliases input");
-    return cf::correct(u, v, w, nu, nv, nw, p, cf::SlabZ{n, z0, z1, halo}, ldu, ldv, ldw, h, coef, div_post_host,
+    return cf::correct(u, v, w, nu, nv, nw, p, cf::SlabZ{n, n, n, 0, n, 0}, ldu, ldv, ldw, h, coef, div_post_host,
                        stream);
-}
-
-int cf_diffuse_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n,
-                    int z0, int z1, int halo, int ldu, int ldv, int ldw, double kdt, double lid_u, int lid_dirichlet,
-                    int no_slip, void *stream)
-{
-    CF_REQUIRE(cf::slab_ok(n, z0, z1, halo) && cf::pitches_ok(n, ldu, ldv, ldw), "cf_diffuse: bad slab");
-    CF_REQUIRE(nu != u && nv != v && nw != w, "cf_diffuse: output aliases input");
-    cf::SlabZ sz{n, z0, z1, halo};
-    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw, sz.k_base());
-    long long faces = (long long)(n + 1) * n * (z1 - z0 + 1);
-    dim3 grid(cf::grid_for(faces, cf::kFaceThreads, 8), 3);
-    cf::diffuse_kernel<<<grid, cf::kFaceThreads, 0, cf::as_stream(stream)>>>(in, nu, nv, nw, sz, kdt,
-                                                                              cf::DiffBC{lid_u, lid_dirichlet, no_slip});
-    CF_CHECK_LAUNCH("diffuse_kernel");
-    return CF_OK;
-}
-
-int cf_helmholtz(int mode, int comp, const double *x, double *y, int n, int ld, double kdt, double lid_u,
-                 int lid_dirichlet, int no_slip, void *stream)
-{
-    CF_REQUIRE(n >= 1 && comp >= 0 && comp <= 2 && mode >= 0 && mode <= 2 && ld >= n + (comp == 0),
-               "cf_helmholtz: bad arguments");
-    long long total = (long long)ld * (n + (comp == 1)) * (n + (comp == 2));
-    int grid = cf::grid_for(total, cf::kFaceThreads, 8);
-    cf::DiffBC bc{lid_u, lid_dirichlet, no_slip};
-    cudaStream_t s = cf::as_stream(stream);
-    if (mode == 0) cf::helmholtz_kernel<0><<<grid, cf::kFaceThreads, 0, s>>>(x, y, comp, n, ld, kdt, bc);
-    else if (mode == 1) cf::helmholtz_kernel<1><<<grid, cf::kFaceThreads, 0, s>>>(x, y, comp, n, ld, kdt, bc);
-    else cf::helmholtz_kernel<2><<<grid, cf::kFaceThreads, 0, s>>>(x, y, comp, n, ld, kdt, bc);
-    CF_CHECK_LAUNCH("helmholtz_kernel");
-    return CF_OK;
 }
 
 int cf_diffuse(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int n, int ldu,
                int ldv, int ldw, double kdt, double lid_u, int lid_dirichlet, int no_slip, void *stream)
 {
-    return cf_diffuse_slab(u, v, w, nu, nv, nw, n, 0, n, 0, ldu, ldv, ldw, kdt, lid_u, lid_dirichlet, no_slip, stream);
+    return cf::diffuse(u, v, w, nu, nv, nw, cf::SlabZ{n, n, n, 0, n, 0}, ldu, ldv, ldw, kdt,
+                       cf::DiffBC{lid_u, lid_dirichlet, no_slip}, stream);
+}
+
+// ---- boxes and z-slabs (nx x ny x nz; owned planes [z0, z1), halo planes) -
+int cf_forces_bc_slab(double *u, double *v, double *w, int nx, int ny, int nz, int z0, int z1, int halo, int ldu,
+                      int ldv, int ldw, double lid_dv, int apply_lid, void *stream)
+{
+    return cf::forces_bc(u, v, w, cf::SlabZ{nx, ny, nz, z0, z1, halo}, ldu, ldv, ldw, lid_dv, apply_lid, stream);
+}
+
+int cf_advect_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int nx, int ny,
+                   int nz, int z0, int z1, int halo, int ldu, int ldv, int ldw, double h, double dt, void *stream)
+{
+    return cf::advect(u, v, w, nu, nv, nw, cf::SlabZ{nx, ny, nz, z0, z1, halo}, ldu, ldv, ldw, h, dt, stream);
+}
+
+int cf_divergence_slab(const double *u, const double *v, const double *w, int nx, int ny, int nz, int z0, int z1,
+                       int halo, int ldu, int ldv, int ldw, double h, double scale, double *out, double *maxabs_host,
+                       void *stream)
+{
+    return cf::divergence(u, v, w, cf::SlabZ{nx, ny, nz, z0, z1, halo}, ldu, ldv, ldw, h, scale, out, maxabs_host,
+                          stream);
+}
+
+int cf_pressure_correct_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw,
+                             const double *p, int nx, int ny, int nz, int z0, int z1, int halo, int ldu, int ldv,
+                             int ldw, double h, double coef, double *div_post_host, void *stream)
+{
+    return cf::correct(u, v, w, nu, nv, nw, p, cf::SlabZ{nx, ny, nz, z0, z1, halo}, ldu, ldv, ldw, h, coef,
+                       div_post_host, stream);
+}
+
+int cf_diffuse_slab(const double *u, const double *v, const double *w, double *nu, double *nv, double *nw, int nx,
+                    int ny, int nz, int z0, int z1, int halo, int ldu, int ldv, int ldw, double kdt, double lid_u,
+                    int lid_dirichlet, int no_slip, void *stream)
+{
+    return cf::diffuse(u, v, w, nu, nv, nw, cf::SlabZ{nx, ny, nz, z0, z1, halo}, ldu, ldv, ldw, kdt,
+                       cf::DiffBC{lid_u, lid_dirichlet, no_slip}, stream);
+}
+
+int cf_helmholtz(int mode, int comp, const double *x, double *y, int nx, int ny, int nz, int ld, double kdt,
+                 double lid_u, int lid_dirichlet, int no_slip, void *stream)
+{
+    CF_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && comp >= 0 && comp <= 2 && mode >= 0 && mode <= 2 &&
+                   ld >= nx + (comp == 0),
+               "cf_helmholtz: bad arguments");
+    long long total = (long long)ld * (ny + (comp == 1)) * (nz + (comp == 2));
+    int grid = cf::grid_for(total, cf::kFaceThreads, 8);
+    cf::DiffBC bc{lid_u, lid_dirichlet, no_slip};
+    cudaStream_t s = cf::as_stream(stream);
+    if (mode == 0) cf::helmholtz_kernel<0><<<grid, cf::kFaceThreads, 0, s>>>(x, y, comp, nx, ny, nz, ld, kdt, bc);
+    else if (mode == 1) cf::helmholtz_kernel<1><<<grid, cf::kFaceThreads, 0, s>>>(x, y, comp, nx, ny, nz, ld, kdt, bc);
+    else cf::helmholtz_kernel<2><<<grid, cf::kFaceThreads, 0, s>>>(x, y, comp, nx, ny, nz, ld, kdt, bc);
+    CF_CHECK_LAUNCH("helmholtz_kernel");
+    return CF_OK;
 }
 
 int cf_sample_velocity(const double *u, const double *v, const double *w, int n, int ldu, int ldv, int ldw, double h,
                        double px, double py, double pz, double *out_host, void *stream)
 {
-    CF_REQUIRE(n >= 1 && h > 0 && out_host && cf::pitches_ok(n, ldu, ldv, ldw), "cf_sample_velocity: bad args");
-    cf::Vel3 in = cf::make_vel(u, v, w, n, ldu, ldv, ldw, 0);
+    cf::SlabZ sz{n, n, n, 0, n, 0};
+    CF_REQUIRE(n >= 1 && h > 0 && out_host && cf::pitches_ok(sz, ldu, ldv, ldw), "cf_sample_velocity: bad args");
+    cf::Vel3 in = cf::make_vel(u, v, w, sz, ldu, ldv, ldw);
     cudaStream_t s = cf::as_stream(stream);
     double *scratch = cf::scratch_partials();
     if (!scratch) { cf::set_error("scratch allocation failed"); return CF_ENOMEM; }

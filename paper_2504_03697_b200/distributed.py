@@ -98,9 +98,9 @@ def emulated_pcg(op: StencilOperator, b, nslabs: int, tol: float = 1e-6, max_ite
     bd, host = as_device(b)
     bd = bd.contiguous()
     n = op.n
-    bounds = SlabDecomposition.bounds(n, nslabs).tolist()
-    scg = SlabCG(n, n, n, op.h, "csr" if op.order == _lib.ORDER_CSR else "sym", bounds=bounds)
-    pl = n * n
+    bounds = SlabDecomposition.bounds(op.nz, nslabs).tolist()
+    scg = SlabCG(op.nx, op.ny, op.nz, op.h, "csr" if op.order == _lib.ORDER_CSR else "sym", bounds=bounds)
+    pl = op.nx * op.ny
     xs, st = scg.solve([bd[bounds[k] * pl:bounds[k + 1] * pl] for k in range(nslabs)], tol, max_iter, precond)
     x = torch.cat(xs)
     return (to_host(x) if host else x), st, scg
@@ -113,19 +113,20 @@ class _SlabFields:
     """One slab's device fields: velocity (two buffers) with HALO planes,
     pressure with one halo plane each side, the Poisson RHS."""
 
-    def __init__(self, n: int, z0: int, z1: int, dev):
+    def __init__(self, nx: int, ny: int, z0: int, z1: int, dev):
         from .grid import padded_ld
 
-        self.n, self.z0, self.z1 = n, z0, z1
+        self.nx, self.ny, self.z0, self.z1 = nx, ny, z0, z1
         self.nzl = z1 - z0
-        self.ld = [padded_ld(n + 1), padded_ld(n), padded_ld(n)]
-        self.nb = [n, n + 1, n]
+        self.pl = nx * ny
+        self.ld = [padded_ld(nx + 1), padded_ld(nx), padded_ld(nx)]
+        self.nb = [ny, ny + 1, ny]
         planes = [self.nzl + 2 * HALO, self.nzl + 2 * HALO, self.nzl + 1 + 2 * HALO]
         self.vel = [[torch.zeros((planes[c], self.nb[c], self.ld[c]), dtype=torch.float64, device=dev)
                      for c in range(3)] for _ in range(2)]
         self.cur = 0
-        self.p = torch.zeros((self.nzl + 2) * n * n, dtype=torch.float64, device=dev)
-        self.rhs = torch.zeros(self.nzl * n * n, dtype=torch.float64, device=dev)
+        self.p = torch.zeros((self.nzl + 2) * self.pl, dtype=torch.float64, device=dev)
+        self.rhs = torch.zeros(self.nzl * self.pl, dtype=torch.float64, device=dev)
 
     def planes(self, c: int, buf: int, k0: int, k1: int) -> torch.Tensor:
         """Stored planes for global planes [k0, k1) of component c."""
@@ -133,8 +134,7 @@ class _SlabFields:
         return self.vel[buf][c][k0 - kb:k1 - kb]
 
     def p_owned(self) -> torch.Tensor:
-        pl = self.n * self.n
-        return self.p[pl:pl * (self.nzl + 1)]
+        return self.p[self.pl:self.pl * (self.nzl + 1)]
 
     def ptrs(self, buf: int):
         return tuple(t.data_ptr() for t in self.vel[buf])
@@ -160,11 +160,13 @@ class SlabSim:
         if cfg.warm_start:
             raise ValueError("warm_start is not supported by the z-slab solver")
         lib = _lib.load_library()
-        self.cfg, self.n = cfg, cfg.n
+        self.cfg = cfg
+        self.nx, self.ny, self.nz = cfg.spec.dims  # the cube, or a box (extension)
         self.bounds = [int(b) for b in bounds]
         self.dist = distributed
         dev = torch.device("cuda", torch.cuda.current_device())
-        self.slabs = [_SlabFields(self.n, self.bounds[k], self.bounds[k + 1], dev) for k in range(len(bounds) - 1)]
+        self.slabs = [_SlabFields(self.nx, self.ny, self.bounds[k], self.bounds[k + 1], dev)
+                      for k in range(len(bounds) - 1)]
         for s in self.slabs:
             if s.nzl < HALO + 1:
                 raise ValueError(f"slab [{s.z0}, {s.z1}) is thinner than {HALO + 1} planes")
@@ -175,11 +177,11 @@ class SlabSim:
             dist.broadcast_object_list(obj, src=0)
             lo = self.rank - 1 if self.rank > 0 else -1
             hi = self.rank + 1 if self.rank < self.world - 1 else -1
-            self.cg = SlabCG(self.n, self.n, self.n, cfg.h, order, bounds=self.bounds, nranks=self.world,
+            self.cg = SlabCG(self.nx, self.ny, self.nz, cfg.h, order, bounds=self.bounds, nranks=self.world,
                              rank=self.rank, uid=obj[0], lo_rank=lo, hi_rank=hi)
         else:
             self.rank, self.world = 0, 1
-            self.cg = SlabCG(self.n, self.n, self.n, cfg.h, order, bounds=self.bounds)
+            self.cg = SlabCG(self.nx, self.ny, self.nz, cfg.h, order, bounds=self.bounds)
         self.step_count = 0
         self._lib = lib
 
@@ -189,24 +191,23 @@ class SlabSim:
         comps = [np.asarray(u), np.asarray(v), np.asarray(w)]
         for s in self.slabs:
             for c, arr in enumerate(comps):
-                k1 = s.z1 + (1 if (c == 2 and s.z1 == self.n) else 0)
+                k1 = s.z1 + (1 if (c == 2 and s.z1 == self.nz) else 0)
                 blk = torch.as_tensor(np.ascontiguousarray(arr[:, :, s.z0:k1].transpose(2, 1, 0)))
                 s.planes(c, s.cur, s.z0, k1)[:, :, :arr.shape[0]].copy_(blk)
             if p is not None:
-                pl = self.n * self.n
-                s.p_owned().copy_(torch.as_tensor(np.asarray(p)[s.z0 * pl:s.z1 * pl]))
+                s.p_owned().copy_(torch.as_tensor(np.asarray(p)[s.z0 * s.pl:s.z1 * s.pl]))
 
     def gather(self):
-        """Global reference-layout (u, v, w, p) of the local slabs (emulation: the whole cube)."""
-        n = self.n
-        out = [np.zeros((n + 1, n, n)), np.zeros((n, n + 1, n)), np.zeros((n, n, n + 1))]
-        p = np.zeros(n ** 3)
+        """Global reference-layout (u, v, w, p) of the local slabs (emulation: the whole box)."""
+        nx, ny, nz = self.nx, self.ny, self.nz
+        out = [np.zeros((nx + 1, ny, nz)), np.zeros((nx, ny + 1, nz)), np.zeros((nx, ny, nz + 1))]
+        p = np.zeros(nx * ny * nz)
         for s in self.slabs:
             for c in range(3):
-                k1 = s.z1 + (1 if (c == 2 and s.z1 == n) else 0)
+                k1 = s.z1 + (1 if (c == 2 and s.z1 == nz) else 0)
                 blk = s.planes(c, s.cur, s.z0, k1)[:, :, :out[c].shape[0]].cpu().numpy()
                 out[c][:, :, s.z0:k1] = blk.transpose(2, 1, 0)
-            p[s.z0 * n * n:s.z1 * n * n] = s.p_owned().cpu().numpy()
+            p[s.z0 * s.pl:s.z1 * s.pl] = s.p_owned().cpu().numpy()
         return out[0], out[1], out[2], p
 
     # ------------------------------------------------------------ halos
@@ -242,7 +243,7 @@ class SlabSim:
                 r.wait()
 
     def _exchange_p(self):
-        pl = self.n * self.n
+        pl = self.nx * self.ny
         for a, b in zip(self.slabs, self.slabs[1:]):
             a.p[pl * (a.nzl + 1):pl * (a.nzl + 2)].copy_(b.p[pl:2 * pl])
             b.p[0:pl].copy_(a.p[pl * a.nzl:pl * (a.nzl + 1)])
@@ -275,10 +276,11 @@ class SlabSim:
         """Advance one time step; returns StepStats (src/sim.py:452-474)."""
         from .sim import StepStats
 
-        cfg, n, lib, st = self.cfg, self.n, self._lib, _lib.stream()
+        cfg, lib, st = self.cfg, self._lib, _lib.stream()
+        dims = (self.nx, self.ny, self.nz)
         for s in self.slabs:  # forces + walls (src/sim.py:134-149)
             u, v, w = s.ptrs(s.cur)
-            _lib.check(lib.cf_forces_bc_slab(u, v, w, n, s.z0, s.z1, HALO, *s.ld, cfg.lid_accel * cfg.dt, 1, st),
+            _lib.check(lib.cf_forces_bc_slab(u, v, w, *dims, s.z0, s.z1, HALO, *s.ld, cfg.lid_accel * cfg.dt, 1, st),
                        "forces_bc_slab")
         self._exchange_vel()
         # the HALO-plane halo covers a backtrace of <= 1 cell in z
@@ -293,7 +295,7 @@ class SlabSim:
         for s in self.slabs:  # advection into the spare buffer (src/sim.py:259-289)
             u, v, w = s.ptrs(s.cur)
             nu, nv, nw = s.ptrs(1 - s.cur)
-            _lib.check(lib.cf_advect_slab(u, v, w, nu, nv, nw, n, s.z0, s.z1, HALO, *s.ld, cfg.h, cfg.dt, st),
+            _lib.check(lib.cf_advect_slab(u, v, w, nu, nv, nw, *dims, s.z0, s.z1, HALO, *s.ld, cfg.h, cfg.dt, st),
                        "advect_slab")
             s.cur = 1 - s.cur
         self._exchange_vel()  # the divergence (and diffusion) read neighbour planes
@@ -303,7 +305,7 @@ class SlabSim:
             for s in self.slabs:
                 u, v, w = s.ptrs(s.cur)
                 nu, nv, nw = s.ptrs(1 - s.cur)
-                _lib.check(lib.cf_diffuse_slab(u, v, w, nu, nv, nw, n, s.z0, s.z1, HALO, *s.ld, kdt,
+                _lib.check(lib.cf_diffuse_slab(u, v, w, nu, nv, nw, *dims, s.z0, s.z1, HALO, *s.ld, kdt,
                                                0.0 if lid is None else float(lid), 0 if lid is None else 1,
                                                1 if cfg.no_slip else 0, st), "diffuse_slab")
                 s.cur = 1 - s.cur
@@ -312,7 +314,7 @@ class SlabSim:
         for s in self.slabs:  # b = -(rho/dt) div (src/sim.py:359-360)
             u, v, w = s.ptrs(s.cur)
             mx = ctypes.c_double()
-            _lib.check(lib.cf_divergence_slab(u, v, w, n, s.z0, s.z1, HALO, *s.ld, cfg.h, -cfg.density / cfg.dt,
+            _lib.check(lib.cf_divergence_slab(u, v, w, *dims, s.z0, s.z1, HALO, *s.ld, cfg.h, -cfg.density / cfg.dt,
                                               s.rhs.data_ptr(), ctypes.byref(mx), st), "divergence_slab")
             maxb.append(mx.value)
         div_pre = self._max(maxb) * cfg.dt / cfg.density
@@ -326,8 +328,7 @@ class SlabSim:
             u, v, w = s.ptrs(s.cur)
             nu, nv, nw = s.ptrs(1 - s.cur)
             out = ctypes.c_double()
-            pl = n * n
-            _lib.check(lib.cf_pressure_correct_slab(u, v, w, nu, nv, nw, s.p.data_ptr() + 8 * pl, n, s.z0, s.z1,
+            _lib.check(lib.cf_pressure_correct_slab(u, v, w, nu, nv, nw, s.p.data_ptr() + 8 * s.pl, *dims, s.z0, s.z1,
                                                     HALO, *s.ld, cfg.h, coef, ctypes.byref(out), st),
                        "pressure_correct_slab")
             posts.append(out.value)

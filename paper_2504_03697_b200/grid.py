@@ -47,16 +47,49 @@ def to_host(t: torch.Tensor) -> np.ndarray:
 
 @dataclass(frozen=True)
 class GridSpec:
-    """Cubic grid geometry: ``n`` cells per side, cell edge ``h`` (src/grid.py:22-41)."""
+    """Cubic grid geometry: ``n`` cells per side, cell edge ``h`` (src/grid.py:22-41).
+
+    ``shape=(nx, ny, nz)`` (extension) describes a box of
+    cells instead of the reference's cube; the cube is ``shape=None``.
+    """
 
     n: int
     h: float = 1.0
+    shape: tuple | None = None
 
     def __post_init__(self):
         if self.n < 1:
             raise ValueError(f"grid needs at least one cell per side, got n={self.n}")
         if not self.h > 0:
             raise ValueError(f"cell edge length must be positive, got h={self.h}")
+        if self.shape is not None:
+            if len(self.shape) != 3 or min(self.shape) < 1:
+                raise ValueError(f"shape must be three positive extents, got {self.shape}")
+            object.__setattr__(self, "shape", tuple(int(s) for s in self.shape))
+
+    @classmethod
+    def box(cls, nx: int, ny: int, nz: int, h: float = 1.0) -> "GridSpec":
+        return cls(nx, h, (nx, ny, nz))
+
+    @property
+    def dims(self) -> tuple:
+        return self.shape if self.shape is not None else (self.n, self.n, self.n)
+
+    @property
+    def nx(self) -> int:
+        return self.dims[0]
+
+    @property
+    def ny(self) -> int:
+        return self.dims[1]
+
+    @property
+    def nz(self) -> int:
+        return self.dims[2]
+
+    @property
+    def is_cube(self) -> bool:
+        return self.nx == self.ny == self.nz
 
     @property
     def side_length(self) -> float:
@@ -64,7 +97,7 @@ class GridSpec:
 
     @property
     def num_cells(self) -> int:
-        return self.n ** 3
+        return self.nx * self.ny * self.nz
 
 
 def cell_index(spec: GridSpec, i: int, j: int, k: int) -> int:
@@ -74,8 +107,9 @@ def cell_index(spec: GridSpec, i: int, j: int, k: int) -> int:
     return i + n * j + n * n * k
 
 
-def _extents(n: int):
-    return ((n + 1, n, n), (n, n + 1, n), (n, n, n + 1))
+def _extents(spec: GridSpec):
+    nx, ny, nz = spec.dims
+    return ((nx + 1, ny, nz), (nx, ny + 1, nz), (nx, ny, nz + 1))
 
 
 def padded_ld(na: int) -> int:
@@ -91,7 +125,7 @@ class VelocityField:
         self._phys = []
         self.ld = []
         views = []
-        for comp, (ext, src) in enumerate(zip(_extents(spec.n), (u, v, w))):
+        for comp, (ext, src) in enumerate(zip(_extents(spec), (u, v, w))):
             na, nb, nc = ext
             ld = padded_ld(na)
             phys = torch.zeros((nc, nb, ld), dtype=torch.float64, device=dev)
@@ -149,9 +183,9 @@ class ScalarField:
         return ScalarField(self.spec, self.data.clone())
 
     def as_3d(self) -> torch.Tensor:
-        """View as (n, n, n) with [i, j, k] indexing (no copy)."""
-        n = self.spec.n
-        return self.data.view(n, n, n).permute(2, 1, 0)
+        """View as (nx, ny, nz) with [i, j, k] indexing (no copy)."""
+        nx, ny, nz = self.spec.dims
+        return self.data.view(nz, ny, nx).permute(2, 1, 0)
 
     def numpy(self) -> np.ndarray:
         return to_host(self.data)
@@ -164,6 +198,8 @@ def sample_velocity(field: VelocityField, point) -> np.ndarray:
         raise ValueError(f"point must have 3 components, got shape {p.shape}")
     if not np.all(np.isfinite(p)):
         raise ValueError(f"non-finite sample point {p!r}")
+    if not field.spec.is_cube:
+        raise ValueError("sample_velocity is defined on the reference's cube")
     lib = _lib.load_library()
     out = np.empty(3)
     u, v, w = field.ptrs()
@@ -185,8 +221,9 @@ def _divergence_into(field: VelocityField, scale: float, out: torch.Tensor, want
     lib = _lib.load_library()
     u, v, w = field.ptrs()
     lu, lv, lw = field.ld
+    nx, ny, nz = field.spec.dims
     mx = _lib.dbl_out()
-    _lib.check(lib.cf_divergence(u, v, w, field.spec.n, lu, lv, lw, field.spec.h, float(scale),
-                                 out.data_ptr(), _lib.byref(mx) if want_max else None, _lib.stream()),
+    _lib.check(lib.cf_divergence_slab(u, v, w, nx, ny, nz, 0, nz, 0, lu, lv, lw, field.spec.h, float(scale),
+                                      out.data_ptr(), _lib.byref(mx) if want_max else None, _lib.stream()),
                "divergence")
     return mx.value if want_max else None

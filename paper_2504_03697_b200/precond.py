@@ -88,13 +88,14 @@ def _triangles(a):
     if isinstance(a, StencilOperator):
         # the 7-point pattern generated directly (lower: k-1, j-1, i-1; upper:
         # i+1, j+1, k+1 -- ascending columns, as the CSR triangles would be)
-        n, num = a.n, a.num
+        nx, ny, nz, num = a.nx, a.ny, a.nz, a.num
         idx = np.arange(num, dtype=np.int64)
-        i, j, k = idx % n, (idx // n) % n, idx // (n * n)
+        i, j, k = idx % nx, (idx // nx) % ny, idx // (nx * ny)
         off = -1.0 / (a.h * a.h)
+        pl = nx * ny
         out = []
-        for cols, mask in (((idx - n * n, idx - n, idx - 1), (k > 0, j > 0, i > 0)),
-                           ((idx + 1, idx + n, idx + n * n), (i < n - 1, j < n - 1, k < n - 1))):
+        for cols, mask in (((idx - pl, idx - nx, idx - 1), (k > 0, j > 0, i > 0)),
+                           ((idx + 1, idx + nx, idx + pl), (i < nx - 1, j < ny - 1, k < nz - 1))):
             c = np.stack(cols, axis=1)
             m = np.stack(mask, axis=1)
             ptr = np.concatenate(([0], np.cumsum(m.sum(axis=1)))).astype(np.int64)
@@ -108,8 +109,7 @@ def _levels(a, lower, n):
     """Level of every row: 1 + max level of its lower columns."""
     if isinstance(a, StencilOperator):
         idx = np.arange(n, dtype=np.int64)
-        m = a.n
-        return (idx % m + (idx // m) % m + idx // (m * m)).astype(np.int32)
+        return (idx % a.nx + (idx // a.nx) % a.ny + idx // (a.nx * a.ny)).astype(np.int32)
     lib = _lib.open_library() if _lib._lib is None else _lib._lib
     lv = np.empty(n, dtype=np.int32)
     nl = np.zeros(1, dtype=np.int32)

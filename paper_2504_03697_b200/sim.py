@@ -65,6 +65,7 @@ class SimConfig:
     initial_pressure: float = 1.0        # the reference starts from p = 1 (dynamically inert)
     diffusion: str = "explicit"          # "explicit" | "implicit" (backward Euler, CG per component)
     diffusion_tol: float = 1e-10
+    shape: tuple | None = None           # an nx*ny*nz box instead of the n-cube
 
     def __post_init__(self):
         if self.viscosity < 0:
@@ -99,7 +100,7 @@ class SimConfig:
 
     @property
     def spec(self) -> GridSpec:
-        return GridSpec(self.n, self.h)
+        return GridSpec(self.n, self.h, tuple(self.shape) if self.shape is not None else None)
 
     @property
     def num_steps(self) -> int:
@@ -137,61 +138,60 @@ def initial_state(cfg: SimConfig) -> SimState:
     return SimState(vel=VelocityField(spec), p=p)
 
 
-def _vel_args(vel: VelocityField):
-    u, v, w = vel.ptrs()
-    return u, v, w, vel.spec.n, vel.ld[0], vel.ld[1], vel.ld[2]
+def _box(vel: VelocityField):
+    """(nx, ny, nz, z0, z1, halo, ldu, ldv, ldw) of the whole box for the cf_*_slab entry points."""
+    nx, ny, nz = vel.spec.dims
+    return (nx, ny, nz, 0, nz, 0, vel.ld[0], vel.ld[1], vel.ld[2])
 
 
 def apply_forces(state: SimState, cfg: SimConfig):
     """Lid offset g*dt on the top-layer u faces (src/sim.py:134-137)."""
-    n = cfg.n
-    state.vel.u[1:n, n - 1, :] += cfg.lid_accel * cfg.dt
+    nx, ny, _ = state.vel.spec.dims
+    state.vel.u[1:nx, ny - 1, :] += cfg.lid_accel * cfg.dt
 
 
 def enforce_boundaries(state: SimState):
     """Zero every wall-normal face (src/sim.py:140-149)."""
     lib = _lib.load_library()
-    _lib.check(lib.cf_forces_bc(*_vel_args(state.vel), 0.0, 0, _lib.stream()), "enforce_boundaries")
+    _lib.check(lib.cf_forces_bc_slab(*state.vel.ptrs(), *_box(state.vel), 0.0, 0, _lib.stream()),
+               "enforce_boundaries")
 
 
 def _forces_and_walls(state: SimState, cfg: SimConfig):
     lib = _lib.load_library()
-    _lib.check(lib.cf_forces_bc(*_vel_args(state.vel), cfg.lid_accel * cfg.dt, 1, _lib.stream()),
-               "forces_bc")
+    _lib.check(lib.cf_forces_bc_slab(*state.vel.ptrs(), *_box(state.vel), cfg.lid_accel * cfg.dt, 1,
+                                     _lib.stream()), "forces_bc")
 
 
 def _advect_into(src: VelocityField, dst: VelocityField, cfg: SimConfig):
     lib = _lib.load_library()
-    u, v, w, n, lu, lv, lw = _vel_args(src)
-    nu, nv, nw = dst.ptrs()
-    _lib.check(lib.cf_advect(u, v, w, nu, nv, nw, n, lu, lv, lw, src.spec.h, cfg.dt, _lib.stream()),
+    _lib.check(lib.cf_advect_slab(*src.ptrs(), *dst.ptrs(), *_box(src), src.spec.h, cfg.dt, _lib.stream()),
                "advect")
 
 
 def _diffuse_into(src: VelocityField, dst: VelocityField, cfg: SimConfig):
     lib = _lib.load_library()
-    u, v, w, n, lu, lv, lw = _vel_args(src)
-    nu, nv, nw = dst.ptrs()
     kdt = cfg.viscosity * cfg.dt / (cfg.h * cfg.h)
     lid = cfg.lid_velocity
-    _lib.check(lib.cf_diffuse(u, v, w, nu, nv, nw, n, lu, lv, lw, kdt, 0.0 if lid is None else float(lid),
-                              0 if lid is None else 1, 1 if cfg.no_slip else 0, _lib.stream()), "diffuse")
+    _lib.check(lib.cf_diffuse_slab(*src.ptrs(), *dst.ptrs(), *_box(src), kdt, 0.0 if lid is None else float(lid),
+                                   0 if lid is None else 1, 1 if cfg.no_slip else 0, _lib.stream()), "diffuse")
 
 
 class HelmholtzOperator:
     """(I - kdt L) for one velocity component on its physical padded array
     (cf_helmholtz); an ``apply_a`` for pcg's per-op path."""
 
-    def __init__(self, comp: int, n: int, ld: int, kdt: float, lid_velocity, no_slip: bool):
-        self.comp, self.n, self.ld, self.kdt = comp, n, ld, float(kdt)
+    def __init__(self, comp: int, dims: tuple, ld: int, kdt: float, lid_velocity, no_slip: bool):
+        self.comp, self.dims, self.ld, self.kdt = comp, tuple(dims), ld, float(kdt)
         self.lid = 0.0 if lid_velocity is None else float(lid_velocity)
         self.dirichlet = 0 if lid_velocity is None else 1
         self.no_slip = 1 if no_slip else 0
 
     def _run(self, mode, x, y):
         lib = _lib.load_library()
-        _lib.check(lib.cf_helmholtz(mode, self.comp, x.data_ptr() if x is not None else None, y.data_ptr(), self.n,
-                                    self.ld, self.kdt, self.lid, self.dirichlet, self.no_slip, _lib.stream()),
+        _lib.check(lib.cf_helmholtz(mode, self.comp, x.data_ptr() if x is not None else None, y.data_ptr(),
+                                    *self.dims, self.ld, self.kdt, self.lid, self.dirichlet, self.no_slip,
+                                    _lib.stream()),
                    "helmholtz")
         return y
 
@@ -214,7 +214,7 @@ def _diffuse_implicit(vel: VelocityField, cfg: SimConfig):
     stats = []
     for comp, phys in enumerate(vel._phys):
         flat = phys.view(-1)
-        op = HelmholtzOperator(comp, cfg.n, vel.ld[comp], kdt, cfg.lid_velocity, cfg.no_slip)
+        op = HelmholtzOperator(comp, vel.spec.dims, vel.ld[comp], kdt, cfg.lid_velocity, cfg.no_slip)
         b = op.rhs(flat)
         pre = JacobiPreconditioner(1.0 / op.diagonal_tensor(flat))
         x, st = pcg(op, b, x0=flat, precond=pre, tol=cfg.diffusion_tol, max_iter=10000, variant="optimized")
@@ -292,13 +292,14 @@ class PoissonCache:
 
     def operator(self, cfg: SimConfig) -> StencilOperator:
         # optimized variant <-> spmv_sym order, baseline <-> spmv (CSR) order
-        key = (cfg.n, cfg.h, cfg.variant)
+        key = (cfg.n, cfg.h, cfg.variant, cfg.spec.dims)
         if key not in self._ops:
-            self._ops[key] = StencilOperator(cfg.n, cfg.h, "sym" if cfg.variant == "optimized" else "csr")
+            self._ops[key] = StencilOperator(cfg.n, cfg.h, "sym" if cfg.variant == "optimized" else "csr",
+                                             shape=cfg.spec.dims)
         return self._ops[key]
 
     def preconditioner(self, cfg: SimConfig, op: StencilOperator):
-        key = (cfg.n, cfg.h, cfg.preconditioner)
+        key = (cfg.n, cfg.h, cfg.preconditioner, cfg.spec.dims)
         if key not in self._precond:
             if cfg.preconditioner == "dic":
                 from .precond import dic_from
@@ -366,12 +367,10 @@ def solve_pressure_correction(state: SimState, cfg: SimConfig, cache: PoissonCac
 
 def _correct_into(src: VelocityField, dst: VelocityField, p: ScalarField, cfg: SimConfig) -> float:
     lib = _lib.load_library()
-    u, v, w, n, lu, lv, lw = _vel_args(src)
-    nu, nv, nw = dst.ptrs()
     coef = cfg.dt / (cfg.density * cfg.h)
     out = _lib.dbl_out()
-    _lib.check(lib.cf_pressure_correct(u, v, w, nu, nv, nw, p.data.data_ptr(), n, lu, lv, lw, cfg.h, coef,
-                                       _lib.byref(out), _lib.stream()), "pressure_correct")
+    _lib.check(lib.cf_pressure_correct_slab(*src.ptrs(), *dst.ptrs(), p.data.data_ptr(), *_box(src), cfg.h, coef,
+                                            _lib.byref(out), _lib.stream()), "pressure_correct")
     return float(out.value)
 
 

@@ -64,7 +64,7 @@ class CgWorkspace:
     def __init__(self, op: StencilOperator):
         lib = _lib.load_library()
         h = ctypes.c_void_p()
-        _lib.check(lib.cf_cg_create(ctypes.byref(h), op.n, op.n, op.n, op.h, op.order, _lib.stream()),
+        _lib.check(lib.cf_cg_create(ctypes.byref(h), op.nx, op.ny, op.nz, op.h, op.order, _lib.stream()),
                    "cf_cg_create")
         self._h = h
         self.op = op

@@ -282,12 +282,14 @@ class StencilOperator:
     variant) so results are bit-identical to the matching reference SpMV.
     """
 
-    def __init__(self, n: int, h: float, order: str = "sym"):
+    def __init__(self, n: int, h: float, order: str = "sym", shape=None):
         if order not in ("csr", "sym"):
             raise ValueError("order must be 'csr' or 'sym'")
         self.n, self.h = int(n), float(h)
+        # shape (extension): an nx*ny*nz box; the reference operator is the n-cube
+        self.nx, self.ny, self.nz = (self.n,) * 3 if shape is None else tuple(int(s) for s in shape)
         self.order = _lib.ORDER_CSR if order == "csr" else _lib.ORDER_SYM
-        self.num = self.n ** 3
+        self.num = self.nx * self.ny * self.nz
         self.inv_diag_value = 1.0 / (6.0 / (self.h * self.h))  # jacobi_from's 1.0 / diag
 
     def __call__(self, x, out=None):
@@ -296,7 +298,7 @@ class StencilOperator:
             raise ValueError(f"operator has dimension {self.num} but x has length {xd.shape[0]}")
         y, host_out = _out_like(out, self.num, host)
         lib = _lib.load_library()
-        _lib.check(lib.cf_stencil7_apply(self.n, self.n, self.n, self.h, self.order,
+        _lib.check(lib.cf_stencil7_apply(self.nx, self.ny, self.nz, self.h, self.order,
                                          xd.contiguous().data_ptr(), y.data_ptr(), _lib.stream()),
                    "stencil7_apply")
         return _finish(y, host_out, host)

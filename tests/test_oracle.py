@@ -199,3 +199,31 @@ def test_extension_implicit_diffusion_restatement():
     r = ext.helmholtz_apply(0, iu, n, 1e-3, 1.0, True)[0]
     want = u.copy(); want[1:n, n - 1, :] += 1e-3 * 2.0
     assert np.abs(r - want).max() <= 1e-11
+
+
+def test_box_restatement_consistency(golden):
+    """The non-cubic extension (shape=(nx,ny,nz)): shape=(n,n,n) reproduces the
+    reference-pinned cube exactly; a box operator is symmetric with diagonal
+    6/h^2 and the CSR/symmetric forms agree to rounding; a box run projects."""
+    g = golden("sparse")
+    h = float(g["n5_h"])
+    cube = orc.poisson_csr(5, h, (5, 5, 5))
+    assert np.array_equal(cube.row_ptr, g["n5_row_ptr"]) and np.array_equal(cube.col_idx, g["n5_col_idx"])
+    shape = (7, 4, 6)
+    a, s = orc.poisson_csr(0, h, shape), orc.poisson_sym(0, h, shape)
+    x = np.random.default_rng(0).standard_normal(7 * 4 * 6)
+    dense = np.zeros((a.n_rows, a.n_rows))
+    for r in range(a.n_rows):
+        dense[r, a.col_idx[a.row_ptr[r]:a.row_ptr[r + 1]]] = a.values[a.row_ptr[r]:a.row_ptr[r + 1]]
+    assert np.array_equal(dense, dense.T) and np.all(np.diag(dense) == 6.0 / h ** 2)
+    assert np.allclose(orc.spmv_sym(s, x), dense @ x, rtol=0, atol=1e-9 / h ** 2)
+    # cell (i,j,k) neighbours: i+1 is +1, j+1 is +nx, k+1 is +nx*ny
+    r = 1 + 7 * (1 + 4 * 1)
+    cols = set(a.col_idx[a.row_ptr[r]:a.row_ptr[r + 1]].tolist())
+    assert cols == {r, r - 1, r + 1, r - 7, r + 7, r - 28, r + 28}
+    cfg = orc.Cfg(n=9, h=1.0 / 9, dt=0.05, t_end=0.1, tol=1e-8, max_iter=5000, preconditioner="jacobi",
+                  variant="optimized", shape=(9, 5, 7))
+    st, results = orc.run(cfg)
+    assert st.u.shape == (10, 5, 7) and st.p.shape == (9 * 5 * 7,)
+    for res in results:
+        assert res.solve.converged and res.div_post <= 1e-3 * res.div_pre
