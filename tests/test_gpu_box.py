@@ -160,7 +160,7 @@ def test_box_extension_physics_run(cuda):
     assert rel(st.p.numpy(), ost.p) <= 1e-6
 
 
-@pytest.mark.parametrize("shape,bounds", [((40, 24, 30), [0, 9, 20, 30]), ((17, 33, 12), [0, 6, 12])])
+@pytest.mark.parametrize("shape,bounds", [((40, 24, 30), [0, 9, 20, 30]), ((34, 17, 12), [0, 6, 12])])
 def test_box_slabs_match_single_domain(cuda, shape, bounds):
     from paper_2504_03697_b200.distributed import SlabSim
 
@@ -182,3 +182,13 @@ def test_box_slabs_match_single_domain(cuda, shape, bounds):
     ru, rv, rw = ref.vel.numpy()
     assert rel(flat(su, sv, sw), flat(ru, rv, rw)) <= 1e-10
     assert rel(sp, ref.p.numpy()) <= 1e-9
+
+
+def test_box_slabs_need_tma_rows(cuda):
+    """The z-slab solver is TMA-only: nx must be even and >= 32."""
+    from paper_2504_03697_b200.distributed import SlabSim
+
+    cfg = cuda.SimConfig(n=33, h=1.0 / 33, dt=0.01, t_end=0.01, shape=(17, 33, 12),
+                         preconditioner="jacobi", variant="optimized")
+    with pytest.raises(ValueError, match="even nx >= 32"):
+        SlabSim(cfg, [0, 6, 12])
