@@ -35,6 +35,7 @@ extern "C" {
 #define CF_EINVAL (-1)      /* bad argument            (ValueError in the reference) */
 #define CF_ECUDA (-2)       /* CUDA runtime failure */
 #define CF_ENOMEM (-3)
+#define CF_EIO (-4)         /* file I/O failure        (OSError in the reference) */
 
 /* SpMV summation order: CSR order is src/sparse.py:194-201 over the columns
  * of src/sim.py:306-308 (k-1, j-1, i-1, diag, i+1, j+1, k+1); SYM order is
@@ -219,6 +220,23 @@ int cf_helmholtz(int mode, int comp, const double *x, double *y, int nx, int ny,
 int cf_sample_velocity(const double *u, const double *v, const double *w, int n, int ldu,
                        int ldv, int ldw, double h, double px, double py, double pz,
                        double *out_host, void *stream);
+
+/* ---- snapshots (src/snapshots.py) --------------------- */
+/* Cell-centred view of the state (src/snapshots.py:46-62): out (device,
+ * 4*nx*ny*nz doubles) = [uc | vc | wc | p], each i-fastest, uc = 0.5*(u[i] +
+ * u[i+1]) etc.  p is the flat pressure vector. */
+int cf_snapshot_cells(const double *u, const double *v, const double *w, const double *p, int nx, int ny, int nz,
+                      int ldu, int ldv, int ldw, double *out, void *stream);
+/* repr(float(v)) minus a trailing ".0" (src/snapshots.py:65-70) into out
+ * (cap >= 32); returns the length. */
+int cf_format_double(double v, char *out, int cap);
+/* The snapshot CSV of cf_snapshot_cells' output (copied to HOST), x/y/z the
+ * cell centres ((i+0.5)h ...): byte-identical to write_snapshot
+ * (src/snapshots.py:82-108) for any `threads`. */
+int cf_snapshot_write(const char *path, const double *cells_host, int nx, int ny, int nz, double h, int threads);
+/* The same CSV from seven HOST columns (a prebuilt Snapshot). */
+int cf_csv_write_columns(const char *path, const double *x, const double *y, const double *z, const double *u,
+                         const double *v, const double *w, const double *p, int64_t nrows, int threads);
 
 #ifdef __cplusplus
 }

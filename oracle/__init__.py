@@ -511,3 +511,17 @@ def snapshot_columns(s: State, h: float):
     wc = 0.5 * (s.w[:, :, :-1] + s.w[:, :, 1:])
     f = lambda a: a.flatten(order="F")  # noqa: E731
     return {"x": f(x), "y": f(y), "z": f(z), "u": f(uc), "v": f(vc), "w": f(wc), "p": s.p.copy()}
+
+
+def format_value(v: float) -> str:
+    """src/snapshots.py:65-70 -- shortest round-trip repr, integral '.0' dropped."""
+    s = repr(float(v))
+    return s[:-2] if s.endswith(".0") else s
+
+
+def snapshot_csv(cols: dict) -> bytes:
+    """src/snapshots.py:73-108 -- the CSV bytes of a column dict (either mode)."""
+    names = ("x", "y", "z", "u", "v", "w", "p")
+    rows = zip(*(cols[c].tolist() for c in names))
+    body = "".join(",".join(format_value(a) for a in r) + "\n" for r in rows)
+    return ("x,y,z,u,v,w,p\n" + body).encode()

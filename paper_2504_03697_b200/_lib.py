@@ -22,6 +22,7 @@ CF_NOT_CONVERGED = 2
 CF_EINVAL = -1
 CF_ECUDA = -2
 CF_ENOMEM = -3
+CF_EIO = -4
 
 ORDER_CSR = 0
 ORDER_SYM = 1
@@ -81,6 +82,10 @@ _SIGNATURES = {
     "cf_diffuse_slab": ([_vp] * 6 + [_int] * 9 + [_dbl, _dbl, _int, _int, _vp], _int),
     "cf_sample_velocity":([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _dbl, _dbl, _pd, _vp],
                            _int),
+    "cf_snapshot_cells": ([_vp, _vp, _vp, _vp, _int, _int, _int, _int, _int, _int, _vp, _vp], _int),
+    "cf_format_double": ([_dbl, ctypes.c_char_p, _int], _int),
+    "cf_snapshot_write": ([ctypes.c_char_p, _vp, _int, _int, _int, _dbl, _int], _int),
+    "cf_csv_write_columns": ([ctypes.c_char_p, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int], _int),
 }
 
 EXPORTED = tuple(_SIGNATURES)
@@ -114,8 +119,22 @@ def load_library():
     return _lib
 
 
+_host = None
+
+
+def host_library():
+    """The library for its host-only entry points (level schedule, snapshot
+    CSV formatting): those make no CUDA call, so no device is required."""
+    global _host
+    if _lib is not None:
+        return _lib
+    if _host is None:
+        _host = open_library()
+    return _host
+
+
 def last_error() -> str:
-    return load_library().cf_last_error().decode(errors="replace")
+    return (_lib if _lib is not None else host_library()).cf_last_error().decode(errors="replace")
 
 
 def check(rc: int, what: str) -> int:
@@ -125,6 +144,8 @@ def check(rc: int, what: str) -> int:
             raise ValueError(msg)
         if rc == CF_ENOMEM:
             raise MemoryError(msg)
+        if rc == CF_EIO:
+            raise OSError(msg)
         raise RuntimeError(msg)
     return rc
 

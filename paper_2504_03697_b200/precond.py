@@ -110,7 +110,7 @@ def _levels(a, lower, n):
     if isinstance(a, StencilOperator):
         idx = np.arange(n, dtype=np.int64)
         return (idx % a.nx + (idx // a.nx) % a.ny + idx // (a.nx * a.ny)).astype(np.int32)
-    lib = _lib.open_library() if _lib._lib is None else _lib._lib
+    lib = _lib.host_library()
     lv = np.empty(n, dtype=np.int32)
     nl = np.zeros(1, dtype=np.int32)
     _lib.check(lib.cf_level_schedule(n, lower[0].ctypes.data, lower[1].ctypes.data, lv.ctypes.data,

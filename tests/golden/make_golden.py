@@ -179,7 +179,65 @@ def cavity_fixtures():
     save("cavity.npz", **out)
 
 
+REF_CSV = "/root/reference/pkg/tests/data/reference_n8_step3.csv"
+
+
+def snapshot_fixtures():
+    """Byte-level pins of the snapshot writer (src/snapshots.py:65-108):
+    the sha256 of the reference's committed CSV, and the reference writer's
+    output (both modes) on a state with values spanning every branch of the
+    repr format (exponent forms, integral values, signed zeros, subnormals)."""
+    import hashlib
+    import tempfile
+
+    from cavityflow import snapshots
+
+    out = {}
+    with open(REF_CSV, "rb") as f:
+        raw = f.read()
+    out["ref_csv_sha256"] = np.frombuffer(hashlib.sha256(raw).digest(), dtype=np.uint8)
+    out["ref_csv_len"] = np.int64(len(raw))
+    n, h = 6, 0.1
+    cfg = sim.SimConfig(n=n, h=h, dt=0.01, t_end=0.0)
+    st = sim.initial_state(cfg)
+    rng = np.random.default_rng(17)
+
+    def exotic(shape):
+        a = rng.standard_normal(shape) * 10.0 ** rng.integers(-20, 24, size=shape)
+        flat = a.reshape(-1)
+        pick = rng.random(flat.size)
+        flat[pick < 0.1] = np.round(flat[pick < 0.1] * 1e-3 * 10.0 ** rng.integers(0, 8))
+        flat[(pick >= 0.1) & (pick < 0.13)] = 0.0
+        flat[(pick >= 0.13) & (pick < 0.16)] = -0.0
+        flat[(pick >= 0.16) & (pick < 0.18)] = 5e-324 * rng.integers(1, 1000)
+        flat[(pick >= 0.18) & (pick < 0.2)] = np.array([1e16, 1e15, 1e-4, 1e-5, 0.0001234, 123456789012345678.0,
+                                                          9999999999999998.0, 2.0 ** 60, 0.1, 1.0 / 3.0])[
+            rng.integers(0, 10, size=int(((pick >= 0.18) & (pick < 0.2)).sum()))]
+        return a
+
+    st.vel.u[:] = exotic(st.vel.u.shape)
+    st.vel.v[:] = exotic(st.vel.v.shape)
+    st.vel.w[:] = exotic(st.vel.w.shape)
+    st.p.data[:] = exotic(st.p.data.shape)
+    with tempfile.TemporaryDirectory() as d:
+        a, b = os.path.join(d, "a.csv"), os.path.join(d, "b.csv")
+        snapshots.write_snapshot(st, a)
+        snapshots.write_snapshot(st, b, mode="buffered_parallel", threads=3)
+        with open(a, "rb") as f:
+            sa = f.read()
+        with open(b, "rb") as f:
+            assert f.read() == sa
+    out["exotic_h"] = np.float64(h)
+    for c, arr in zip("uvw", st.vel.components()):
+        out[f"exotic_{c}"] = arr.copy()
+    out["exotic_p"] = st.p.data.copy()
+    out["exotic_sha256"] = np.frombuffer(hashlib.sha256(sa).digest(), dtype=np.uint8)
+    out["exotic_len"] = np.int64(len(sa))
+    save("snapshot.npz", **out)
+
+
 if __name__ == "__main__":
+    snapshot_fixtures()
     sparse_fixtures()
     advection_fixtures()
     cavity_fixtures()
