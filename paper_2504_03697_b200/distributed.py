@@ -159,6 +159,8 @@ class SlabSim:
             raise ValueError("the z-slab solver shards Jacobi-PCG only (DIC's sweeps do not shard)")
         if cfg.warm_start:
             raise ValueError("warm_start is not supported by the z-slab solver")
+        if cfg.viscosity > 0.0 and cfg.diffusion != "explicit":
+            raise ValueError("the z-slab step runs explicit diffusion only")
         lib = _lib.load_library()
         self.cfg = cfg
         self.nx, self.ny, self.nz = cfg.spec.dims  # the cube, or a box (extension)
@@ -272,16 +274,15 @@ class SlabSim:
         return m
 
     # ------------------------------------------------------------ the step
-    def step(self):
-        """Advance one time step; returns StepStats (src/sim.py:452-474)."""
-        from .sim import StepStats
-
-        cfg, lib, st = self.cfg, self._lib, _lib.stream()
-        dims = (self.nx, self.ny, self.nz)
+    def _forces(self, lib, st, dims):
+        cfg = self.cfg
         for s in self.slabs:  # forces + walls (src/sim.py:134-149)
             u, v, w = s.ptrs(s.cur)
             _lib.check(lib.cf_forces_bc_slab(u, v, w, *dims, s.z0, s.z1, HALO, *s.ld, cfg.lid_accel * cfg.dt, 1, st),
                        "forces_bc_slab")
+
+    def _advect(self, lib, st, dims):
+        cfg = self.cfg
         self._exchange_vel()
         # the HALO-plane halo covers a backtrace of <= 1 cell in z
         wmax = []
@@ -299,17 +300,22 @@ class SlabSim:
                        "advect_slab")
             s.cur = 1 - s.cur
         self._exchange_vel()  # the divergence (and diffusion) read neighbour planes
-        if cfg.viscosity > 0.0:  # extension: explicit diffusion
-            kdt = cfg.viscosity * cfg.dt / (cfg.h * cfg.h)
-            lid = cfg.lid_velocity
-            for s in self.slabs:
-                u, v, w = s.ptrs(s.cur)
-                nu, nv, nw = s.ptrs(1 - s.cur)
-                _lib.check(lib.cf_diffuse_slab(u, v, w, nu, nv, nw, *dims, s.z0, s.z1, HALO, *s.ld, kdt,
-                                               0.0 if lid is None else float(lid), 0 if lid is None else 1,
-                                               1 if cfg.no_slip else 0, st), "diffuse_slab")
-                s.cur = 1 - s.cur
-            self._exchange_vel()
+
+    def _diffuse(self, lib, st, dims):
+        cfg = self.cfg
+        kdt = cfg.viscosity * cfg.dt / (cfg.h * cfg.h)
+        lid = cfg.lid_velocity
+        for s in self.slabs:
+            u, v, w = s.ptrs(s.cur)
+            nu, nv, nw = s.ptrs(1 - s.cur)
+            _lib.check(lib.cf_diffuse_slab(u, v, w, nu, nv, nw, *dims, s.z0, s.z1, HALO, *s.ld, kdt,
+                                           0.0 if lid is None else float(lid), 0 if lid is None else 1,
+                                           1 if cfg.no_slip else 0, st), "diffuse_slab")
+            s.cur = 1 - s.cur
+        self._exchange_vel()
+
+    def _pressure(self, lib, st, dims, prof):
+        cfg = self.cfg
         maxb = []
         for s in self.slabs:  # b = -(rho/dt) div (src/sim.py:359-360)
             u, v, w = s.ptrs(s.cur)
@@ -318,10 +324,15 @@ class SlabSim:
                                               s.rhs.data_ptr(), ctypes.byref(mx), st), "divergence_slab")
             maxb.append(mx.value)
         div_pre = self._max(maxb) * cfg.dt / cfg.density
-        xs, stats = self.cg.solve([s.rhs for s in self.slabs], cfg.tol, cfg.max_iter, "jacobi")
+        with prof.region("pcg"):
+            xs, stats = self.cg.solve([s.rhs for s in self.slabs], cfg.tol, cfg.max_iter, "jacobi")
         for s, x in zip(self.slabs, xs):
             s.p_owned().copy_(x)
         self._exchange_p()
+        return stats, div_pre
+
+    def _correct(self, lib, st, dims):
+        cfg = self.cfg
         coef = cfg.dt / (cfg.density * cfg.h)
         posts = []
         for s in self.slabs:  # correction + div_post + walls (src/sim.py:426-449)
@@ -333,7 +344,28 @@ class SlabSim:
                        "pressure_correct_slab")
             posts.append(out.value)
             s.cur = 1 - s.cur
-        div_post = self._max(posts)
+        return self._max(posts)
+
+    def step(self, profiler=None):
+        """Advance one time step; returns StepStats (src/sim.py:452-474).
+        ``profiler`` times the reference's step regions (src/sim.py:461-471)."""
+        from .profiling import NULL_PROFILER
+        from .sim import StepStats
+
+        prof = NULL_PROFILER if profiler is None else profiler
+        lib, st = self._lib, _lib.stream()
+        dims = (self.nx, self.ny, self.nz)
+        with prof.region("applyForces"):
+            self._forces(lib, st, dims)
+        with prof.region("solveAdvection"):
+            self._advect(lib, st, dims)
+        if self.cfg.viscosity > 0.0:  # extension: explicit diffusion (SURVEY.md §8 f2)
+            with prof.region("solveDiffusion"):
+                self._diffuse(lib, st, dims)
+        with prof.region("solvePressureCorrection"):
+            stats, div_pre = self._pressure(lib, st, dims, prof)
+        with prof.region("applyPressureCorrection"):
+            div_post = self._correct(lib, st, dims)
         self.step_count += 1
         return StepStats(solve=stats, div_pre=div_pre, div_post=div_post)
 
@@ -353,3 +385,74 @@ def init_slab_cg(n: int, h: float, order: str = "sym", nz: int | None = None) ->
     scg = SlabCG(n, n, nz, h, order, bounds=[dec.z0, dec.z1], nranks=world, rank=rank, uid=obj[0], lo_rank=lo,
                  hi_rank=hi)
     return scg, dec
+
+
+def run(cfg, slabs: int | None = None, distributed: bool = False):
+    """``sim.run`` (src/sim.py:477-505) over z-slabs: ``distributed=True``
+    gives this rank its slab of a torch.distributed job (one GPU per rank);
+    otherwise ``slabs`` consecutive slabs are emulated on this device.
+    Returns (SlabSim, RunReport) with the reference's region names; no
+    snapshot output (gather() the state and write it on one rank)."""
+    import time
+
+    from .profiling import Profiler
+    from .sim import ROOT_REGION, RunReport
+
+    if cfg.output_dir is not None:
+        raise ValueError("z-slab runs write no snapshots: set output_dir=None and gather() the state")
+    nx, ny, nz = cfg.spec.dims
+    if distributed:
+        import torch.distributed as dist
+
+        dec = SlabDecomposition(nx, ny, nz, dist.get_world_size(), dist.get_rank())
+        bounds = [dec.z0, dec.z1]
+    else:
+        bounds = SlabDecomposition.bounds(nz, 1 if slabs is None else int(slabs)).tolist()
+    sim = SlabSim(cfg, bounds, distributed=distributed)
+    prof = Profiler()
+    report = RunReport()
+    t0 = time.perf_counter()
+    with prof.region(ROOT_REGION):
+        for _ in range(cfg.num_steps):
+            report.steps.append(sim.step(prof))
+    report.regions = prof.stats()
+    report.wall_seconds = time.perf_counter() - t0
+    return sim, report
+
+
+def _sweep_worker(argv=None) -> int:
+    """One rank of profiling.scaling_sweep's multi-GPU leg (launched by torchrun)."""
+    import argparse
+    import dataclasses
+    import json
+    import os
+
+    import torch.distributed as dist
+
+    from .profiling import save_report
+    from .sim import SimConfig
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", required=True)
+    ap.add_argument("--out", required=True)
+    a = ap.parse_args(argv)
+    kw = json.loads(a.config)
+    if kw.get("shape") is not None:
+        kw["shape"] = tuple(kw["shape"])
+    names = {f.name for f in dataclasses.fields(SimConfig)}
+    cfg = SimConfig(**{k: v for k, v in kw.items() if k in names})
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        _, report = run(cfg, distributed=True)
+        if dist.get_rank() == 0:
+            save_report(report.regions, a.out)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(_sweep_worker())

@@ -413,14 +413,16 @@ def step(state: SimState, cfg: SimConfig, cache: PoissonCache | None = None, poo
     return StepStats(solve=stats, div_pre=div_pre, div_post=div_post)
 
 
-def run(cfg: SimConfig):
-    """Run the configured simulation (src/sim.py:477-505)."""
+def run(cfg: SimConfig, profiler=None):
+    """Run the configured simulation (src/sim.py:477-505).  ``profiler``
+    (extension) is a fresh ``Profiler`` to time with, e.g.
+    ``Profiler(timer="events")``; the default is the reference's wall clock."""
     from .profiling import Profiler
     from . import snapshots
 
     state = initial_state(cfg)
     report = RunReport()
-    profiler = Profiler()
+    profiler = Profiler() if profiler is None else profiler
     cache = PoissonCache()
     if cfg.output_dir is not None:
         os.makedirs(cfg.output_dir, exist_ok=True)

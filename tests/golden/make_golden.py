@@ -236,7 +236,44 @@ def snapshot_fixtures():
     save("snapshot.npz", **out)
 
 
+def profiling_fixtures():
+    """The reference's report renderers and writers (src/bench.py:159-324) on
+    fixed region records: render_report, save_report, compare_reports,
+    render_comparison and write_scaling_csv outputs, as text."""
+    import json
+    import tempfile
+
+    from cavityflow import bench
+
+    R = bench.RegionStats
+    a = [R("cavityflow", None, 1, 12.5, 1.0), R("write_to_file", "cavityflow", 4, 0.75, 0.06),
+         R("applyForces", "cavityflow", 3, 0.01, 0.0008), R("solveAdvection", "cavityflow", 3, 1.2, 0.096),
+         R("solvePressureCorrection", "cavityflow", 3, 10.0, 0.8), R("pcg", "solvePressureCorrection", 3, 9.5, 0.76),
+         R("spmv", "pcg", 300, 4.0, 0.32), R("dot", "pcg", 900, 1.5, 0.12),
+         R("applyPressureCorrection", "cavityflow", 3, 0.4, 0.032), R("other_root", None, 2, 0.0, 0.0)]
+    b = [R("cavityflow", None, 1, 3.25, 1.0), R("applyForces", "cavityflow", 3, 0.02, 0.006),
+         R("solvePressureCorrection", "cavityflow", 3, 2.0, 0.6), R("pcg", "solvePressureCorrection", 3, 1.9, 0.58),
+         R("fused_cg", "pcg", 3, 1.8, 0.55), R("write_to_file", "cavityflow", 4, 0.5, 0.15)]
+    rows = [(1, "cavityflow", 12.5), (2, "pcg", 0.1 + 0.2), (8, "dot", 1e-7)]
+    with tempfile.TemporaryDirectory() as d:
+        bench.save_report(a, os.path.join(d, "r.json"))
+        with open(os.path.join(d, "r.json"), encoding="utf-8") as f:
+            saved = f.read()
+        bench.write_scaling_csv(rows, os.path.join(d, "s.csv"))
+        with open(os.path.join(d, "s.csv"), encoding="utf-8", newline="") as f:
+            scaling = f.read()
+    cmp = bench.compare_reports(a, b)
+    out = {"a": [vars(r) for r in a], "b": [vars(r) for r in b], "scaling_rows": rows,
+           "render_a": bench.render_report(a), "render_b": bench.render_report(b), "saved_a": saved,
+           "compare": cmp, "render_compare": bench.render_comparison(cmp), "scaling_csv": scaling}
+    path = os.path.join(HERE, "profiling.json")
+    with open(path, "w", encoding="utf-8") as f:
+        json.dump(out, f, indent=1, ensure_ascii=False)
+    print("wrote", path)
+
+
 if __name__ == "__main__":
+    profiling_fixtures()
     snapshot_fixtures()
     sparse_fixtures()
     advection_fixtures()
