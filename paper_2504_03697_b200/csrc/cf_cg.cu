@@ -20,6 +20,8 @@
 // summation order differs (a fixed two-level tree, deterministic).
 // The iteration loop is a CUDA graph with a conditional WHILE node whose
 // condition is cleared on the device when the solve stops.
+#include <algorithm>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -246,6 +248,42 @@ __global__ void __launch_bounds__(kMarchThreads) cg_rz_kernel(long long n, const
 }
 
 #include "cf_cg_tma.cuh"
+#include "cf_cg_pair.cuh"
+
+// Host: geometry of the pair-march kernels -- 64 x kPairRows tiles, z cut into
+// chunks of ~kPairPlanes planes (measured: enough CTAs in flight to keep HBM
+// busy, few enough partials for the last block).  env_name overrides.
+constexpr int kPairPlanes = 32;
+PairGeom pair_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, const char *env_name)
+{
+    PairGeom g{nx, ny, nz, lo_halo, hi_halo, (nx + kPairX - 1) / kPairX, (ny + kPairRows - 1) / kPairRows, 1};
+    int c = (nz + kPairPlanes - 1) / kPairPlanes;
+    if (const char *e = env_name ? getenv(env_name) : nullptr) {
+        const int v = atoi(e);
+        if (v >= 1) c = v;
+    }
+    g.nchunk = c < 1 ? 1 : (c > nz ? nz : c);
+    return g;
+}
+
+// Which form runs each CG kernel: the register pair march, the TMA pipeline,
+// or the scalar LDG march (odd nx).  Defaults (measured, tools/kernel_matrix.sh,
+// 256^3 / 512^3): direction = pair march run top-down, update = TMA -- 209.6 /
+// 1709 us per iteration against 217.3 / 1738 for TMA + TMA.
+// CF_CG_DIR / CF_CG_UPD = "pair" | "tma" | "ldg" override.
+enum KernKind { KK_LDG = 0, KK_TMA = 1, KK_PAIR = 2 };
+int kern_kind(const char *env_name, int deflt, bool tma_ok, bool pair_ok)
+{
+    int k = deflt;
+    if (const char *e = getenv(env_name)) {
+        if (!strcmp(e, "pair")) k = KK_PAIR;
+        else if (!strcmp(e, "tma")) k = KK_TMA;
+        else if (!strcmp(e, "ldg")) k = KK_LDG;
+    }
+    if (k == KK_TMA && !tma_ok) k = pair_ok ? KK_PAIR : KK_LDG;
+    if (k == KK_PAIR && !pair_ok) k = KK_LDG;
+    return k;
+}
 
 // ---------------------------------------------------------------- small grids
 // Whole solve in ONE block: r, p, x live in shared memory (16^3: 96 KB), the
@@ -361,6 +399,9 @@ struct cf_cg {
     int direct = 0, direct_batch = 8;
     // TMA-staged kernels (even nx >= 32; CF_NO_TMA=1 forces the LDG march)
     bool tma = false;
+    // kernel form per CG kernel (cf::KernKind) and the pair-march geometry
+    int kind_dir = 0, kind_upd = 0;
+    cf::PairGeom pg_dir{}, pg_upd{};
     cf::TmaGeom geom_dir{}, geom_upd{};
     CUtensorMap m_r{}, m_z{}, m_p[2]{}, m_ri{}, m_xi{};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -380,25 +421,42 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
     for (int half = 0; half < 2; ++half) {
         const double *p_old = ws->p[half];
         double *p_new = ws->p[half ^ 1];
-        if (PK != PK_JVEC && ws->tma) {
-            const TmaGeom &gd = ws->geom_dir, &gu = ws->geom_upd;
+        // the TMA forms have no per-cell Jacobi vector
+        const int kd = (PK == PK_JVEC && ws->kind_dir == KK_TMA) ? KK_PAIR : ws->kind_dir;
+        const int ku = (PK == PK_JVEC && ws->kind_upd == KK_TMA) ? KK_PAIR : ws->kind_upd;
+        if (kd == KK_TMA) {
+            const TmaGeom &gd = ws->geom_dir;
             cg_dir_tma<ORDER, PK><<<gd.ntx * gd.nty * gd.nchunk, kWSThreads, kDirSmem, s>>>(
                 PK == PK_ZVEC ? ws->m_z : ws->m_r, ws->m_p[half], gd, ws->off, ws->diag, p_new, zc, ws->sc,
                 ws->partials, ws->tk, nullptr);
             CF_CHECK_LAUNCH("cg_dir_tma");
+        } else if (kd == KK_PAIR) {
+            cg_dir_pair<ORDER, PK><<<ws->pg_dir.ctas(), kPairThreads, 0, s>>>(
+                ws->pg_dir, ws->off, ws->diag, PK == PK_ZVEC ? ws->zbuf : ws->r, ws->jd, p_old, p_new, zc, ws->sc,
+                ws->partials, ws->tk, nullptr);
+            CF_CHECK_LAUNCH("cg_dir_pair");
+        } else {
+            cg_dir_kernel<ORDER, PK><<<ws->grid_dir, kMarchThreads, 0, s>>>(
+                ws->bx, ws->off, ws->diag, ws->r, ws->jd, ws->zbuf, p_old, p_new, zc, ws->sc, ws->partials,
+                ws->tk);
+            CF_CHECK_LAUNCH("cg_dir_kernel");
+        }
+        if (ku == KK_TMA) {
+            const TmaGeom &gu = ws->geom_upd;
             cg_update_tma<ORDER, PK><<<gu.ntx * gu.nty * gu.nchunk, kWSThreads, kUpdSmem, s>>>(
                 ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc,
                 ws->partials, ws->tk, use_cond, cond, nullptr);
             CF_CHECK_LAUNCH("cg_update_tma");
+        } else if (ku == KK_PAIR) {
+            cg_update_pair<ORDER, PK><<<ws->pg_upd.ctas(), kPairThreads, 0, s>>>(
+                ws->pg_upd, ws->off, ws->diag, p_new, ws->r, ws->x, ws->jd, zc, ws->sc, ws->partials, ws->tk,
+                use_cond, cond, nullptr);
+            CF_CHECK_LAUNCH("cg_update_pair");
         } else {
-        cg_dir_kernel<ORDER, PK><<<ws->grid_dir, kMarchThreads, 0, s>>>(
-            ws->bx, ws->off, ws->diag, ws->r, ws->jd, ws->zbuf, p_old, p_new, zc, ws->sc, ws->partials,
-            ws->tk);
-        CF_CHECK_LAUNCH("cg_dir_kernel");
-        cg_update_kernel<ORDER, PK><<<ws->grid_upd, kMarchThreads, 0, s>>>(
-            ws->bx, ws->off, ws->diag, p_new, ws->r, ws->x, ws->jd, zc, ws->sc, ws->partials, ws->tk, use_cond,
-            cond);
-        CF_CHECK_LAUNCH("cg_update_kernel");
+            cg_update_kernel<ORDER, PK><<<ws->grid_upd, kMarchThreads, 0, s>>>(
+                ws->bx, ws->off, ws->diag, p_new, ws->r, ws->x, ws->jd, zc, ws->sc, ws->partials, ws->tk, use_cond,
+                cond);
+            CF_CHECK_LAUNCH("cg_update_kernel");
         }
         if (PK == PK_ZVEC) {
             // z = M^-1 r by the level sweeps, then r.z and beta (src/solver.py:163-166)
@@ -558,6 +616,11 @@ static void set_grids(cf_cg *ws)
         if (const char *e = getenv("CF_TMA_CHUNKS_DIR")) ws->geom_dir.nchunk = atoi(e) > 0 ? atoi(e) : 1;
         if (const char *e = getenv("CF_TMA_CHUNKS_UPD")) ws->geom_upd.nchunk = atoi(e) > 0 ? atoi(e) : 1;
     }
+    const bool pair_ok = ws->bx.nx % 2 == 0 && !(no_tma && atoi(no_tma) > 0);
+    ws->pg_dir = pair_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, "CF_PAIR_CHUNKS_DIR");
+    ws->pg_upd = pair_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, "CF_PAIR_CHUNKS_UPD");
+    ws->kind_dir = kern_kind("CF_CG_DIR", KK_PAIR, ws->tma, pair_ok);
+    ws->kind_upd = kern_kind("CF_CG_UPD", KK_TMA, ws->tma, pair_ok);
 }
 
 static bool build_maps(cf_cg *ws)
@@ -602,6 +665,7 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
         if (g1 > maxg) maxg = g1;
         if (g2 > maxg) maxg = g2;
     }
+    maxg = std::max(maxg, std::max(ws->pg_dir.ctas(), ws->pg_upd.ctas()));
     size_t vec = (size_t)ws->n * sizeof(double);
     cudaError_t e = cudaSuccess;
     for (double **b : {&ws->r, &ws->x, &ws->p[0], &ws->p[1]})
@@ -618,7 +682,11 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
         cf_cg_destroy(ws);
         return rc;
     }
-    if (ws->tma && !cf::build_maps(ws)) ws->tma = false;  // fall back to the LDG march
+    if (ws->tma && !cf::build_maps(ws)) {  // TMA cannot describe the arrays: pair / LDG forms
+        ws->tma = false;
+        if (ws->kind_dir == cf::KK_TMA) ws->kind_dir = ws->bx.nx % 2 == 0 ? cf::KK_PAIR : cf::KK_LDG;
+        if (ws->kind_upd == cf::KK_TMA) ws->kind_upd = ws->bx.nx % 2 == 0 ? cf::KK_PAIR : cf::KK_LDG;
+    }
     *out = ws;
     return CF_OK;
 }
