@@ -247,6 +247,18 @@ __global__ void __launch_bounds__(kMarchThreads) cg_rz_kernel(long long n, const
     }
 }
 
+// Deferred-x epilogue: a solve that stopped after a skipping iteration (odd
+// iteration count) still owes x += alpha * p of that iteration; p is the
+// buffer the skipping half read as its new direction (p[1]).
+__global__ void __launch_bounds__(kMarchThreads) cg_x_fixup(long long n, double *__restrict__ x,
+                                                           const double *__restrict__ p, const CgScalars *sc)
+{
+    if ((sc->it & 1) == 0) return;
+    const double alpha = sc->alpha;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[i] = x[i] + alpha * p[i];  // src/solver.py:155
+}
+
 #include "cf_cg_tma.cuh"
 #include "cf_cg_pair.cuh"
 
@@ -403,7 +415,9 @@ struct cf_cg {
     int kind_dir = 0, kind_upd = 0;
     cf::PairGeom pg_dir{}, pg_upd{};
     cf::TmaGeom geom_dir{}, geom_upd{};
-    CUtensorMap m_r{}, m_z{}, m_p[2]{}, m_ri{}, m_xi{};
+    CUtensorMap m_r{}, m_z{}, m_p[2]{}, m_ri{}, m_xi{}, m_pi[2]{};
+    // x updated once per two iterations (XM_SKIP / XM_DOUBLE, cf_cg_common.cuh)
+    bool defer_x = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_loop_ms = 0.f;
     // one instantiated while-graph per (preconditioner kind)
@@ -443,14 +457,34 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
         }
         if (ku == KK_TMA) {
             const TmaGeom &gu = ws->geom_upd;
-            cg_update_tma<ORDER, PK><<<gu.ntx * gu.nty * gu.nchunk, kWSThreads, kUpdSmem, s>>>(
-                ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc,
-                ws->partials, ws->tk, use_cond, cond, nullptr);
+            const int nb = gu.ntx * gu.nty * gu.nchunk;
+            if (!ws->defer_x)
+                cg_update_tma<ORDER, PK, XM_EACH><<<nb, kWSThreads, kUpdSmem, s>>>(
+                    ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc,
+                    ws->sc, ws->partials, ws->tk, use_cond, cond, nullptr);
+            else if (half == 0)
+                cg_update_tma<ORDER, PK, XM_SKIP><<<nb, kWSThreads, kUpdSmem, s>>>(
+                    ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc,
+                    ws->sc, ws->partials, ws->tk, use_cond, cond, nullptr);
+            else
+                cg_update_tma<ORDER, PK, XM_DOUBLE><<<nb, kWSThreads, kUpdSmem, s>>>(
+                    ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc,
+                    ws->sc, ws->partials, ws->tk, use_cond, cond, nullptr);
             CF_CHECK_LAUNCH("cg_update_tma");
         } else if (ku == KK_PAIR) {
-            cg_update_pair<ORDER, PK><<<ws->pg_upd.ctas(), kPairThreads, 0, s>>>(
-                ws->pg_upd, ws->off, ws->diag, p_new, ws->r, ws->x, ws->jd, zc, ws->sc, ws->partials, ws->tk,
-                use_cond, cond, nullptr);
+            const int nb = ws->pg_upd.ctas();
+            if (!ws->defer_x)
+                cg_update_pair<ORDER, PK, XM_EACH><<<nb, kPairThreads, 0, s>>>(
+                    ws->pg_upd, ws->off, ws->diag, p_new, p_old, ws->r, ws->x, ws->jd, zc, ws->sc, ws->partials,
+                    ws->tk, use_cond, cond, nullptr);
+            else if (half == 0)
+                cg_update_pair<ORDER, PK, XM_SKIP><<<nb, kPairThreads, 0, s>>>(
+                    ws->pg_upd, ws->off, ws->diag, p_new, p_old, ws->r, ws->x, ws->jd, zc, ws->sc, ws->partials,
+                    ws->tk, use_cond, cond, nullptr);
+            else
+                cg_update_pair<ORDER, PK, XM_DOUBLE><<<nb, kPairThreads, 0, s>>>(
+                    ws->pg_upd, ws->off, ws->diag, p_new, p_old, ws->r, ws->x, ws->jd, zc, ws->sc, ws->partials,
+                    ws->tk, use_cond, cond, nullptr);
             CF_CHECK_LAUNCH("cg_update_pair");
         } else {
             cg_update_kernel<ORDER, PK><<<ws->grid_upd, kMarchThreads, 0, s>>>(
@@ -495,6 +529,16 @@ static int build_graph(cf_cg *ws, cudaStream_t s, double zc)
     cudaStreamDestroy(cs);
     if (rc != CF_OK) return rc;
     CF_CUDA(e);
+    if (ws->defer_x) {  // x += alpha * p owed by a final skipping iteration
+        cudaKernelNodeParams kp = {};
+        void *args[] = {&ws->n, &ws->x, &ws->p[1], &ws->sc};
+        kp.func = (void *)cg_x_fixup;
+        kp.gridDim = dim3(ws->grid_init);
+        kp.blockDim = dim3(kMarchThreads);
+        kp.kernelParams = args;
+        cudaGraphNode_t fix;
+        CF_CUDA(cudaGraphAddKernelNode(&fix, g, &node, 1, &kp));
+    }
     cudaGraphExec_t exec;
     CF_CUDA(cudaGraphInstantiate(&exec, g, 0));
     ws->graph[PK] = g;
@@ -557,6 +601,10 @@ static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, c
             CF_CUDA(cudaStreamSynchronize(s));
             if (ws->sc_host->done) break;
         }
+        if (ws->defer_x) {
+            cg_x_fixup<<<ws->grid_init, kMarchThreads, 0, s>>>(ws->n, ws->x, ws->p[1], ws->sc);
+            CF_CHECK_LAUNCH("cg_x_fixup");
+        }
         CF_CUDA(cudaEventRecord(ws->ev1, s));
         return CF_OK;
     }
@@ -588,6 +636,15 @@ static int solve_dispatch(cf_cg *ws, int pk, const double *b, const double *x0, 
     }
 }
 
+template <int ORDER, int XM>
+static void set_upd_smem()
+{
+    cudaFuncSetAttribute(cg_update_tma<ORDER, PK_NONE, XM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem);
+    cudaFuncSetAttribute(cg_update_tma<ORDER, PK_JCONST, XM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kUpdSmem);
+    cudaFuncSetAttribute(cg_update_tma<ORDER, PK_ZVEC, XM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem);
+}
+
 template <int ORDER>
 static void set_grids(cf_cg *ws)
 {
@@ -605,10 +662,9 @@ static void set_grids(cf_cg *ws)
         cudaFuncSetAttribute(cg_dir_tma<ORDER, PK_NONE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDirSmem);
         cudaFuncSetAttribute(cg_dir_tma<ORDER, PK_JCONST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDirSmem);
         cudaFuncSetAttribute(cg_dir_tma<ORDER, PK_ZVEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDirSmem);
-        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_NONE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem);
-        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_JCONST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kUpdSmem);
-        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_ZVEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem);
+        set_upd_smem<ORDER, XM_EACH>();
+        set_upd_smem<ORDER, XM_SKIP>();
+        set_upd_smem<ORDER, XM_DOUBLE>();
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bd, cg_dir_tma<ORDER, PK_JCONST>, kWSThreads, kDirSmem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, cg_update_tma<ORDER, PK_JCONST>, kWSThreads, kUpdSmem);
         ws->geom_dir = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bd > 0 ? bd : 1);
@@ -621,6 +677,8 @@ static void set_grids(cf_cg *ws)
     ws->pg_upd = pair_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, "CF_PAIR_CHUNKS_UPD");
     ws->kind_dir = kern_kind("CF_CG_DIR", KK_PAIR, ws->tma, pair_ok);
     ws->kind_upd = kern_kind("CF_CG_UPD", KK_TMA, ws->tma, pair_ok);
+    const char *dx = getenv("CF_CG_DEFER_X");
+    ws->defer_x = ws->kind_upd != KK_LDG && !(dx && atoi(dx) == 0);
 }
 
 static bool build_maps(cf_cg *ws)
@@ -628,7 +686,9 @@ static bool build_maps(cf_cg *ws)
     const int nx = ws->bx.nx, ny = ws->bx.ny, nz = ws->bx.nz;
     bool ok = make_map(&ws->m_r, ws->r, nx, ny, nz, kHX, kHY) && make_map(&ws->m_p[0], ws->p[0], nx, ny, nz, kHX, kHY) &&
               make_map(&ws->m_p[1], ws->p[1], nx, ny, nz, kHX, kHY) &&
-              make_map(&ws->m_ri, ws->r, nx, ny, nz, kTTX, kTTY) && make_map(&ws->m_xi, ws->x, nx, ny, nz, kTTX, kTTY);
+              make_map(&ws->m_ri, ws->r, nx, ny, nz, kTTX, kTTY) && make_map(&ws->m_xi, ws->x, nx, ny, nz, kTTX, kTTY) &&
+              make_map(&ws->m_pi[0], ws->p[0], nx, ny, nz, kTTX, kTTY) &&
+              make_map(&ws->m_pi[1], ws->p[1], nx, ny, nz, kTTX, kTTY);
     return ok;
 }
 
@@ -686,6 +746,7 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
         ws->tma = false;
         if (ws->kind_dir == cf::KK_TMA) ws->kind_dir = ws->bx.nx % 2 == 0 ? cf::KK_PAIR : cf::KK_LDG;
         if (ws->kind_upd == cf::KK_TMA) ws->kind_upd = ws->bx.nx % 2 == 0 ? cf::KK_PAIR : cf::KK_LDG;
+        if (ws->kind_upd == cf::KK_LDG) ws->defer_x = false;
     }
     *out = ws;
     return CF_OK;

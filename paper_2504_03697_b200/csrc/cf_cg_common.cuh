@@ -10,11 +10,22 @@ enum PrecKind { PK_NONE = 0, PK_JCONST = 1, PK_JVEC = 2, PK_ZVEC = 3 };
 
 struct CgScalars {
     double rz, alpha, beta, pap, rr, norm_b, res, tol;
+    double alpha_prev;  // alpha of the previous iteration (deferred x update, XM_DOUBLE)
     long long it, max_iter;
     int done, status;  // status: 0 running, 1 converged, 2 max_iter, 3 breakdown
 };
 
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_BREAKDOWN = 3 };
+
+// x-update modes of the update kernels.  The solution is only read at the
+// end, so the loop body (two iterations, p buffers swapped) updates x once:
+// the first iteration skips it, the second applies both steps in order,
+//   x = (x + alpha_prev * p_prev) + alpha * p,
+// the same two roundings as two separate updates (src/solver.py:155), saving
+// 16 N of the 128 N a pair of iterations moves (+8 N for reading p_prev).
+// A solve that stops after a skipping iteration is finished by
+// cg_x_fixup (x += alpha * p_prev when the iteration count is odd).
+enum { XM_EACH = 0, XM_SKIP = 1, XM_DOUBLE = 2 };
 
 struct CgTickets {
     unsigned int init, dir, upd, pad;
@@ -39,6 +50,7 @@ __device__ __forceinline__ void scalar_after_dir(CgScalars *sc, double pap)
         sc->status = ST_BREAKDOWN;
         sc->done = 1;
     } else {
+        sc->alpha_prev = sc->alpha;
         sc->alpha = sc->rz / pap;  // :153
     }
 }

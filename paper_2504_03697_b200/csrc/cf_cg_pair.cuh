@@ -252,9 +252,11 @@ __global__ void __launch_bounds__(kPairThreads, 8) cg_dir_pair(PairGeom g, doubl
 // ---------------------------------------------------------------- update
 // Ap recomputed from p, x += alpha p, r += (-alpha) Ap, partial r.r (and r.z
 // for Jacobi/none); last block -> convergence test and beta.
-template <int ORDER, int PK>
+template <int ORDER, int PK, int XM = XM_EACH>
 __global__ void __launch_bounds__(kPairThreads, 8) cg_update_pair(PairGeom g, double off, double diag,
-                                                               const double *__restrict__ p, double *__restrict__ r,
+                                                               const double *__restrict__ p,
+                                                               const double *__restrict__ p_prev,
+                                                               double *__restrict__ r,
                                                                double *__restrict__ x,
                                                                const double *__restrict__ jd, double zc,
                                                                CgScalars *sc, double *partials, CgTickets *tk,
@@ -270,14 +272,21 @@ __global__ void __launch_bounds__(kPairThreads, 8) cg_update_pair(PairGeom g, do
     const PairCoords c = pair_coords(g);
     struct Epi {
         double *r, *x;
-        const double *jd;
-        double alpha, malpha, zc;
+        const double *jd, *q;
+        double alpha, malpha, zc, alpha_prev;
         double rr, rz;
         __device__ __forceinline__ void cell(long long o, double2 cc, double a0, double a1)
         {
-            const double2 xo = __ldcs(reinterpret_cast<const double2 *>(x + o));
             const double2 ro = __ldcs(reinterpret_cast<const double2 *>(r + o));
-            __stcs(reinterpret_cast<double2 *>(x + o), make_double2(xo.x + alpha * cc.x, xo.y + alpha * cc.y));
+            if (XM == XM_EACH) {
+                const double2 xo = __ldcs(reinterpret_cast<const double2 *>(x + o));
+                __stcs(reinterpret_cast<double2 *>(x + o), make_double2(xo.x + alpha * cc.x, xo.y + alpha * cc.y));
+            } else if (XM == XM_DOUBLE) {  // the skipped step first, then this one
+                const double2 xo = __ldcs(reinterpret_cast<const double2 *>(x + o));
+                const double2 qo = __ldcs(reinterpret_cast<const double2 *>(q + o));
+                const double x0 = xo.x + alpha_prev * qo.x, x1 = xo.y + alpha_prev * qo.y;
+                __stcs(reinterpret_cast<double2 *>(x + o), make_double2(x0 + alpha * cc.x, x1 + alpha * cc.y));
+            }
             const double r0 = ro.x + malpha * a0, r1 = ro.y + malpha * a1;  // src/solver.py:155-157
             __stcs(reinterpret_cast<double2 *>(r + o), make_double2(r0, r1));
             rr = rr + r0 * r0;
@@ -288,7 +297,7 @@ __global__ void __launch_bounds__(kPairThreads, 8) cg_update_pair(PairGeom g, do
             }
         }
         __device__ __forceinline__ void halo(long long, double2) {}
-    } epi{r, x, jd, sc->alpha, -sc->alpha, zc, 0.0, 0.0};
+    } epi{r, x, jd, p_prev, sc->alpha, -sc->alpha, zc, sc->alpha_prev, 0.0, 0.0};
     if (c.row_ok) pair_march<ORDER, false>(c, g, off, diag, UpdSrc{p}, epi);
     double rr = block_sum<kPairThreads>(epi.rr, red);
     double rz = PK != PK_ZVEC ? block_sum<kPairThreads>(epi.rz, red) : 0.0;

@@ -101,10 +101,10 @@ __global__ void __launch_bounds__(kWSThreads, 4) cg_dir_tma(const __grid_constan
 }
 
 // ---------------------------------------------------------------- update
-template <int PK>
+template <int PK, int XM>
 struct UpdPolicy {
-    const double *sp, *sr, *sx;
-    double alpha, malpha, zc;
+    const double *sp, *sr, *sx, *sq;
+    double alpha, malpha, zc, alpha_prev;
     double *r, *x;
     long long nx, plane;
     double rr = 0.0, rz = 0.0;
@@ -115,8 +115,15 @@ struct UpdPolicy {
     {
         const int k = m.ty * kTTX + 2 * m.tx2;
         const long long gi = m.i + nx * m.j + plane * z;
-        const double2 xo = ld2(sx + s * kInt + k), ro = ld2(sr + s * kInt + k);
-        st2(x + gi, xo.x + alpha * c.x, xo.y + alpha * c.y);            // src/solver.py:155
+        const double2 ro = ld2(sr + s * kInt + k);
+        if (XM == XM_EACH) {
+            const double2 xo = ld2(sx + s * kInt + k);
+            st2(x + gi, xo.x + alpha * c.x, xo.y + alpha * c.y);  // src/solver.py:155
+        } else if (XM == XM_DOUBLE) {  // the skipped step first, then this one
+            const double2 xo = ld2(sx + s * kInt + k), q = ld2(sq + s * kInt + k);
+            const double x0 = xo.x + alpha_prev * q.x, x1 = xo.y + alpha_prev * q.y;
+            st2(x + gi, x0 + alpha * c.x, x1 + alpha * c.y);
+        }
         const double r0 = ro.x + malpha * a0, r1 = ro.y + malpha * a1;  // :157
         st2(r + gi, r0, r1);
         rr = rr + r0 * r0;
@@ -129,12 +136,16 @@ struct UpdPolicy {
     __device__ __forceinline__ void halo(const MarchCoords &, int, double2) {}
 };
 
-template <int ORDER, int PK>
+// interior boxes staged per plane: r, plus x (XM_EACH / XM_DOUBLE), plus p_prev (XM_DOUBLE)
+template <int XM>
+__host__ __device__ constexpr int upd_interiors() { return XM == XM_SKIP ? 1 : (XM == XM_EACH ? 2 : 3); }
+
+template <int ORDER, int PK, int XM = XM_EACH>
 __global__ void __launch_bounds__(kWSThreads) cg_update_tma(
     const __grid_constant__ CUtensorMap mp, const __grid_constant__ CUtensorMap mr,
-    const __grid_constant__ CUtensorMap mx, TmaGeom g, double off, double diag, double *__restrict__ r,
-    double *__restrict__ x, double zc, CgScalars *sc, double *partials, CgTickets *tk, int use_cond,
-    cudaGraphConditionalHandle cond, double *red_out)
+    const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mq, TmaGeom g, double off,
+    double diag, double *__restrict__ r, double *__restrict__ x, double zc, CgScalars *sc, double *partials,
+    CgTickets *tk, int use_cond, cudaGraphConditionalHandle cond, double *red_out)
 {
     extern __shared__ unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
@@ -147,23 +158,26 @@ __global__ void __launch_bounds__(kWSThreads) cg_update_tma(
     double *const sp = aligned_smem(smem_raw);
     double *const sr = sp + kStages * kBoxStride;
     double *const sx = sr + kStages * kInt;
+    double *const sq = sx + kStages * kInt;
     const double alpha = sc->alpha;
     const MarchCoords m = march_coords(g);
-    UpdPolicy<PK> pol{sp, sr, sx, alpha, -alpha, zc, r, x, g.nx, (long long)g.nx * g.ny};
+    UpdPolicy<PK, XM> pol{sp, sr, sx, sq, alpha, -alpha, zc, sc->alpha_prev, r, x, g.nx, (long long)g.nx * g.ny};
     init_ws_bars(full, empty);
     if (threadIdx.x >= kPThreads) {  // producer warp
         if (threadIdx.x == kPThreads) {
             prefetch_map(&mp);
             prefetch_map(&mr);
-            prefetch_map(&mx);
+            if (XM != XM_SKIP) prefetch_map(&mx);
+            if (XM == XM_DOUBLE) prefetch_map(&mq);
             ws_produce(m.nplanes, full, empty, [&](int q, int s, uint64_t *bar) {
                 const int z = m.zs + q;
-                const bool own = z >= m.z0 && z < m.z1;  // r and x only for owned planes
-                mbar_expect_tx(bar, kBoxBytes + (own ? 2 * kIntBytes : 0));
+                const bool own = z >= m.z0 && z < m.z1;  // r, x, p_prev only for owned planes
+                mbar_expect_tx(bar, kBoxBytes + (own ? upd_interiors<XM>() * kIntBytes : 0));
                 tma_load_3d(sp + s * kBoxStride, &mp, m.bx0, m.by0, z + g.lo_halo, bar);
                 if (own) {
                     tma_load_3d(sr + s * kInt, &mr, m.x0, m.y0, z + g.lo_halo, bar);
-                    tma_load_3d(sx + s * kInt, &mx, m.x0, m.y0, z + g.lo_halo, bar);
+                    if (XM != XM_SKIP) tma_load_3d(sx + s * kInt, &mx, m.x0, m.y0, z + g.lo_halo, bar);
+                    if (XM == XM_DOUBLE) tma_load_3d(sq + s * kInt, &mq, m.x0, m.y0, z + g.lo_halo, bar);
                 }
             });
         }
@@ -191,4 +205,4 @@ __global__ void __launch_bounds__(kWSThreads) cg_update_tma(
 }
 
 constexpr size_t kDirSmem = 2 * kStages * kBoxStride * sizeof(double) + 128;
-constexpr size_t kUpdSmem = kStages * (kBoxStride + 2 * kInt) * sizeof(double) + 128;
+constexpr size_t kUpdSmem = kStages * (kBoxStride + 3 * kInt) * sizeof(double) + 128;

@@ -194,8 +194,8 @@ static int iteration(cf_dcg *ws, int half, double zc, cudaStream_t s)
         Slab &sb = ws->slabs[k];
         const TmaGeom &g = sb.gu;
         cg_update_tma<ORDER, PK><<<g.ntx * g.nty * g.nchunk, kWSThreads, kUpdSmem, s>>>(
-            sb.m_p[half ^ 1], sb.m_ri, sb.m_xi, g, ws->off, ws->diag, sb.r, sb.x, zc, ws->sc, sb.partials, sb.tk, 0,
-            0, ws->red + 2 * k);
+            sb.m_p[half ^ 1], sb.m_ri, sb.m_xi, sb.m_xi, g, ws->off, ws->diag, sb.r, sb.x, zc, ws->sc, sb.partials,
+            sb.tk, 0, 0, ws->red + 2 * k);
         CF_CHECK_LAUNCH("cg_update_tma (slab)");
     }
     rc = reduce_phase(ws, 2, PH_UPD, s);
