@@ -270,6 +270,13 @@ def poisson_symmetric(n: int, h: float) -> SymCsrMatrix:
     return SymCsrMatrix(num, np.full(num, 6.0 / (h * h)), ptr, cols.ravel()[keep], vals.ravel()[keep])
 
 
+def _build_preconditioner(a, kind: str):
+    """src/sim.py:375-376 (built once per cached operator here: the matrix is constant)."""
+    from .precond import dic_from
+
+    return dic_from(a) if kind == "dic" else jacobi_from(a)
+
+
 class PoissonCache:
     """Per-grid device state reused across steps (src/sim.py:336-349).
 
@@ -301,12 +308,7 @@ class PoissonCache:
     def preconditioner(self, cfg: SimConfig, op: StencilOperator):
         key = (cfg.n, cfg.h, cfg.preconditioner, cfg.spec.dims)
         if key not in self._precond:
-            if cfg.preconditioner == "dic":
-                from .precond import dic_from
-
-                self._precond[key] = dic_from(op)
-            else:
-                self._precond[key] = jacobi_from(op)
+            self._precond[key] = _build_preconditioner(op, cfg.preconditioner)
         return self._precond[key]
 
     def rhs_buffer(self, spec: GridSpec) -> torch.Tensor:
