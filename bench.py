@@ -295,8 +295,10 @@ def run_ours(args, rank, world, local_rank):
 
 def run_slabs(args, cfg, rank, world, local_rank, barrier):
     """N > 1: the same 256^3 cavity z-slab sharded over the ranks (strong
-    scaling): velocity/pressure halos by NCCL P2P, the CG in cf_dcg with NCCL
-    all-reduce + r-halo send/recv, one slab per GPU."""
+    scaling), one slab per GPU: velocity/pressure halos by NCCL P2P; the CG
+    with its collectives fused into the kernels over peer memory (cf_pcg,
+    default) or as NCCL all-reduce + r-halo send/recv (cf_dcg,
+    --collective nccl)."""
     import torch
     import torch.distributed as dist
 
@@ -305,7 +307,7 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
 
     n = cfg.n
     dec = SlabDecomposition(n, n, n, world, rank)
-    sim = SlabSim(cfg, [dec.z0, dec.z1], distributed=True)
+    sim = SlabSim(cfg, [dec.z0, dec.z1], distributed=True, collective=args.collective)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         sim.step()
@@ -363,11 +365,11 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
         "config": {"workload": f"lid-driven cavity {n}^3 (BASELINE config 4), z-slab over {world} GPUs",
                    "n": n, "h": 1.0 / n, "dt": args.dt, "tol": 1e-8, "preconditioner": "jacobi",
                    "variant": "optimized", "physics": "reference (lid acceleration, inviscid)",
-                   "parallelism": f"zslab{world}", "l2": "inputs larger than L2 (no flush needed)"},
+                   "parallelism": f"zslab{world}", "collective": args.collective, "l2": "inputs larger than L2 (no flush needed)"},
         "sim_steps_per_s": args.steps / (ms_max / 1e3), "cg_iterations": its,
         "fused_iter_us": iter_s * 1e6, "fused_iter_gbs_per_gpu": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "per-GPU z-slab CG iteration (dir + update + all-reduces + r halo)",
+                     "traffic": None, "kernel": f"per-GPU z-slab CG iteration (dir + update + all-reduces + r halo; {args.collective})",
                      "algorithmic_bytes_per_iteration": 88 * cells_rank, "peak_kind": peak_kind},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_rank * world,
                 "d2h_bytes_per_step": bytes_rank * world},
@@ -388,6 +390,8 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=40)
     ap.add_argument("--ref-iters", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--collective", choices=("p2p", "nccl"), default="p2p",
+                    help="z-slab CG collectives (N > 1): fused peer-memory kernels, or NCCL calls")
     ap.add_argument("--force-slabs", action="store_true",
                     help="run the z-slab/NCCL path even on one rank (plumbing check)")
     args = ap.parse_args()

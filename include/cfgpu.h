@@ -151,6 +151,27 @@ int cf_dcg_solve(cf_dcg *ws, const double *const *b_slabs, double *const *x_slab
                  int64_t max_iter, int precond, int64_t *iters_host, double *res_host, void *stream);
 int cf_dcg_last_loop_ms(cf_dcg *ws, float *ms_host);
 
+/* ---- z-slab CG with the collectives fused into the kernels (peer memory) --
+ * Same solve as cf_dcg, but each iteration is two kernels per GPU: the r
+ * halo planes are stored straight into the neighbours' memory by the update
+ * kernel, and each reduction is posted to every rank's mailbox and summed
+ * (rank order) by the kernels' last blocks -- no NCCL, no extra launches
+ * (csrc/cf_p2p.cu).  nslabs == 1: this process is `rank` of `nranks`, one GPU
+ * each; link the ranks with cf_pcg_export (publish this rank's IPC handles)
+ * and cf_pcg_import (all ranks' blobs in rank order) before solving.
+ * nslabs == nranks (rank 0): every slab in this process on one device, the
+ * single-device verification of the same kernels.  nx even, <= 8 ranks. */
+typedef struct cf_pcg cf_pcg;
+int cf_pcg_create(cf_pcg **ws, int nx, int ny, int nz, double h, int order, int nranks, int rank, int nslabs,
+                  const int *slab_bounds, void *stream);
+int cf_pcg_export_size(void);
+int cf_pcg_export(cf_pcg *ws, void *out, int cap);
+int cf_pcg_import(cf_pcg *ws, const void *all_blobs, int nranks);
+int cf_pcg_destroy(cf_pcg *ws);
+int cf_pcg_solve(cf_pcg *ws, const double *const *b_slabs, double *const *x_slabs, double tol, int64_t max_iter,
+                 int precond, int64_t *iters_host, double *res_host, void *stream);
+int cf_pcg_last_loop_ms(cf_pcg *ws, float *ms_host);
+
 /* ---- time-step kernels (src/sim.py:134-289, :352-449) ------------------- */
 /* Lid forcing u[1:n, n-1, :] += lid_dv, then zero the six wall-normal face
  * planes.  Replaces apply_forces + enforce_boundaries (:134-149).

@@ -68,6 +68,13 @@ _SIGNATURES = {
     "cf_dcg_destroy": ([_vp], _int),
     "cf_dcg_solve": ([_vp, _vp, _vp, _dbl, _i64, _int, _pi64, _pd, _vp], _int),
     "cf_dcg_last_loop_ms": ([_vp, _pf], _int),
+    "cf_pcg_create": ([ctypes.POINTER(_vp), _int, _int, _int, _dbl, _int, _int, _int, _int, _vp, _vp], _int),
+    "cf_pcg_export_size": ([], _int),
+    "cf_pcg_export": ([_vp, _vp, _int], _int),
+    "cf_pcg_import": ([_vp, _vp, _int], _int),
+    "cf_pcg_destroy": ([_vp], _int),
+    "cf_pcg_solve": ([_vp, _vp, _vp, _dbl, _i64, _int, _pi64, _pd, _vp], _int),
+    "cf_pcg_last_loop_ms": ([_vp, _pf], _int),
     "cf_forces_bc": ([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _int, _vp], _int),
     "cf_advect": ([_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _vp], _int),
     "cf_divergence": ([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _vp, _pd, _vp], _int),

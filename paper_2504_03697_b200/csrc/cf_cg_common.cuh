@@ -13,6 +13,7 @@ struct CgScalars {
     double alpha_prev;  // alpha of the previous iteration (deferred x update, XM_DOUBLE)
     long long it, max_iter;
     int done, status;  // status: 0 running, 1 converged, 2 max_iter, 3 breakdown
+    unsigned long long phase;  // collective phases completed (peer-memory z-slab CG, cf_p2p.cu)
 };
 
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_BREAKDOWN = 3 };

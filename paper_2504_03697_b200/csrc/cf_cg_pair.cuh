@@ -30,6 +30,10 @@ struct PairGeom {
     __host__ __device__ int ctas() const { return ntx * nty * nchunk; }
 };
 
+// Host: geometry for an nx*ny*nz block (z-slab halos lo/hi), z cut into
+// chunks of ~32 planes (env_name: override of the chunk count).  cf_cg.cu.
+PairGeom pair_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, const char *env_name);
+
 struct PairCoords {
     int lane, i, j, z0, z1, zlo, zhi;
     bool row_ok, valid;        // row j exists; the pair (i, i+1) exists
@@ -37,11 +41,11 @@ struct PairCoords {
     long long base;            // flat offset of (i, j, 0)
 };
 
-__device__ __forceinline__ PairCoords pair_coords(const PairGeom &g)
+__device__ __forceinline__ PairCoords pair_coords(const PairGeom &g, int bid)
 {
     PairCoords c;
     const int ntiles = g.ntx * g.nty;
-    const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+    const int tile = bid % ntiles, chunk = bid / ntiles;
     c.lane = threadIdx.x & 31;
     c.i = (tile % g.ntx) * kPairX + 2 * c.lane;
     c.j = (tile / g.ntx) * kPairRows + (threadIdx.x >> 5);
@@ -207,18 +211,14 @@ struct UpdSrc {
 // partial to red_out).  In slab mode the halo planes of p (-1, nz) are
 // recomputed from the exchanged r halo and stored so the update kernel's
 // stencil can read them (bit-identical to the neighbour's owned p).
+// The direction march of one block; returns the thread's partial p.Ap.
 template <int ORDER, int PK>
-__global__ void __launch_bounds__(kPairThreads, 8) cg_dir_pair(PairGeom g, double off, double diag,
-                                                            const double *__restrict__ zsrc,
-                                                            const double *__restrict__ jd,
-                                                            const double *__restrict__ p_old,
-                                                            double *__restrict__ p_new, double zc, CgScalars *sc,
-                                                            double *partials, CgTickets *tk, double *red_out)
+__device__ __forceinline__ double dir_pair_body(const PairGeom &g, int bid, double off, double diag,
+                                                const double *__restrict__ zsrc, const double *__restrict__ jd,
+                                                const double *__restrict__ p_old, double *__restrict__ p_new,
+                                                double zc, double beta, bool first)
 {
-    __shared__ double red[32];
-    __shared__ int is_last;
-    if (sc->done) return;
-    const PairCoords c = pair_coords(g);
+    const PairCoords c = pair_coords(g, bid);
     struct Epi {
         double *p_new;
         bool valid;
@@ -235,10 +235,26 @@ __global__ void __launch_bounds__(kPairThreads, 8) cg_dir_pair(PairGeom g, doubl
         }
     } epi{p_new, c.valid, 0.0};
     if (c.row_ok) {
-        const DirSrc<PK> src{zsrc, p_old, jd, zc, sc->beta, sc->it == 0};
+        const DirSrc<PK> src{zsrc, p_old, jd, zc, beta, first};
         pair_march<ORDER, true>(c, g, off, diag, src, epi);
     }
-    double pap = block_sum<kPairThreads>(epi.pap, red);
+    return epi.pap;
+}
+
+template <int ORDER, int PK>
+__global__ void __launch_bounds__(kPairThreads, 8) cg_dir_pair(PairGeom g, double off, double diag,
+                                                            const double *__restrict__ zsrc,
+                                                            const double *__restrict__ jd,
+                                                            const double *__restrict__ p_old,
+                                                            double *__restrict__ p_new, double zc, CgScalars *sc,
+                                                            double *partials, CgTickets *tk, double *red_out)
+{
+    __shared__ double red[32];
+    __shared__ int is_last;
+    if (sc->done) return;
+    double pap = dir_pair_body<ORDER, PK>(g, blockIdx.x, off, diag, zsrc, jd, p_old, p_new, zc, sc->beta,
+                                          sc->it == 0);
+    pap = block_sum<kPairThreads>(pap, red);
     if (threadIdx.x == 0) partials[blockIdx.x] = pap;
     if (last_block(&tk->dir, &is_last)) {
         pap = reduce_partials<kPairThreads>(partials, gridDim.x, 1, red);
@@ -269,7 +285,7 @@ __global__ void __launch_bounds__(kPairThreads, 8) cg_update_pair(PairGeom g, do
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
         return;
     }
-    const PairCoords c = pair_coords(g);
+    const PairCoords c = pair_coords(g, blockIdx.x);
     struct Epi {
         double *r, *x;
         const double *jd, *q;

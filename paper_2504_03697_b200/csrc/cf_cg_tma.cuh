@@ -107,6 +107,10 @@ struct UpdPolicy {
     double alpha, malpha, zc, alpha_prev;
     double *r, *x;
     long long nx, plane;
+    // z-slab peer form (cf_p2p.cu): the bottom / top owned r plane is also
+    // stored into the neighbours' halo planes (null: no neighbour / not used)
+    double *lo_r, *hi_r;
+    int ztop;
     double rr = 0.0, rz = 0.0;
 
     __device__ __forceinline__ double2 value2(int s, int o) const { return ld2(sp + s * kBoxStride + o); }
@@ -126,6 +130,8 @@ struct UpdPolicy {
         }
         const double r0 = ro.x + malpha * a0, r1 = ro.y + malpha * a1;  // :157
         st2(r + gi, r0, r1);
+        if (lo_r && z == 0) st2(lo_r + (gi - plane * z), r0, r1);
+        if (hi_r && z == ztop) st2(hi_r + (gi - plane * z), r0, r1);
         rr = rr + r0 * r0;
         rr = rr + r1 * r1;
         if (PK != PK_ZVEC) {
@@ -140,6 +146,52 @@ struct UpdPolicy {
 template <int XM>
 __host__ __device__ constexpr int upd_interiors() { return XM == XM_SKIP ? 1 : (XM == XM_EACH ? 2 : 3); }
 
+// The update march of one block (block `bid` of the geometry): producer warp
+// streams the p halo box and the interior boxes through the mbarrier ring,
+// consumers run the stencil + epilogue.  Returns the block sums (rr, rz) on
+// thread 0.  Maps may live in the parameter block or in global memory.
+template <int ORDER, int PK, int XM>
+__device__ __forceinline__ void update_tma_body(const CUtensorMap *mp, const CUtensorMap *mr, const CUtensorMap *mx,
+                                             const CUtensorMap *mq, const TmaGeom g, int bid, double off, double diag,
+                                             double *__restrict__ r, double *__restrict__ x, double zc, double alpha,
+                                             double alpha_prev, double *__restrict__ lo_r, double *__restrict__ hi_r,
+                                             double *red, double &rr_out, double &rz_out)
+{
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    double *const sp = aligned_smem(smem_raw);
+    double *const sr = sp + kStages * kBoxStride;
+    double *const sx = sr + kStages * kInt;
+    double *const sq = sx + kStages * kInt;
+    const MarchCoords m = march_coords(g, bid);
+    UpdPolicy<PK, XM> pol{sp,  sr,   sx,   sq,   alpha,   -alpha, zc, alpha_prev, r, x, g.nx, (long long)g.nx * g.ny,
+                          lo_r, hi_r, g.nz - 1};
+    init_ws_bars(full, empty);
+    if (threadIdx.x >= kPThreads) {  // producer warp
+        if (threadIdx.x == kPThreads) {
+            prefetch_map(mp);
+            prefetch_map(mr);
+            if (XM != XM_SKIP) prefetch_map(mx);
+            if (XM == XM_DOUBLE) prefetch_map(mq);
+            ws_produce(m.nplanes, full, empty, [&](int q, int s, uint64_t *bar) {
+                const int z = m.zs + q;
+                const bool own = z >= m.z0 && z < m.z1;  // r, x, p_prev only for owned planes
+                mbar_expect_tx(bar, kBoxBytes + (own ? upd_interiors<XM>() * kIntBytes : 0));
+                tma_load_3d(sp + s * kBoxStride, mp, m.bx0, m.by0, z + g.lo_halo, bar);
+                if (own) {
+                    tma_load_3d(sr + s * kInt, mr, m.x0, m.y0, z + g.lo_halo, bar);
+                    if (XM != XM_SKIP) tma_load_3d(sx + s * kInt, mx, m.x0, m.y0, z + g.lo_halo, bar);
+                    if (XM == XM_DOUBLE) tma_load_3d(sq + s * kInt, mq, m.x0, m.y0, z + g.lo_halo, bar);
+                }
+            });
+        }
+    } else {
+        ws_consume<ORDER>(g, m, off, diag, pol, full, empty);
+    }
+    rr_out = block_sum<kWSThreads>(pol.rr, red);
+    rz_out = PK != PK_ZVEC ? block_sum<kWSThreads>(pol.rz, red) : 0.0;
+}
+
 template <int ORDER, int PK, int XM = XM_EACH>
 __global__ void __launch_bounds__(kWSThreads) cg_update_tma(
     const __grid_constant__ CUtensorMap mp, const __grid_constant__ CUtensorMap mr,
@@ -147,45 +199,15 @@ __global__ void __launch_bounds__(kWSThreads) cg_update_tma(
     double diag, double *__restrict__ r, double *__restrict__ x, double zc, CgScalars *sc, double *partials,
     CgTickets *tk, int use_cond, cudaGraphConditionalHandle cond, double *red_out)
 {
-    extern __shared__ unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
     __shared__ double red[32];
     __shared__ int is_last;
     if (sc->done) {
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
         return;
     }
-    double *const sp = aligned_smem(smem_raw);
-    double *const sr = sp + kStages * kBoxStride;
-    double *const sx = sr + kStages * kInt;
-    double *const sq = sx + kStages * kInt;
-    const double alpha = sc->alpha;
-    const MarchCoords m = march_coords(g);
-    UpdPolicy<PK, XM> pol{sp, sr, sx, sq, alpha, -alpha, zc, sc->alpha_prev, r, x, g.nx, (long long)g.nx * g.ny};
-    init_ws_bars(full, empty);
-    if (threadIdx.x >= kPThreads) {  // producer warp
-        if (threadIdx.x == kPThreads) {
-            prefetch_map(&mp);
-            prefetch_map(&mr);
-            if (XM != XM_SKIP) prefetch_map(&mx);
-            if (XM == XM_DOUBLE) prefetch_map(&mq);
-            ws_produce(m.nplanes, full, empty, [&](int q, int s, uint64_t *bar) {
-                const int z = m.zs + q;
-                const bool own = z >= m.z0 && z < m.z1;  // r, x, p_prev only for owned planes
-                mbar_expect_tx(bar, kBoxBytes + (own ? upd_interiors<XM>() * kIntBytes : 0));
-                tma_load_3d(sp + s * kBoxStride, &mp, m.bx0, m.by0, z + g.lo_halo, bar);
-                if (own) {
-                    tma_load_3d(sr + s * kInt, &mr, m.x0, m.y0, z + g.lo_halo, bar);
-                    if (XM != XM_SKIP) tma_load_3d(sx + s * kInt, &mx, m.x0, m.y0, z + g.lo_halo, bar);
-                    if (XM == XM_DOUBLE) tma_load_3d(sq + s * kInt, &mq, m.x0, m.y0, z + g.lo_halo, bar);
-                }
-            });
-        }
-    } else {
-        ws_consume<ORDER>(g, m, off, diag, pol, full, empty);
-    }
-    double rr = block_sum<kWSThreads>(pol.rr, red);
-    double rz = PK != PK_ZVEC ? block_sum<kWSThreads>(pol.rz, red) : 0.0;
+    double rr, rz;
+    update_tma_body<ORDER, PK, XM>(&mp, &mr, &mx, &mq, g, blockIdx.x, off, diag, r, x, zc, sc->alpha, sc->alpha_prev,
+                                   nullptr, nullptr, red, rr, rz);
     if (threadIdx.x == 0) {
         partials[2 * blockIdx.x] = rr;
         partials[2 * blockIdx.x + 1] = rz;

@@ -42,14 +42,14 @@ struct MarchCoords {
     int o;              // smem offset of cell (i, j) in a halo box
 };
 
-__device__ __forceinline__ MarchCoords march_coords(const TmaGeom &g)
+__device__ __forceinline__ MarchCoords march_coords(const TmaGeom &g, int bid)
 {
     MarchCoords m;
     const int tid = threadIdx.x;
     m.tx2 = tid % kPairs;
     m.ty = tid / kPairs;
     const int ntiles = g.ntx * g.nty;
-    const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+    const int tile = bid % ntiles, chunk = bid / ntiles;
     m.x0 = (tile % g.ntx) * kTTX;
     m.y0 = (tile / g.ntx) * kTTY;
     m.z0 = (int)((long long)g.nz * chunk / g.nchunk);
@@ -66,6 +66,8 @@ __device__ __forceinline__ MarchCoords march_coords(const TmaGeom &g)
     m.o = (m.j - m.by0) * kHX + (m.i - m.bx0);
     return m;
 }
+
+__device__ __forceinline__ MarchCoords march_coords(const TmaGeom &g) { return march_coords(g, blockIdx.x); }
 
 __device__ __forceinline__ void init_bars(uint64_t *bars)
 {

@@ -91,15 +91,94 @@ class SlabCG:
             pass
 
 
+class PeerSlabCG:
+    """CG over z-slabs with the collectives fused into the kernels over peer
+    memory (cf_pcg_*, csrc/cf_p2p.cu): one slab per rank (GPU) linked through
+    CUDA IPC handles exchanged over torch.distributed, or -- ``bounds`` with
+    several slabs, no process group -- every slab on this device, the
+    single-device verification of the same kernels and protocol.
+    Same ``solve`` interface as ``SlabCG`` (the NCCL form)."""
+
+    def __init__(self, nx: int, ny: int, nz: int, h: float, order: str = "sym", bounds=None,
+                 distributed: bool = False):
+        lib = _lib.load_library()
+        bounds = [0, nz] if bounds is None else [int(b) for b in bounds]
+        self.nx, self.ny, self.nz, self.h = nx, ny, nz, float(h)
+        self.bounds = bounds
+        self.plane = nx * ny
+        self.order = _lib.ORDER_CSR if order == "csr" else _lib.ORDER_SYM
+        nslab = len(bounds) - 1
+        if distributed:
+            import torch.distributed as dist
+
+            nranks, rank = dist.get_world_size(), dist.get_rank()
+            if nslab != 1:
+                raise ValueError("one slab per rank in a distributed run")
+        else:
+            nranks, rank = nslab, 0
+        arr = (ctypes.c_int * len(bounds))(*bounds)
+        hdl = ctypes.c_void_p()
+        _lib.check(lib.cf_pcg_create(ctypes.byref(hdl), nx, ny, nz, self.h, self.order, nranks, rank, nslab, arr,
+                                     _lib.stream()), "cf_pcg_create")
+        self._h = hdl
+        self.last_loop_ms = 0.0
+        if distributed and nranks > 1:  # publish this rank's IPC handles, open the peers'
+            import torch.distributed as dist
+
+            size = lib.cf_pcg_export_size()
+            blob = ctypes.create_string_buffer(size)
+            _lib.check(lib.cf_pcg_export(self._h, blob, size), "cf_pcg_export")
+            blobs = [None] * nranks
+            dist.all_gather_object(blobs, blob.raw)
+            allb = ctypes.create_string_buffer(b"".join(blobs), size * nranks)
+            _lib.check(lib.cf_pcg_import(self._h, allb, nranks), "cf_pcg_import")
+            dist.barrier()
+
+    def solve(self, b_slabs, tol: float = 1e-6, max_iter: int = 1000, precond: str | None = "jacobi"):
+        lib = _lib.load_library()
+        ns = len(self.bounds) - 1
+        if len(b_slabs) != ns:
+            raise ValueError(f"expected {ns} slabs, got {len(b_slabs)}")
+        bs = [as_device(b)[0].contiguous() for b in b_slabs]
+        for k, b in enumerate(bs):
+            want = self.plane * (self.bounds[k + 1] - self.bounds[k])
+            if b.numel() != want:
+                raise ValueError(f"slab {k} needs {want} values, got {b.numel()}")
+        xs = [torch.empty_like(b) for b in bs]
+        bp = (ctypes.c_void_p * ns)(*(b.data_ptr() for b in bs))
+        xp = (ctypes.c_void_p * ns)(*(x.data_ptr() for x in xs))
+        pk = _lib.PRECOND_JACOBI if precond == "jacobi" else _lib.PRECOND_NONE
+        its = ctypes.c_int64()
+        res = ctypes.c_double()
+        rc = lib.cf_pcg_solve(self._h, bp, xp, float(tol), int(max_iter), pk, ctypes.byref(its), ctypes.byref(res),
+                              _lib.stream())
+        ms = ctypes.c_float()
+        lib.cf_pcg_last_loop_ms(self._h, ctypes.byref(ms))
+        self.last_loop_ms = float(ms.value)
+        if rc == _lib.CF_BREAKDOWN:
+            raise BreakdownError(_lib.last_error())
+        _lib.check(rc, "cf_pcg_solve")
+        return xs, SolveStats(int(its.value), float(res.value), rc == _lib.CF_OK)
+
+    def __del__(self):
+        try:
+            if self._h and _lib._lib is not None:
+                _lib._lib.cf_pcg_destroy(self._h)
+        except Exception:
+            pass
+
+
 def emulated_pcg(op: StencilOperator, b, nslabs: int, tol: float = 1e-6, max_iter: int = 1000,
-                 precond: str | None = "jacobi"):
+                 precond: str | None = "jacobi", collective: str = "nccl"):
     """Single-device run of the z-slab decomposition (slabs = contiguous views
-    of the global x-fastest vector).  Returns (x, SolveStats, SlabCG)."""
+    of the global x-fastest vector).  ``collective``: "nccl" (SlabCG, the
+    kernels + collective calls form) or "p2p" (PeerSlabCG, collectives fused
+    into the kernels).  Returns (x, SolveStats, solver)."""
     bd, host = as_device(b)
     bd = bd.contiguous()
-    n = op.n
     bounds = SlabDecomposition.bounds(op.nz, nslabs).tolist()
-    scg = SlabCG(op.nx, op.ny, op.nz, op.h, "csr" if op.order == _lib.ORDER_CSR else "sym", bounds=bounds)
+    cls = PeerSlabCG if collective == "p2p" else SlabCG
+    scg = cls(op.nx, op.ny, op.nz, op.h, "csr" if op.order == _lib.ORDER_CSR else "sym", bounds=bounds)
     pl = op.nx * op.ny
     xs, st = scg.solve([bd[bounds[k] * pl:bounds[k + 1] * pl] for k in range(nslabs)], tol, max_iter, precond)
     x = torch.cat(xs)
@@ -152,9 +231,11 @@ class SlabSim:
     the CG exchanges its own r halos inside cf_dcg.
     """
 
-    def __init__(self, cfg, bounds, distributed: bool = False):
+    def __init__(self, cfg, bounds, distributed: bool = False, collective: str = "p2p"):
         import torch.distributed as dist
 
+        if collective not in ("p2p", "nccl"):
+            raise ValueError(f"collective must be 'p2p' or 'nccl', got {collective!r}")
         if cfg.preconditioner != "jacobi":
             raise ValueError("the z-slab solver shards Jacobi-PCG only (DIC's sweeps do not shard)")
         if cfg.warm_start:
@@ -173,7 +254,12 @@ class SlabSim:
             if s.nzl < HALO + 1:
                 raise ValueError(f"slab [{s.z0}, {s.z1}) is thinner than {HALO + 1} planes")
         order = "sym" if cfg.variant == "optimized" else "csr"
-        if distributed:
+        self.collective = collective
+        if collective == "p2p":
+            self.rank, self.world = (dist.get_rank(), dist.get_world_size()) if distributed else (0, 1)
+            self.cg = PeerSlabCG(self.nx, self.ny, self.nz, cfg.h, order, bounds=self.bounds,
+                                 distributed=distributed)
+        elif distributed:
             self.rank, self.world = dist.get_rank(), dist.get_world_size()
             obj = [nccl_unique_id() if self.rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
@@ -370,14 +456,17 @@ class SlabSim:
         return StepStats(solve=stats, div_pre=div_pre, div_post=div_post)
 
 
-def init_slab_cg(n: int, h: float, order: str = "sym", nz: int | None = None) -> tuple:
-    """Per-rank z-slab solver over torch.distributed (one GPU per rank).
-    Returns (SlabCG, SlabDecomposition)."""
+def init_slab_cg(n: int, h: float, order: str = "sym", nz: int | None = None, collective: str = "p2p") -> tuple:
+    """Per-rank z-slab solver over torch.distributed (one GPU per rank):
+    ``collective`` "p2p" (collectives fused into the kernels, PeerSlabCG) or
+    "nccl" (SlabCG).  Returns (solver, SlabDecomposition)."""
     import torch.distributed as dist
 
     world, rank = dist.get_world_size(), dist.get_rank()
     nz = n if nz is None else nz
     dec = SlabDecomposition(n, n, nz, world, rank)
+    if collective == "p2p":
+        return PeerSlabCG(n, n, nz, h, order, bounds=[dec.z0, dec.z1], distributed=True), dec
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     lo = dec.lo_neighbor if dec.lo_neighbor is not None else -1
@@ -387,7 +476,7 @@ def init_slab_cg(n: int, h: float, order: str = "sym", nz: int | None = None) ->
     return scg, dec
 
 
-def run(cfg, slabs: int | None = None, distributed: bool = False):
+def run(cfg, slabs: int | None = None, distributed: bool = False, collective: str = "p2p"):
     """``sim.run`` (src/sim.py:477-505) over z-slabs: ``distributed=True``
     gives this rank its slab of a torch.distributed job (one GPU per rank);
     otherwise ``slabs`` consecutive slabs are emulated on this device.
@@ -408,7 +497,7 @@ def run(cfg, slabs: int | None = None, distributed: bool = False):
         bounds = [dec.z0, dec.z1]
     else:
         bounds = SlabDecomposition.bounds(nz, 1 if slabs is None else int(slabs)).tolist()
-    sim = SlabSim(cfg, bounds, distributed=distributed)
+    sim = SlabSim(cfg, bounds, distributed=distributed, collective=collective)
     prof = Profiler()
     report = RunReport()
     t0 = time.perf_counter()

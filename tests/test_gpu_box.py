@@ -185,10 +185,12 @@ def test_box_slabs_match_single_domain(cuda, shape, bounds):
 
 
 def test_box_slabs_need_tma_rows(cuda):
-    """The z-slab solver is TMA-only: nx must be even and >= 32."""
+    """The NCCL z-slab solver is TMA-only (even nx >= 32); the peer-memory one needs an even nx."""
     from paper_2504_03697_b200.distributed import SlabSim
 
     cfg = cuda.SimConfig(n=33, h=1.0 / 33, dt=0.01, t_end=0.01, shape=(17, 33, 12),
                          preconditioner="jacobi", variant="optimized")
     with pytest.raises(ValueError, match="even nx >= 32"):
+        SlabSim(cfg, [0, 6, 12], collective="nccl")
+    with pytest.raises(ValueError, match="nx even"):
         SlabSim(cfg, [0, 6, 12])

@@ -67,7 +67,8 @@ def test_slabs_edge_cases(cuda):
 
 
 @pytest.mark.parametrize("nslabs", [2, 3, 5])
-def test_slab_time_steps_match_single_domain(cuda, nslabs):
+@pytest.mark.parametrize("collective", ["p2p", "nccl"])
+def test_slab_time_steps_match_single_domain(cuda, nslabs, collective):
     """Whole time steps (forces, advection with velocity halos, divergence,
     z-slab CG, correction with pressure halos) on emulated slabs vs the
     single-domain step.  Everything but the CG's reduction order is the same
@@ -89,7 +90,7 @@ def test_slab_time_steps_match_single_domain(cuda, nslabs):
     ref = cuda.initial_state(cfg)
     ref.vel.load_host(u0, v0, w0)
     cache = cuda.PoissonCache()
-    sim = SlabSim(cfg, SlabDecomposition.bounds(n, nslabs).tolist())
+    sim = SlabSim(cfg, SlabDecomposition.bounds(n, nslabs).tolist(), collective=collective)
     sim.load_global(u0, v0, w0)
     for _ in range(cfg.num_steps):
         a = cuda.step(ref, cfg, cache)
@@ -131,3 +132,62 @@ def test_slabs_full_size(cuda):
     r = b - op(x4)
     assert float(torch.linalg.norm(r) / torch.linalg.norm(b)) <= 2e-8
     assert float(torch.linalg.norm(x4 - x1) / torch.linalg.norm(x1)) <= 1e-7
+
+
+# ---------------------------------------------------------------- peer-memory form (cf_pcg, csrc/cf_p2p.cu)
+
+
+@pytest.mark.parametrize("order", ["sym", "csr"])
+@pytest.mark.parametrize("nslabs", [1, 2, 3, 5, 8])
+def test_peer_slabs_match_single_domain(cuda, order, nslabs):
+    """Collectives fused into the kernels: all slabs in ONE launch per phase,
+    mailbox posts / polls and halo stores between the slabs' arrays."""
+    from paper_2504_03697_b200.distributed import emulated_pcg
+
+    n = 64
+    h = 1.0 / n
+    b = np.random.default_rng(nslabs).uniform(-1, 1, n ** 3)
+    op = cuda.StencilOperator(n, h, order)
+    x1, s1 = cuda.pcg(op, b, precond=cuda.jacobi_from(op), tol=1e-10, max_iter=20000)
+    xs, ss, _ = emulated_pcg(op, b, nslabs, tol=1e-10, max_iter=20000, collective="p2p")
+    assert ss.converged
+    assert abs(ss.iterations - s1.iterations) <= 2, (ss.iterations, s1.iterations)
+    assert rel(xs, x1) <= 1e-9
+
+
+def test_peer_slabs_oracle_box_and_edges(cuda):
+    from paper_2504_03697_b200.distributed import PeerSlabCG, emulated_pcg
+
+    n = 32
+    h = 1.0 / n
+    b = np.random.default_rng(0).uniform(-1, 1, n ** 3)
+    a = orc.poisson_sym(n, h)
+    xo, so = orc.pcg(lambda v, o: orc.spmv_sym(a, v, 1, o), b, precond=orc.jacobi_from(a), tol=1e-8,
+                     max_iter=20000)
+    x, st, scg = emulated_pcg(cuda.StencilOperator(n, h, "sym"), b, 4, tol=1e-8, max_iter=20000, collective="p2p")
+    assert abs(st.iterations - so.iterations) <= 2
+    assert rel(x, xo) <= 1e-8
+    # repeated solves on one workspace (phase numbers carry over), odd / even stops
+    for its in (1, 2, 3, 4):
+        xa, sa, _ = emulated_pcg(cuda.StencilOperator(n, h, "sym"), b, 3, tol=1e-14, max_iter=its, collective="p2p")
+        xb, sb = orc.pcg(lambda v, o: orc.spmv_sym(a, v, 1, o), b, precond=orc.jacobi_from(a), tol=1e-14,
+                         max_iter=its)
+        assert sa.iterations == its and not sa.converged
+        assert rel(xa, xb) <= 1e-12
+    pl = n * n
+    bd = torch.as_tensor(b, device="cuda")
+    for _ in range(2):
+        xs, s2 = scg.solve([bd[k * pl * 8:(k + 1) * pl * 8] for k in range(4)], 1e-8, 20000, "jacobi")
+        assert s2.iterations == st.iterations
+    # zero right-hand side, no preconditioner, a box
+    x0, s0, _ = emulated_pcg(cuda.StencilOperator(n, h, "sym"), np.zeros(n ** 3), 2, collective="p2p")
+    assert s0.iterations == 0 and s0.converged and not x0.any()
+    shape = (34, 20, 30)
+    op = cuda.StencilOperator(34, 1.0 / 34, "sym", shape=shape)
+    bb = np.random.default_rng(5).standard_normal(34 * 20 * 30)
+    x1, s1 = cuda.pcg(op, bb, tol=1e-10, max_iter=5000)
+    xq, sq, _ = emulated_pcg(op, bb, 3, tol=1e-10, max_iter=5000, precond=None, collective="p2p")
+    assert abs(sq.iterations - s1.iterations) <= 2
+    assert rel(xq, x1) <= 1e-9
+    with pytest.raises(ValueError):
+        PeerSlabCG(33, 8, 8, 1.0)  # odd nx
