@@ -143,6 +143,19 @@ __device__ __forceinline__ bool last_block_sys(unsigned int *ticket, int *flag_s
     return last;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// A peer that never posts (a crashed or diverged rank) must not hang the GPU:
+// the wait gives up after kPeerTimeoutNs, stops the solve (done, status
+// ST_PEER_TIMEOUT) and the host reports an error.
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+constexpr int ST_PEER_TIMEOUT = 4;
+
 // Thread 0 of a slab's last block: post `v` (ncomp values) to every rank,
 // wait for every rank's post of this phase, return the rank-ordered sums.
 __device__ __forceinline__ void p2p_allreduce(const P2PSet &ps, const P2PSlab &sl, int ncomp, const double *v,
@@ -154,8 +167,18 @@ __device__ __forceinline__ void p2p_allreduce(const P2PSet &ps, const P2PSlab &s
         for (int c = 0; c < ncomp; ++c) st_relaxed_sys(&ps.mail[q]->val[par][me][c], v[c]);
     for (int q = 0; q < ps.nranks; ++q) st_release_sys(&ps.mail[q]->seq[par][me], ph);
     Mailbox *mine = ps.mail[me];
-    for (int q = 0; q < ps.nranks; ++q)
-        while (ld_acquire_sys(&mine->seq[par][q]) < ph) __nanosleep(64);
+    const unsigned long long t0 = globaltimer_ns();
+    for (int q = 0; q < ps.nranks; ++q) {
+        while (ld_acquire_sys(&mine->seq[par][q]) < ph) {
+            __nanosleep(64);
+            if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
+                sl.sc->status = ST_PEER_TIMEOUT;
+                sl.sc->done = 1;
+                for (int c = 0; c < ncomp; ++c) out[c] = __longlong_as_double(0x7ff8000000000000ll);
+                return;
+            }
+        }
+    }
     for (int c = 0; c < ncomp; ++c) {
         double sum = 0.0;
         for (int q = 0; q < ps.nranks; ++q) sum = sum + ld_relaxed_sys(&mine->val[par][q][c]);
@@ -829,6 +852,11 @@ int cf_pcg_solve(cf_pcg *ws, const double *const *b_slabs, double *const *x_slab
     CF_CUDA(cudaStreamSynchronize(s));
     if (iters_host) *iters_host = h->it;
     if (res_host) *res_host = h->res;
+    if (h->status == cf::ST_PEER_TIMEOUT) {
+        cf::set_error("cf_pcg_solve: a peer rank did not post its partial sums within 20 s (rank failed or "
+                      "ranks diverged)");
+        return CF_ECUDA;
+    }
     if (h->status == cf::ST_BREAKDOWN) {
         cf::set_error("p^T A p = " + std::to_string(h->pap) + " at iteration " + std::to_string(h->it + 1));
         return CF_BREAKDOWN;
