@@ -13,6 +13,8 @@
 // single-domain entry points are the slab [0, nz) with H = 0.
 #include <algorithm>
 
+#include <cmath>
+
 #include "cf_common.cuh"
 
 namespace cf {
@@ -86,47 +88,75 @@ constexpr int kFaceThreads = 256;
 
 // src/sim.py:193-240 + :283-288.  blockIdx.y = component; a grid-stride
 // loop over the slab's owned faces with i fastest (coalesced stores).
-__global__ void __launch_bounds__(kFaceThreads) advect_kernel(Vel3 in, double *nu, double *nv, double *nw,
-                                                              SlabZ sz, double h, double dt)
+// POW2: h is a power of two, so every q / h the reference evaluates equals
+// q * (1/h) exactly (scaling by 2^k is exact) -- the dozen fp64 divisions per
+// face, which dominated this kernel, become multiplications, bit-identically.
+template <bool POW2>
+__device__ __forceinline__ void advect_face(const Vel3 &in, const Comp &me, double *out, const SlabZ &sz, int comp,
+                                            long long f, double h, double inv_h, double dt, double lx, double ly,
+                                            double lz)
 {
-    const int comp = blockIdx.y;
-    const Comp me = in.c[comp];
-    double *out = comp == 0 ? nu : (comp == 1 ? nv : nw);
-    const int kend = comp == 2 ? sz.w_end() : sz.z1;
-    const long long total = (long long)me.na * me.nb * (kend - sz.z0);
-    const long long stride = (long long)gridDim.x * kFaceThreads;
-    const int wall_n = sz.ext(comp);
-    const double lx = sz.nx * h, ly = sz.ny * h, lz = sz.nz * h;  // side lengths (length = n*h)
-    for (long long f = (long long)blockIdx.x * kFaceThreads + threadIdx.x; f < total; f += stride) {
-        const int i = (int)(f % me.na);
-        const long long rest = f / me.na;
-        const int j = (int)(rest % me.nb), k = sz.z0 + (int)(rest / me.nb);
-        double *dst = out + me.off(i, j, k);
-        const int wall = comp == 0 ? i : (comp == 1 ? j : k);
-        if (wall == 0 || wall == wall_n) {  // wall-normal planes are zeroed (:283-288)
-            *dst = 0.0;
-            continue;
-        }
-        double x, y, z;
-        if (comp == 0) {
-            x = i * h; y = (j + 0.5) * h; z = (k + 0.5) * h;
-        } else if (comp == 1) {
-            x = (i + 0.5) * h; y = j * h; z = (k + 0.5) * h;
-        } else {
-            x = (i + 0.5) * h; y = (j + 0.5) * h; z = k * h;
-        }
-        const double su = trilerp(in.c[0], x / h, y / h - 0.5, z / h - 0.5);
-        const double sv = trilerp(in.c[1], x / h - 0.5, y / h, z / h - 0.5);
-        const double sw = trilerp(in.c[2], x / h - 0.5, y / h - 0.5, z / h);
-        const double xb = clamp_hi(x - dt * su, lx);
-        const double yb = clamp_hi(y - dt * sv, ly);
-        const double zb = clamp_hi(z - dt * sw, lz);
-        double r;
-        if (comp == 0) r = trilerp(me, xb / h, yb / h - 0.5, zb / h - 0.5);
-        else if (comp == 1) r = trilerp(me, xb / h - 0.5, yb / h, zb / h - 0.5);
-        else r = trilerp(me, xb / h - 0.5, yb / h - 0.5, zb / h);
-        *dst = r;
+    auto over_h = [&](double q) { return POW2 ? q * inv_h : q / h; };
+    const int i = (int)(f % me.na);
+    const long long rest = f / me.na;
+    const int j = (int)(rest % me.nb), k = sz.z0 + (int)(rest / me.nb);
+    double *dst = out + me.off(i, j, k);
+    const int wall = comp == 0 ? i : (comp == 1 ? j : k);
+    if (wall == 0 || wall == sz.ext(comp)) {  // wall-normal planes are zeroed (:283-288)
+        *dst = 0.0;
+        return;
     }
+    double x, y, z;
+    if (comp == 0) {
+        x = i * h; y = (j + 0.5) * h; z = (k + 0.5) * h;
+    } else if (comp == 1) {
+        x = (i + 0.5) * h; y = j * h; z = (k + 0.5) * h;
+    } else {
+        x = (i + 0.5) * h; y = (j + 0.5) * h; z = k * h;
+    }
+    const double xh = over_h(x), yh = over_h(y), zh = over_h(z);
+    const double su = trilerp(in.c[0], xh, yh - 0.5, zh - 0.5);
+    const double sv = trilerp(in.c[1], xh - 0.5, yh, zh - 0.5);
+    const double sw = trilerp(in.c[2], xh - 0.5, yh - 0.5, zh);
+    const double xb = over_h(clamp_hi(x - dt * su, lx));
+    const double yb = over_h(clamp_hi(y - dt * sv, ly));
+    const double zb = over_h(clamp_hi(z - dt * sw, lz));
+    double r;
+    if (comp == 0) r = trilerp(me, xb, yb - 0.5, zb - 0.5);
+    else if (comp == 1) r = trilerp(me, xb - 0.5, yb, zb - 0.5);
+    else r = trilerp(me, xb - 0.5, yb - 0.5, zb);
+    *dst = r;
+}
+
+// src/sim.py:193-240 + :283-288: a grid-stride loop over face index f with
+// i fastest (coalesced stores); each thread advects face f of ALL three
+// components, so the three sweeps move through the domain together and the
+// velocity planes they sample are read from HBM once (a launch per component
+// -- or blockIdx.y = component -- sweeps the whole field three times).
+// POW2: h is a power of two, so every q / h the reference evaluates equals
+// q * (1/h) exactly (scaling by 2^k is exact): the fp64 divisions become
+// multiplications, bit-identically.
+template <bool POW2>
+__global__ void __launch_bounds__(kFaceThreads) advect_kernel(Vel3 in, double *nu, double *nv, double *nw,
+                                                              SlabZ sz, double h, double inv_h, double dt)
+{
+    long long total[3];
+    for (int c = 0; c < 3; ++c)
+        total[c] = (long long)in.c[c].na * in.c[c].nb * ((c == 2 ? sz.w_end() : sz.z1) - sz.z0);
+    const long long tmax = max(total[0], max(total[1], total[2]));
+    const long long stride = (long long)gridDim.x * kFaceThreads;
+    const double lx = sz.nx * h, ly = sz.ny * h, lz = sz.nz * h;  // side lengths (length = n*h)
+    for (long long f = (long long)blockIdx.x * kFaceThreads + threadIdx.x; f < tmax; f += stride) {
+        if (f < total[0]) advect_face<POW2>(in, in.c[0], nu, sz, 0, f, h, inv_h, dt, lx, ly, lz);
+        if (f < total[1]) advect_face<POW2>(in, in.c[1], nv, sz, 1, f, h, inv_h, dt, lx, ly, lz);
+        if (f < total[2]) advect_face<POW2>(in, in.c[2], nw, sz, 2, f, h, inv_h, dt, lx, ly, lz);
+    }
+}
+
+static bool is_pow2(double h)
+{
+    int e;
+    return h > 0 && std::frexp(h, &e) == 0.5;
 }
 
 // src/sim.py:134-149 on the slab.  blockIdx.y selects the task: 0 = lid row
@@ -463,8 +493,11 @@ static int advect(const double *u, const double *v, const double *w, double *nu,
     CF_REQUIRE(nu != u && nv != v && nw != w, "advect: output aliases input");
     Vel3 in = make_vel(u, v, w, sz, ldu, ldv, ldw);
     long long faces = (long long)(sz.nx + 1) * (sz.ny + 1) * (sz.z1 - sz.z0 + 1);
-    dim3 grid(grid_for(faces, kFaceThreads, 8), 3);
-    advect_kernel<<<grid, kFaceThreads, 0, as_stream(stream)>>>(in, nu, nv, nw, sz, h, dt);
+    const int grid = grid_for(faces, kFaceThreads, 8);
+    if (is_pow2(h))
+        advect_kernel<true><<<grid, kFaceThreads, 0, as_stream(stream)>>>(in, nu, nv, nw, sz, h, 1.0 / h, dt);
+    else
+        advect_kernel<false><<<grid, kFaceThreads, 0, as_stream(stream)>>>(in, nu, nv, nw, sz, h, 1.0 / h, dt);
     CF_CHECK_LAUNCH("advect_kernel");
     return CF_OK;
 }
