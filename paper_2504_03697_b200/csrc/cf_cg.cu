@@ -263,13 +263,18 @@ __global__ void __launch_bounds__(kMarchThreads) cg_x_fixup(long long n, double 
 #include "cf_cg_pair.cuh"
 
 // Host: geometry of the pair-march kernels -- 64 x kPairRows tiles, z cut into
-// chunks of ~kPairPlanes planes (measured: enough CTAs in flight to keep HBM
-// busy, few enough partials for the last block).  env_name overrides.
+// chunks: at most ~kPairPlanes planes each (measured: enough CTAs in flight
+// to keep HBM busy at 256^3 / 512^3) and at least ~7 CTAs per SM in total
+// (the L2-resident 128^3 solve: 4 chunks 48 us/iteration, 16 chunks 36 us),
+// never below 4 planes.  env_name overrides the chunk count.
 constexpr int kPairPlanes = 32;
 PairGeom pair_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, const char *env_name)
 {
     PairGeom g{nx, ny, nz, lo_halo, hi_halo, (nx + kPairX - 1) / kPairX, (ny + kPairRows - 1) / kPairRows, 1};
-    int c = (nz + kPairPlanes - 1) / kPairPlanes;
+    const int tiles = g.ntx * g.nty;
+    const int by_planes = (nz + kPairPlanes - 1) / kPairPlanes;
+    const int by_ctas = (num_sms() * 7 + tiles - 1) / tiles;
+    int c = std::max(by_planes, std::min(by_ctas, std::max(1, nz / 4)));
     if (const char *e = env_name ? getenv(env_name) : nullptr) {
         const int v = atoi(e);
         if (v >= 1) c = v;
