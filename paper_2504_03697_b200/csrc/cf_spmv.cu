@@ -4,10 +4,35 @@
 //     the reference's per-row order (bit-identical results);
 //   * the matrix-free 7-point stencil (cf_stencil.cuh), 16 B/cell of HBM
 //     traffic against 12*nnz/N + 20 B/cell for CSR.
+#include <cstdlib>
+#include <cstring>
+
+#include "cf_cg_common.cuh"
 #include "cf_stencil.cuh"
 #include "cf_tma_march.cuh"
 
 namespace cf {
+
+#include "cf_cg_pair.cuh"
+
+// y = A x through the full-occupancy register pair march (cf_cg_pair.cuh):
+// warp = one 64-cell tile row of cell pairs, x-neighbours by shuffle.
+template <int ORDER>
+__global__ void __launch_bounds__(kPairThreads, 8) stencil_apply_pair(PairGeom g, double off, double diag,
+                                                                     const double *__restrict__ x,
+                                                                     double *__restrict__ y)
+{
+    const PairCoords c = pair_coords(g, blockIdx.x);
+    struct Epi {
+        double *y;
+        __device__ __forceinline__ void cell(long long o, double2, double a0, double a1)
+        {
+            *reinterpret_cast<double2 *>(y + o) = make_double2(a0, a1);
+        }
+        __device__ __forceinline__ void halo(long long, double2) {}
+    } epi{y};
+    if (c.row_ok) pair_march<ORDER, false>(c, g, off, diag, UpdSrc{x}, epi);
+}
 
 // y = A x through the warp-specialised TMA march (halo boxes of x staged by a
 // producer warp; the consumer warps' stencil reads shared memory only).
@@ -167,8 +192,20 @@ int cf_stencil7_apply(int nx, int ny, int nz, double h, int order, const double 
     // the same literals the reference assembles (src/sim.py:303-304)
     const double off = -1.0 / (h * h), diag = 6.0 / (h * h);
     cudaStream_t s = cf::as_stream(stream);
+    // default: the pair march (even nx); CF_APPLY=tma selects the TMA pipeline
+    const char *form = getenv("CF_APPLY");
+    if (nx % 2 == 0 && !(form && !strcmp(form, "tma")) && !(form && !strcmp(form, "ldg"))) {
+        const cf::PairGeom g = cf::pair_geom(nx, ny, nz, 0, 0, "CF_APPLY_CHUNKS");
+        if (order == CF_ORDER_CSR)
+            cf::stencil_apply_pair<CF_ORDER_CSR><<<g.ctas(), cf::kPairThreads, 0, s>>>(g, off, diag, x, y);
+        else
+            cf::stencil_apply_pair<CF_ORDER_SYM><<<g.ctas(), cf::kPairThreads, 0, s>>>(g, off, diag, x, y);
+        CF_CHECK_LAUNCH("stencil_apply_pair");
+        return CF_OK;
+    }
     bool used = false;
-    int rc = order == CF_ORDER_CSR
+    int rc = (form && !strcmp(form, "ldg")) ? CF_OK
+             : order == CF_ORDER_CSR
                  ? cf::stencil_apply_tma_launch<CF_ORDER_CSR>(nx, ny, nz, off, diag, x, y, s, &used)
                  : cf::stencil_apply_tma_launch<CF_ORDER_SYM>(nx, ny, nz, off, diag, x, y, s, &used);
     if (rc != CF_OK || used) return rc;
