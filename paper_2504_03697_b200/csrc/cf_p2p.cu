@@ -296,15 +296,15 @@ __global__ void __launch_bounds__(kPairThreads, 8) p2p_update(const P2PSet *__re
         double rr, rz;
         __device__ __forceinline__ void cell(long long o, double2 cc, double a0, double a1)
         {
-            const double2 ro = __ldcs(reinterpret_cast<const double2 *>(r + o));
+            const double2 ro = *reinterpret_cast<const double2 *>(r + o);
             if (XM == XM_EACH) {
-                const double2 xo = __ldcs(reinterpret_cast<const double2 *>(x + o));
-                __stcs(reinterpret_cast<double2 *>(x + o), make_double2(xo.x + alpha * cc.x, xo.y + alpha * cc.y));
+                const double2 xo = *reinterpret_cast<const double2 *>(x + o);
+                *reinterpret_cast<double2 *>(x + o) = make_double2(xo.x + alpha * cc.x, xo.y + alpha * cc.y);
             } else if (XM == XM_DOUBLE) {  // the skipped step first, then this one
-                const double2 xo = __ldcs(reinterpret_cast<const double2 *>(x + o));
-                const double2 qo = __ldcs(reinterpret_cast<const double2 *>(q + o));
+                const double2 xo = *reinterpret_cast<const double2 *>(x + o);
+                const double2 qo = *reinterpret_cast<const double2 *>(q + o);
                 const double x0 = xo.x + alpha_prev * qo.x, x1 = xo.y + alpha_prev * qo.y;
-                __stcs(reinterpret_cast<double2 *>(x + o), make_double2(x0 + alpha * cc.x, x1 + alpha * cc.y));
+                *reinterpret_cast<double2 *>(x + o) = make_double2(x0 + alpha * cc.x, x1 + alpha * cc.y);
             }
             const double r0 = ro.x + malpha * a0, r1 = ro.y + malpha * a1;  // src/solver.py:155-157
             const double2 rn = make_double2(r0, r1);
