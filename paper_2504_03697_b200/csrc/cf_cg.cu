@@ -261,6 +261,24 @@ __global__ void __launch_bounds__(kMarchThreads) cg_x_fixup(long long n, double 
 
 #include "cf_cg_tma.cuh"
 #include "cf_cg_pair.cuh"
+#include "cf_cg_pass.cuh"
+
+// Host: single-reduction pass geometry (32 x 16 tiles; chunks of ~32 planes,
+// the 4-plane pipeline prologue amortised; CF_PASS_CHUNKS overrides).
+PassGeom pass_geom(int nx, int ny, int nz)
+{
+    PassGeom g{nx, ny, nz, (nx + kPassTX - 1) / kPassTX, (ny + kPassTY - 1) / kPassTY, 1};
+    int c = (nz + 31) / 32;
+    const int tiles = g.ntx * g.nty;
+    const int by_ctas = (num_sms() * 4 + tiles - 1) / tiles;
+    c = std::max(c, std::min(by_ctas, std::max(1, nz / 8)));
+    if (const char *e = getenv("CF_PASS_CHUNKS")) {
+        const int v = atoi(e);
+        if (v >= 1) c = v;
+    }
+    g.nchunk = std::min(std::max(c, 1), nz);
+    return g;
+}
 
 // Host: geometry of the pair-march kernels -- 64 x kPairRows tiles, z cut into
 // chunks: at most ~kPairPlanes planes each (measured: enough CTAs in flight
@@ -423,6 +441,13 @@ struct cf_cg {
     CUtensorMap m_r{}, m_z{}, m_p[2]{}, m_ri{}, m_xi{}, m_pi[2]{};
     // x updated once per two iterations (XM_SKIP / XM_DOUBLE, cf_cg_common.cuh)
     bool defer_x = false;
+    // single-reduction CG (cf_cg_pass.cuh): one kernel per iteration; r ping-pongs
+    bool pass = false;
+    cf::PassGeom pass_g{};
+    double *r2 = nullptr;
+    cudaGraphExec_t exec_pass[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaGraph_t graph_pass[4] = {nullptr, nullptr, nullptr, nullptr};
+    double zc_pass[4] = {0, 0, 0, 0};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_loop_ms = 0.f;
     // one instantiated while-graph per (preconditioner kind)
@@ -577,6 +602,88 @@ static int launch_init(cf_cg *ws, const double *b, const double *x0, double zc, 
 }
 
 template <int ORDER, int PK>
+static int pass_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond, int use_cond)
+{
+    const PassGeom &g = ws->pass_g;
+    for (int half = 0; half < 2; ++half) {
+        const double *r_in = half ? ws->r2 : ws->r;
+        double *r_out = half ? ws->r : ws->r2;
+        cg_pass_kernel<ORDER, PK><<<g.ctas(), kPassThreads, kPassSmem, s>>>(
+            g, ws->off, ws->diag, zc, r_in, r_out, ws->p[half], ws->p[half ^ 1], ws->x, ws->sc, ws->partials, ws->tk,
+            use_cond, cond);
+        CF_CHECK_LAUNCH("cg_pass_kernel");
+    }
+    return CF_OK;
+}
+
+template <int ORDER, int PK>
+static int pass_build_graph(cf_cg *ws, double zc)
+{
+    cudaGraph_t g;
+    CF_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle cond;
+    CF_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CF_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+    cudaStream_t cs;
+    CF_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CF_CUDA(cudaStreamBeginCaptureToGraph(cs, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeRelaxed));
+    int rc = pass_body<ORDER, PK>(ws, cs, zc, cond, 1);
+    cudaGraph_t captured;
+    cudaError_t e = cudaStreamEndCapture(cs, &captured);
+    cudaStreamDestroy(cs);
+    if (rc != CF_OK) return rc;
+    CF_CUDA(e);
+    cudaGraphExec_t exec;
+    CF_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    ws->graph_pass[PK] = g;
+    ws->exec_pass[PK] = exec;
+    ws->zc_pass[PK] = zc;
+    return CF_OK;
+}
+
+template <int ORDER, int PK>
+static int pass_solve(cf_cg *ws, const double *b, double zc, cudaStream_t s)
+{
+    cg_pass_init<ORDER, PK><<<ws->pg_upd.ctas(), kPairThreads, 0, s>>>(ws->pg_upd, ws->off, ws->diag, zc, b, ws->r,
+                                                                       ws->x, ws->sc, ws->partials, ws->tk);
+    CF_CHECK_LAUNCH("cg_pass_init");
+    if (ws->direct) {
+        CF_CUDA(cudaEventRecord(ws->ev0, s));
+        for (;;) {
+            for (int b2 = 0; b2 < ws->direct_batch; ++b2) {
+                int rc = pass_body<ORDER, PK>(ws, s, zc, 0, 0);
+                if (rc != CF_OK) return rc;
+            }
+            CF_CUDA(cudaMemcpyAsync(&ws->sc_host->done, &ws->sc->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CF_CUDA(cudaStreamSynchronize(s));
+            if (ws->sc_host->done) break;
+        }
+        CF_CUDA(cudaEventRecord(ws->ev1, s));
+        return CF_OK;
+    }
+    if (!ws->exec_pass[PK] || ws->zc_pass[PK] != zc) {
+        if (ws->exec_pass[PK]) {
+            cudaGraphExecDestroy(ws->exec_pass[PK]);
+            cudaGraphDestroy(ws->graph_pass[PK]);
+            ws->exec_pass[PK] = nullptr;
+        }
+        int rc = pass_build_graph<ORDER, PK>(ws, zc);
+        if (rc != CF_OK) return rc;
+    }
+    CF_CUDA(cudaEventRecord(ws->ev0, s));
+    CF_CUDA(cudaGraphLaunch(ws->exec_pass[PK], s));
+    CF_CUDA(cudaEventRecord(ws->ev1, s));
+    return CF_OK;
+}
+
+template <int ORDER, int PK>
 static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, cudaStream_t s)
 {
     const char *ns = getenv("CF_NO_SMALL");
@@ -589,6 +696,9 @@ static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, c
         CF_CHECK_LAUNCH("cg_small_kernel");
         CF_CUDA(cudaEventRecord(ws->ev1, s));
         return CF_OK;
+    }
+    if ((PK == PK_NONE || PK == PK_JCONST) && ws->pass && !x0) {
+        if constexpr (PK == PK_NONE || PK == PK_JCONST) return pass_solve<ORDER, PK>(ws, b, zc, s);
     }
     int rc = launch_init<ORDER, PK>(ws, b, x0, zc, s);
     if (rc != CF_OK) return rc;
@@ -682,6 +792,19 @@ static void set_grids(cf_cg *ws)
     ws->pg_upd = pair_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, "CF_PAIR_CHUNKS_UPD");
     ws->kind_dir = kern_kind("CF_CG_DIR", KK_PAIR, ws->tma, pair_ok);
     ws->kind_upd = kern_kind("CF_CG_UPD", KK_TMA, ws->tma, pair_ok);
+    // single-reduction CG (one kernel per iteration, cf_cg_pass.cuh): opt-in.
+    // Measured at 256^3 it runs 215 us/iteration against 205 for the
+    // two-kernel form (instruction-bound: ~64 % issue slots), so the default
+    // stays the two-kernel form, which is also the reference's recurrence.
+    const char *algo = getenv("CF_CG_ALGO");
+    ws->pass = pair_ok && algo && !strcmp(algo, "pass");
+    if (ws->pass) {
+        ws->pass_g = pass_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz);
+        cudaFuncSetAttribute(cg_pass_kernel<ORDER, PK_NONE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kPassSmem);
+        cudaFuncSetAttribute(cg_pass_kernel<ORDER, PK_JCONST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kPassSmem);
+    }
     const char *dx = getenv("CF_CG_DEFER_X");
     ws->defer_x = ws->kind_upd != KK_LDG && !(dx && atoi(dx) == 0);
 }
@@ -731,11 +854,13 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
         if (g2 > maxg) maxg = g2;
     }
     maxg = std::max(maxg, std::max(ws->pg_dir.ctas(), ws->pg_upd.ctas()));
+    if (ws->pass) maxg = std::max(maxg, ws->pass_g.ctas());
     size_t vec = (size_t)ws->n * sizeof(double);
     cudaError_t e = cudaSuccess;
     for (double **b : {&ws->r, &ws->x, &ws->p[0], &ws->p[1]})
         if (e == cudaSuccess) e = cudaMalloc(b, vec);
-    if (e == cudaSuccess) e = cudaMalloc(&ws->partials, sizeof(double) * 2 * (size_t)maxg);
+    if (e == cudaSuccess) e = cudaMalloc(&ws->partials, sizeof(double) * 3 * (size_t)maxg);
+    if (e == cudaSuccess && ws->pass) e = cudaMalloc(&ws->r2, vec);
     if (e == cudaSuccess) e = cudaMalloc(&ws->sc, sizeof(cf::CgScalars));
     if (e == cudaSuccess) e = cudaMalloc(&ws->tk, sizeof(cf::CgTickets));
     if (e == cudaSuccess) e = cudaMemsetAsync(ws->tk, 0, sizeof(cf::CgTickets), cf::as_stream(stream));
@@ -764,7 +889,11 @@ int cf_cg_destroy(cf_cg *ws)
         if (ws->exec[k]) cudaGraphExecDestroy(ws->exec[k]);
         if (ws->graph[k]) cudaGraphDestroy(ws->graph[k]);
     }
-    for (double *b : {ws->r, ws->x, ws->p[0], ws->p[1], ws->jd, ws->partials, ws->zbuf, ws->wbuf})
+    for (int k = 0; k < 4; ++k) {
+        if (ws->exec_pass[k]) cudaGraphExecDestroy(ws->exec_pass[k]);
+        if (ws->graph_pass[k]) cudaGraphDestroy(ws->graph_pass[k]);
+    }
+    for (double *b : {ws->r, ws->x, ws->p[0], ws->p[1], ws->jd, ws->partials, ws->zbuf, ws->wbuf, ws->r2})
         if (b) cudaFree(b);
     if (ws->sc) cudaFree(ws->sc);
     if (ws->tk) cudaFree(ws->tk);
