@@ -223,33 +223,32 @@ __global__ void __launch_bounds__(kPassThreads) cg_pass_kernel(PassGeom g, doubl
                                                      Pp[bo], true, true, true, true, true, true, off, diag);
                     rn = Rk[bo] + malpha * a;  // src/solver.py:157
                     if (write_out && qx >= 1 && qx <= kPassTX && qy >= 1 && qy <= kPassTY) {
-                        // the tile's own cells: p_k, r_{k+1}, x_{k+1} = x_k + alpha p_k (:155)
+                        // the tile's own cells: p_k, r_{k+1}, x_{k+1} = x_k + alpha p_k (:155),
+                        // and r.r, r.z of r_{k+1} (:158, :163-166)
                         const long long o = (long long)gi + (long long)g.nx * gj + plane * zq;
                         p_new[o] = c;
                         r_out[o] = rn;
                         x[o] = xk[q] + alpha * c;
+                        rr = rr + rn * rn;
+                        gam = gam + rn * zscale<PK>(rn, zc);
                     }
                 }
-                Q[e] = rn;
+                Q[e] = zscale<PK>(rn, zc);  // the ring holds z_{k+1} = M^-1 r_{k+1}
             }
         }
         __syncthreads();
-        // ---- w = A z_{k+1} on plane t (interior, two cells per thread), dot partials
+        // ---- w = A z_{k+1} on plane t (interior, two cells per thread): z.w
         if (t >= z0) {
             const double *const Qm = ring_q + ((t - 1 + 6) % 3) * kP1;
             const double *const Qc = ring_q + ((t + 6) % 3) * kP1;
             const double *const Qp = ring_q + ((t + 1 + 6) % 3) * kP1;
-            auto zz = [&](double v) { return zscale<PK>(v, zc); };
             for (int e = tid; e < kPassTX * kPassTY; e += kPassThreads) {
                 const int cy = e / kPassTX, cx = e % kPassTX;
                 if (x0 + cx >= g.nx || y0 + cy >= g.ny) continue;
                 const int qo = (cy + 1) * kP1X + (cx + 1);
-                const double rc = Qc[qo], c = zz(rc);
-                const double w = stencil7<ORDER>(c, zz(Qc[qo - 1]), zz(Qc[qo + 1]), zz(Qc[qo - kP1X]),
-                                                 zz(Qc[qo + kP1X]), zz(Qm[qo]), zz(Qp[qo]), true, true, true, true,
-                                                 true, true, off, diag);
-                rr = rr + rc * rc;
-                gam = gam + rc * c;  // r.z (:163-166)
+                const double c = Qc[qo];
+                const double w = stencil7<ORDER>(c, Qc[qo - 1], Qc[qo + 1], Qc[qo - kP1X], Qc[qo + kP1X], Qm[qo],
+                                                 Qp[qo], true, true, true, true, true, true, off, diag);
                 dlt = dlt + c * w;
             }
         }
