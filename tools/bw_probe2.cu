@@ -31,6 +31,37 @@ __global__ void tile_copy(const double *__restrict__ a, double *__restrict__ b, 
     }
 }
 
+// streaming mixes with no stencil: R reads + W writes per cell (distinct arrays)
+template <int TX, int TY, int R, int W>
+__global__ void tile_mix(const double *__restrict__ a, const double *__restrict__ b, const double *__restrict__ c,
+                         double *__restrict__ d, double *__restrict__ e, int n, int nchunk)
+{
+    const int ntx = n / TX, nty = n / TY, ntiles = ntx * nty;
+    const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+    const int i = (tile % ntx) * TX + 2 * (threadIdx.x % (TX / 2));
+    const int j = (tile / ntx) * TY + threadIdx.x / (TX / 2);
+    const int z0 = n * chunk / nchunk, z1 = n * (chunk + 1) / nchunk;
+    const long long pl = (long long)n * n;
+    const long long base = i + (long long)n * j;
+#pragma unroll 2
+    for (int z = z0; z < z1; ++z) {
+        const long long o = base + pl * z;
+        double2 v = __ldg(reinterpret_cast<const double2 *>(a + o));
+        if (R > 1) {
+            double2 w = __ldg(reinterpret_cast<const double2 *>(b + o));
+            v.x += w.x;
+            v.y += w.y;
+        }
+        if (R > 2) {
+            double2 w = __ldg(reinterpret_cast<const double2 *>(c + o));
+            v.x += w.x;
+            v.y += w.y;
+        }
+        *reinterpret_cast<double2 *>(d + o) = v;
+        if (W > 1) *reinterpret_cast<double2 *>(e + o) = make_double2(v.y, v.x);
+    }
+}
+
 template <int TX, int TY>
 __global__ void tile_stencil(const double *__restrict__ a, double *__restrict__ b, int n, int nchunk)
 {
@@ -107,6 +138,27 @@ static void sweep(Args &a, double bytes)
     }
 }
 
+template <int R, int W>
+static void mix(double *a, double *b, double *c, double *d, double *e, int n)
+{
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int nc : {4, 8, 16}) {
+        const int grid = (n / 64) * (n / 4) * nc;
+        for (int w = 0; w < 3; ++w) tile_mix<64, 4, R, W><<<grid, 128>>>(a, b, c, d, e, n, nc);
+        cudaEventRecord(e0);
+        for (int k = 0; k < 10; ++k) tile_mix<64, 4, R, W><<<grid, 128>>>(a, b, c, d, e, n, nc);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ms /= 10;
+        const double bytes = 8.0 * (R + W) * n * (double)n * n;
+        printf("mix %dR+%dW chunks=%2d: %6.1f us %5.0f GB/s\n", R, W, nc, ms * 1e3, bytes / (ms * 1e-3) / 1e9);
+    }
+}
+
 int main(int argc, char **argv)
 {
     const int n = argc > 1 ? atoi(argv[1]) : 256;
@@ -122,6 +174,19 @@ int main(int argc, char **argv)
         a.grid = g;
         float ms = time_it(run_copy, &a);
         printf("flat copy grid=%d: %.1f us %.0f GB/s\n", g, ms * 1e3, bytes / (ms * 1e-3) / 1e9);
+    }
+    if (argc > 2) {
+        double *c, *d, *e;
+        cudaMalloc(&c, N * 8);
+        cudaMalloc(&d, N * 8);
+        cudaMalloc(&e, N * 8);
+        cudaMemset(c, 0, N * 8);
+        mix<1, 1>(a.x, a.y, c, d, e, n);
+        mix<2, 1>(a.x, a.y, c, d, e, n);
+        mix<3, 1>(a.x, a.y, c, d, e, n);
+        mix<3, 2>(a.x, a.y, c, d, e, n);
+        mix<2, 2>(a.x, a.y, c, d, e, n);
+        return 0;
     }
     sweep<32, 16>(a, bytes);
     sweep<64, 8>(a, bytes);
