@@ -171,6 +171,10 @@ int cf_pcg_destroy(cf_pcg *ws);
 int cf_pcg_solve(cf_pcg *ws, const double *const *b_slabs, double *const *x_slabs, double tol, int64_t max_iter,
                  int precond, int64_t *iters_host, double *res_host, void *stream);
 int cf_pcg_last_loop_ms(cf_pcg *ws, float *ms_host);
+/* Diagnostics (tests): which 0 = this rank's r allocation incl. halo planes
+ * (read or write), 1 / 2 = the peer plane this rank's bottom / top r plane is
+ * stored into (read only) -- checks the IPC linking without running kernels. */
+int cf_pcg_debug_io(cf_pcg *ws, int which, int write, double *host, int64_t n);
 
 /* ---- time-step kernels (src/sim.py:134-289, :352-449) ------------------- */
 /* Lid forcing u[1:n, n-1, :] += lid_dv, then zero the six wall-normal face

@@ -75,6 +75,7 @@ _SIGNATURES = {
     "cf_pcg_destroy": ([_vp], _int),
     "cf_pcg_solve": ([_vp, _vp, _vp, _dbl, _i64, _int, _pi64, _pd, _vp], _int),
     "cf_pcg_last_loop_ms": ([_vp, _pf], _int),
+    "cf_pcg_debug_io": ([_vp, _int, _int, _vp, _i64], _int),
     "cf_forces_bc": ([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _int, _vp], _int),
     "cf_advect": ([_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _vp], _int),
     "cf_divergence": ([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _vp, _pd, _vp], _int),

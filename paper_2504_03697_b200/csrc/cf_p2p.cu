@@ -448,8 +448,39 @@ struct PSlab {
 
 struct ExportBlob {  // what one rank publishes to the others
     cudaIpcMemHandle_t mail, r;
+    unsigned long long mail_off, r_off;  // byte offsets of the arrays inside the exported allocations
     int nzl, lo, hi, rank;
 };
+
+// cudaMalloc may sub-allocate small requests from a larger driver allocation;
+// an IPC handle names that allocation and the importer maps its base, so the
+// exporter publishes each array's offset within it (cuMemGetAddressRange).
+typedef int (*AddressRangeFn)(unsigned long long *base, size_t *size, unsigned long long ptr);
+static AddressRangeFn address_range_fn()
+{
+    static AddressRangeFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<AddressRangeFn>(p);
+    }
+    return fn;
+}
+
+static bool alloc_offset(const void *ptr, unsigned long long *off)
+{
+    AddressRangeFn fn = address_range_fn();
+    if (!fn) return false;
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0) return false;
+    *off = reinterpret_cast<unsigned long long>(ptr) - base;
+    return true;
+}
 
 }  // namespace
 
@@ -741,6 +772,8 @@ int cf_pcg_export(cf_pcg *ws, void *out, int cap)
     const PSlab &sb = ws->slabs[0];
     CF_CUDA(cudaIpcGetMemHandle(&b.mail, sb.mail));
     CF_CUDA(cudaIpcGetMemHandle(&b.r, sb.alloc[0]));
+    CF_REQUIRE(alloc_offset(sb.mail, &b.mail_off) && alloc_offset(sb.alloc[0], &b.r_off),
+               "cf_pcg_export: cuMemGetAddressRange unavailable");
     b.nzl = sb.nzl;
     b.lo = sb.lo;
     b.hi = sb.hi;
@@ -762,12 +795,12 @@ int cf_pcg_import(cf_pcg *ws, const void *all, int nranks)
         void *m = nullptr;
         CF_CUDA(cudaIpcOpenMemHandle(&m, blobs[q].mail, cudaIpcMemLazyEnablePeerAccess));
         ws->opened.push_back(m);
-        ws->set.mail[q] = static_cast<cf::Mailbox *>(m);
+        ws->set.mail[q] = reinterpret_cast<cf::Mailbox *>(static_cast<char *>(m) + blobs[q].mail_off);
         if (q == ws->rank - 1 || q == ws->rank + 1) {
             void *r = nullptr;
             CF_CUDA(cudaIpcOpenMemHandle(&r, blobs[q].r, cudaIpcMemLazyEnablePeerAccess));
             ws->opened.push_back(r);
-            double *base = static_cast<double *>(r);
+            double *base = reinterpret_cast<double *>(static_cast<char *>(r) + blobs[q].r_off);
             if (q == ws->rank - 1) d.lo_r = base + (size_t)(blobs[q].lo + blobs[q].nzl) * pl;  // its hi halo plane
             else d.hi_r = base;                                                                // its lo halo plane
         }
@@ -862,6 +895,32 @@ int cf_pcg_solve(cf_pcg *ws, const double *const *b_slabs, double *const *x_slab
         return CF_BREAKDOWN;
     }
     return h->status == cf::ST_CONVERGED ? CF_OK : CF_NOT_CONVERGED;
+}
+
+int cf_pcg_debug_io(cf_pcg *ws, int which, int write, double *host, int64_t n)
+{
+    CF_REQUIRE(ws && host && n >= 0 && ws->slabs.size() == 1 && which >= 0 && which <= 2,
+               "cf_pcg_debug_io: bad arguments");
+    const size_t pl = (size_t)ws->nx * ws->ny;
+    const PSlab &sb = ws->slabs[0];
+    double *dev = nullptr;
+    size_t cap = 0;
+    if (which == 0) {
+        dev = sb.alloc[0];
+        cap = pl * (size_t)(sb.nzl + sb.lo + sb.hi);
+    } else {
+        dev = which == 1 ? ws->set.s[0].lo_r : ws->set.s[0].hi_r;
+        cap = pl;
+        CF_REQUIRE(!write, "cf_pcg_debug_io: peer planes are read-only here");
+    }
+    CF_REQUIRE(dev != nullptr, "cf_pcg_debug_io: no such plane (no neighbour / not linked)");
+    CF_REQUIRE((size_t)n <= cap, "cf_pcg_debug_io: n exceeds the region");
+    // (a pageable H2D cudaMemcpy may return before the DMA lands: synchronise
+    // so a peer reading right after the caller's barrier sees the data)
+    if (write) CF_CUDA(cudaMemcpy(dev, host, (size_t)n * sizeof(double), cudaMemcpyHostToDevice));
+    else CF_CUDA(cudaMemcpy(host, dev, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost));
+    CF_CUDA(cudaDeviceSynchronize());
+    return CF_OK;
 }
 
 int cf_pcg_last_loop_ms(cf_pcg *ws, float *ms_host)
