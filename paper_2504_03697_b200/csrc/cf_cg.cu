@@ -524,7 +524,8 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
         }
         if (PK == PK_ZVEC) {
             // z = M^-1 r by the level sweeps, then r.z and beta (src/solver.py:163-166)
-            int rc = dic_apply_launch(ws->dic, ws->r, ws->wbuf, ws->zbuf, &ws->sc->done, s);
+            int rc = ws->dic.wave.ok ? dic_wave_apply(ws->dic, ws->r, ws->wbuf, ws->zbuf, &ws->sc->done, s)
+                                     : dic_apply_launch(ws->dic, ws->r, ws->wbuf, ws->zbuf, &ws->sc->done, s);
             if (rc != CF_OK) return rc;
             cg_rz_kernel<<<ws->grid_init, kMarchThreads, 0, s>>>(ws->n, ws->r, ws->zbuf, ws->sc, ws->partials,
                                                                  ws->tk, 1);
@@ -592,7 +593,8 @@ static int launch_init(cf_cg *ws, const double *b, const double *x0, double zc, 
     }
     CF_CHECK_LAUNCH("cg_init");
     if (PK == PK_ZVEC) {  // z = M^-1 r, rz = r.z (src/solver.py:141-143)
-        int rc = dic_apply_launch(ws->dic, ws->r, ws->wbuf, ws->zbuf, &ws->sc->done, s);
+        int rc = ws->dic.wave.ok ? dic_wave_apply(ws->dic, ws->r, ws->wbuf, ws->zbuf, &ws->sc->done, s)
+                                 : dic_apply_launch(ws->dic, ws->r, ws->wbuf, ws->zbuf, &ws->sc->done, s);
         if (rc != CF_OK) return rc;
         cg_rz_kernel<<<ws->grid_init, kMarchThreads, 0, s>>>(ws->n, ws->r, ws->zbuf, ws->sc, ws->partials, ws->tk,
                                                              0);
@@ -978,6 +980,9 @@ int cf_cg_set_dic(cf_cg *ws, const int32_t *lp, const int32_t *lc, const double 
     dd.d = d;
     dd.rows = level_rows;
     dd.level_ptr.assign(level_ptr_host, level_ptr_host + nlevels + 1);
+    // the tiled-wavefront sweeps when the triangles are the grid's 7-point pattern
+    int rcw = cf::dic_wave_setup(dd, ws->bx.nx, ws->bx.ny, ws->bx.nz, nullptr);
+    if (rcw != CF_OK) return rcw;
     ws->has_dic = true;
     if (ws->exec[cf::PK_ZVEC]) {  // pointers changed: rebuild on the next solve
         cudaGraphExecDestroy(ws->exec[cf::PK_ZVEC]);

@@ -14,6 +14,17 @@
 
 namespace cf {
 
+// Tiled-wavefront form of the sweeps (cf_dic_wave.cu): structured 7-point
+// pattern with one lower and one upper value, verified at attach time.
+struct DicWave {
+    int nx = 0, ny = 0, nz = 0, ntx = 0, nty = 0;
+    double lval = 0.0, uval = 0.0;
+    int slack = 1;                             // extra steps kept between neighbouring tiles
+    int pub = 8;                               // steps per published progress value
+    int *prog_f = nullptr, *prog_b = nullptr;  // per-tile progress of the two sweeps
+    bool ok = false;
+};
+
 struct DicData {
     long long n = 0;
     const int32_t *lp = nullptr, *lc = nullptr;  // strict lower triangle (CSR)
@@ -23,11 +34,17 @@ struct DicData {
     const double *d = nullptr;                   // modified diagonal
     const int32_t *rows = nullptr;               // rows sorted by level
     std::vector<long long> level_ptr;            // host: level l = rows[level_ptr[l]:level_ptr[l+1]]
+    DicWave wave;                                // used instead of the levels when wave.ok
 };
 
 // z = M^-1 r through w; if `done` is non-null every launch exits when *done
 // is set (used inside the CG graph once the solve has stopped).
 int dic_apply_launch(const DicData &dd, const double *r, double *w, double *z, const int *done,
                      cudaStream_t s);
+
+// Enable the wavefront sweeps for an nx*ny*nz grid if the triangles match
+// (dd.wave.ok tells); and apply them.  cf_dic_wave.cu.
+int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s);
+int dic_wave_apply(const DicData &dd, const double *r, double *w, double *z, const int *done, cudaStream_t s);
 
 }  // namespace cf

@@ -1,0 +1,333 @@
+// cf_dic_wave.cu -- the simplified-DIC sweeps (src/precond.py:38-54) as a
+// tiled 3-D wavefront, for the 7-point pattern of the structured grid.
+//
+// The level-scheduled form (cf_dic.cu) runs one launch per hyperplane
+// i+j+k = const: 3n-2 dependent launches per sweep, ~5 us each inside a
+// graph, so a 128^3 DIC apply costs ~3.9 ms of launch latency.  Here ONE
+// launch does a sweep: a CTA owns a 16 x 8 column of cells (its tile) over
+// all z and walks it along the diagonals s = ti + tj + k -- every cell's
+// lower neighbours (i-1, j-1, k-1) are on diagonal s-1, so one __syncthreads
+// per diagonal orders the whole tile.  Neighbours inside the tile come from
+// shared memory (left, below) or the thread's own register (k-1); across
+// tiles from global memory once the neighbouring tile has published that it
+// is far enough (a per-tile progress counter, release/acquire at GPU scope):
+// the left tile's cell (x0-1, j, k) is written at its step s + 16 - 1, the
+// lower tile's (i, y0-1, k) at s + 8 - 1.  The critical path is the DAG depth
+// (3n-2 diagonals) -- the same as the level schedule, without the launches.
+//
+// Every cell does the reference's operations in the reference's order
+// (forward: s = r_i; s -= L*w for the lower columns in ascending order
+// k-1, j-1, i-1; w_i = s / d_i; backward: s = 0; s += U*z for i+1, j+1, k+1;
+// z_i = w_i - s / d_i), so the result is bit-identical to the sequential
+// sweeps.  Used when the factor's triangles are exactly the 7-point pattern
+// of the CG workspace's grid with one off-diagonal value each (verified on
+// the device at attach time); anything else keeps the level schedule.
+#include <algorithm>
+#include <cstdlib>
+
+#include "cf_common.cuh"
+#include "cf_dic.cuh"
+
+namespace cf {
+
+constexpr int kWTX = 16, kWTY = 8, kWThreads = kWTX * kWTY;
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ int ld_relaxed_gpu(const int *p)
+{
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ void st_release_gpu(int *p, int v)
+{
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Forward sweep (L + D~) w = r.  blockIdx -> tile in increasing (a, b), so a
+// CTA only ever waits for lower-numbered CTAs.
+__global__ void __launch_bounds__(kWThreads) dic_wave_fwd(DicWave dw, const double *__restrict__ d,
+                                                         const double *__restrict__ r, double *__restrict__ w,
+                                                         const int *done)
+{
+    __shared__ double sm[2][kWTY][kWTX];
+    if (done && *done) return;
+    const int ntx = dw.ntx;
+    const int t = blockIdx.x, a = t % ntx, b = t / ntx;
+    const int ti = threadIdx.x % kWTX, tj = threadIdx.x / kWTX;
+    const int i = a * kWTX + ti, j = b * kWTY + tj;
+    const bool col_ok = i < dw.nx && j < dw.ny;
+    const long long pl = (long long)dw.nx * dw.ny;
+    const long long base = (long long)i + (long long)dw.nx * j;
+    if (threadIdx.x == 0) dw.prog_b[t] = 0;  // re-arm the backward sweep's counters (it runs after this launch)
+    const int *left = a > 0 ? dw.prog_f + (t - 1) : nullptr;
+    const int *below = b > 0 ? dw.prog_f + (t - ntx) : nullptr;
+    int seen_l = 0, seen_b = 0, peek_l = 0, peek_b = 0, last_l = 0, last_b = 0;
+    double wk = 0.0;  // w at (i, j, k-1)
+    const int nsteps = dw.nz + kWTX + kWTY - 2;
+    // r and d of this thread's next cell (independent of the sweep: prefetched a step ahead)
+    const int kfirst = -ti - tj;  // k at step 0
+    auto ld_rd = [&](int k, double &rv, double &dv) {
+        if (col_ok && k >= 0 && k < dw.nz) {
+            const long long o = base + pl * k;
+            rv = __ldg(r + o);
+            dv = __ldg(d + o);
+        }
+    };
+    double r_nx = 0.0, d_nx = 1.0;
+    ld_rd(kfirst, r_nx, d_nx);
+    // edge values from the neighbouring tiles, prefetched a step ahead; the
+    // wait below keeps `slack` steps between the tiles so that both the
+    // progress peek and these loads are normally satisfied a step early
+    const int slack = dw.slack;
+    auto ld_edge = [&](int k, double &xl, double &yl) {
+        if (col_ok && k >= 0 && k < dw.nz) {
+            const long long o = base + pl * k;
+            if (ti == 0 && i > 0) xl = __ldcg(w + o - 1);
+            if (tj == 0 && j > 0) yl = __ldcg(w + o - dw.nx);
+        }
+    };
+    double xl_nx = 0.0, yl_nx = 0.0;
+    bool edge_loaded = false;
+    for (int s = 0; s < nsteps; ++s) {
+        // wait until the left / lower tiles have produced what this diagonal
+        // reads (a neighbour's counter ends at nsteps); the relaxed peeks were
+        // issued a step earlier, a fence makes an accepted value an acquire
+        if (threadIdx.x == 0) {
+            const int need_l = min(s + kWTX + slack, nsteps), need_b = min(s + kWTY + slack, nsteps);
+            bool fresh = false;
+            if (left) {
+                seen_l = max(seen_l, peek_l);
+                while (seen_l < need_l) seen_l = ld_relaxed_gpu(left), fresh = true;
+            }
+            if (below) {
+                seen_b = max(seen_b, peek_b);
+                while (seen_b < need_b) seen_b = ld_relaxed_gpu(below), fresh = true;
+            }
+            if (fresh || seen_l != last_l || seen_b != last_b) fence_acq_rel_gpu();  // a newly observed value
+            last_l = seen_l;
+            last_b = seen_b;
+            if (left) peek_l = ld_relaxed_gpu(left);
+            if (below) peek_b = ld_relaxed_gpu(below);
+        }
+        __syncthreads();
+        const int k = s - ti - tj;
+        if (!edge_loaded) {  // first step: nothing prefetched yet
+            ld_edge(k, xl_nx, yl_nx);
+            edge_loaded = true;
+        }
+        const double rv = r_nx, dv = d_nx, xl = xl_nx, yl = yl_nx;
+        ld_rd(k + 1, r_nx, d_nx);
+        ld_edge(k + 1, xl_nx, yl_nx);  // the neighbours are >= slack steps past what this needs
+        double wv = 0.0;
+        if (col_ok && k >= 0 && k < dw.nz) {
+            const long long o = base + pl * k;
+            double acc = rv;
+            if (k > 0) acc = acc - dw.lval * wk;                                       // column i - pl
+            if (j > 0) acc = acc - dw.lval * (tj > 0 ? sm[s & 1][tj - 1][ti] : yl);  // i - nx
+            if (i > 0) acc = acc - dw.lval * (ti > 0 ? sm[s & 1][tj][ti - 1] : xl);  // i - 1
+            wv = acc / dv;
+            w[o] = wv;
+            wk = wv;
+        }
+        sm[(s + 1) & 1][tj][ti] = wv;
+        // (the next step's first barrier orders this step's shared writes
+        // before their reads and the reads of sm[s & 1] before its rewrite)
+        // Progress is published every `pub` steps -- a release waits for the
+        // stores to land, so it is amortised, not paid per diagonal; the
+        // barrier orders every thread's stores before it (cumulativity).
+        if ((s + 1) % dw.pub == 0 || s + 1 == nsteps) {
+            __syncthreads();
+            if (threadIdx.x == 0) st_release_gpu(dw.prog_f + t, s + 1);
+        }
+    }
+}
+
+// Backward sweep (D~ + L^T) z = D~ w, from the top corner: tiles in decreasing
+// (a, b) order, each waits for its right / upper neighbour.
+__global__ void __launch_bounds__(kWThreads) dic_wave_bwd(DicWave dw, const double *__restrict__ d,
+                                                         const double *__restrict__ w, double *__restrict__ z,
+                                                         const int *done)
+{
+    __shared__ double sm[2][kWTY][kWTX];
+    if (done && *done) return;
+    const int ntx = dw.ntx, nty = dw.nty;
+    const int t = ntx * nty - 1 - blockIdx.x, a = t % ntx, b = t / ntx;
+    const int ti = threadIdx.x % kWTX, tj = threadIdx.x / kWTX;
+    const int i = a * kWTX + ti, j = b * kWTY + tj;
+    const bool col_ok = i < dw.nx && j < dw.ny;
+    const long long pl = (long long)dw.nx * dw.ny;
+    const long long base = (long long)i + (long long)dw.nx * j;
+    if (threadIdx.x == 0) dw.prog_f[t] = 0;  // re-arm the next forward sweep's counters
+    const int *right = a < ntx - 1 ? dw.prog_b + (t + 1) : nullptr;
+    const int *above = b < nty - 1 ? dw.prog_b + (t + ntx) : nullptr;
+    int seen_r = 0, seen_a = 0, peek_r = 0, peek_a = 0, last_r = 0, last_a = 0;
+    double zk = 0.0;  // z at (i, j, k+1)
+    const int nsteps = dw.nz + kWTX + kWTY - 2;
+    // a tile's cells with the largest (i, j) start first: local distance from the top corner
+    const int ri = kWTX - 1 - ti, rj = kWTY - 1 - tj;
+    auto ld_wd = [&](int k, double &wv, double &dv) {
+        if (col_ok && k >= 0 && k < dw.nz) {
+            const long long o = base + pl * k;
+            wv = __ldcg(w + o);  // written by the forward launch
+            dv = __ldg(d + o);
+        }
+    };
+    double w_nx = 0.0, d_nx = 1.0;
+    ld_wd(dw.nz - 1 + ri + rj, w_nx, d_nx);
+    const int slack = dw.slack;
+    auto ld_edge = [&](int k, double &xr, double &yu) {
+        if (col_ok && k >= 0 && k < dw.nz) {
+            const long long o = base + pl * k;
+            if (ti == kWTX - 1 && i < dw.nx - 1) xr = __ldcg(z + o + 1);
+            if (tj == kWTY - 1 && j < dw.ny - 1) yu = __ldcg(z + o + dw.nx);
+        }
+    };
+    double xr_nx = 0.0, yu_nx = 0.0;
+    bool edge_loaded = false;
+    for (int s = 0; s < nsteps; ++s) {
+        if (threadIdx.x == 0) {
+            const int need_r = min(s + kWTX + slack, nsteps), need_a = min(s + kWTY + slack, nsteps);
+            if (right) {
+                seen_r = max(seen_r, peek_r);
+                while (seen_r < need_r) seen_r = ld_relaxed_gpu(right);
+            }
+            if (above) {
+                seen_a = max(seen_a, peek_a);
+                while (seen_a < need_a) seen_a = ld_relaxed_gpu(above);
+            }
+            if (seen_r != last_r || seen_a != last_a) fence_acq_rel_gpu();  // a newly observed value
+            last_r = seen_r;
+            last_a = seen_a;
+            if (right) peek_r = ld_relaxed_gpu(right);
+            if (above) peek_a = ld_relaxed_gpu(above);
+        }
+        __syncthreads();
+        const int k = dw.nz - 1 - (s - ri - rj);
+        if (!edge_loaded) {
+            ld_edge(k, xr_nx, yu_nx);
+            edge_loaded = true;
+        }
+        const double wo = w_nx, dv = d_nx, xr = xr_nx, yu = yu_nx;
+        ld_wd(k - 1, w_nx, d_nx);
+        ld_edge(k - 1, xr_nx, yu_nx);
+        double zv = 0.0;
+        if (col_ok && k >= 0 && k < dw.nz) {
+            const long long o = base + pl * k;
+            double acc = 0.0;
+            if (i < dw.nx - 1) acc = acc + dw.uval * (ti < kWTX - 1 ? sm[s & 1][tj][ti + 1] : xr);
+            if (j < dw.ny - 1) acc = acc + dw.uval * (tj < kWTY - 1 ? sm[s & 1][tj + 1][ti] : yu);
+            if (k < dw.nz - 1) acc = acc + dw.uval * zk;
+            zv = wo - acc / dv;
+            z[o] = zv;
+            zk = zv;
+        }
+        sm[(s + 1) & 1][tj][ti] = zv;
+        if ((s + 1) % dw.pub == 0 || s + 1 == nsteps) {
+            __syncthreads();
+            if (threadIdx.x == 0) st_release_gpu(dw.prog_b + t, s + 1);
+        }
+    }
+}
+
+// Verify that the triangles are exactly the 7-point pattern of the grid with
+// one value each; any mismatch clears *ok.
+__global__ void dic_wave_check(const int32_t *lp, const int32_t *lc, const double *lv, const int32_t *up,
+                               const int32_t *uc, const double *uv, int nx, int ny, int nz, double lval, double uval,
+                               int *ok)
+{
+    const long long pl = (long long)nx * ny, n = pl * nz;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n;
+         c += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / pl);
+        long long want[3];
+        int m = 0;
+        if (k > 0) want[m++] = c - pl;
+        if (j > 0) want[m++] = c - nx;
+        if (i > 0) want[m++] = c - 1;
+        int p0 = lp[c], p1 = lp[c + 1];
+        bool good = p1 - p0 == m;
+        for (int q = 0; good && q < m; ++q) good = lc[p0 + q] == want[q] && lv[p0 + q] == lval;
+        m = 0;
+        if (i < nx - 1) want[m++] = c + 1;
+        if (j < ny - 1) want[m++] = c + nx;
+        if (k < nz - 1) want[m++] = c + pl;
+        p0 = up[c];
+        p1 = up[c + 1];
+        good = good && p1 - p0 == m;
+        for (int q = 0; good && q < m; ++q) good = uc[p0 + q] == want[q] && uv[p0 + q] == uval;
+        if (!good) *ok = 0;
+    }
+}
+
+int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
+{
+    dd.wave.ok = false;
+    if (std::getenv("CF_DIC_LEVELS")) return CF_OK;  // force the level schedule
+    if (nx < 2 || ny < 2 || nz < 2 || (long long)nx * ny * nz != dd.n) return CF_OK;
+    DicWave &dw = dd.wave;
+    dw.nx = nx;
+    dw.ny = ny;
+    dw.nz = nz;
+    dw.ntx = (nx + kWTX - 1) / kWTX;
+    dw.nty = (ny + kWTY - 1) / kWTY;
+    const int ntiles = dw.ntx * dw.nty;
+    // every CTA of a sweep must be resident (CTAs wait for lower-numbered ones)
+    int bpsm = 0;
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, dic_wave_fwd, kWThreads, 0));
+    if ((long long)bpsm * num_sms() < ntiles) return CF_OK;
+    // the off-diagonal values (the first lower / upper entry of the first row that has one)
+    double vals[2] = {0.0, 0.0};
+    int32_t p[2];
+    // the last row has the full lower pattern, row 0 the full upper one
+    CF_CUDA(cudaMemcpyAsync(p, dd.lp + (dd.n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CF_CUDA(cudaMemcpyAsync(&p[1], dd.up, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CF_CUDA(cudaStreamSynchronize(s));
+    CF_CUDA(cudaMemcpyAsync(&vals[0], dd.lv + p[0], sizeof(double), cudaMemcpyDeviceToHost, s));
+    CF_CUDA(cudaMemcpyAsync(&vals[1], dd.uv + p[1], sizeof(double), cudaMemcpyDeviceToHost, s));
+    int *ok = nullptr;
+    CF_CUDA(cudaMalloc(&ok, sizeof(int)));
+    const int one = 1;
+    CF_CUDA(cudaMemcpyAsync(ok, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+    dic_wave_check<<<num_sms() * 4, 256, 0, s>>>(dd.lp, dd.lc, dd.lv, dd.up, dd.uc, dd.uv, nx, ny, nz, vals[0],
+                                                 vals[1], ok);
+    int good = 0;
+    CF_CUDA(cudaMemcpyAsync(&good, ok, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CF_CUDA(cudaStreamSynchronize(s));
+    cudaFree(ok);
+    if (!good) return CF_OK;
+    if (!dw.prog_f) {
+        CF_CUDA(cudaMalloc(&dw.prog_f, 2 * (size_t)ntiles * sizeof(int)));
+        dw.prog_b = dw.prog_f + ntiles;
+    }
+    CF_CUDA(cudaMemsetAsync(dw.prog_f, 0, 2 * (size_t)ntiles * sizeof(int), s));
+    dw.lval = vals[0];
+    dw.uval = vals[1];
+    dw.slack = 1;
+    if (const char *e = std::getenv("CF_DIC_SLACK")) dw.slack = std::max(1, std::atoi(e));  // >= 1: edges are prefetched a step ahead
+    dw.pub = 8;
+    if (const char *e = std::getenv("CF_DIC_PUBLISH")) dw.pub = std::max(1, std::atoi(e));
+    dw.ok = true;
+    return CF_OK;
+}
+
+int dic_wave_apply(const DicData &dd, const double *r, double *w, double *z, const int *done, cudaStream_t s)
+{
+    const DicWave &dw = dd.wave;
+    const int ntiles = dw.ntx * dw.nty;
+    dic_wave_fwd<<<ntiles, kWThreads, 0, s>>>(dw, dd.d, r, w, done);
+    dic_wave_bwd<<<ntiles, kWThreads, 0, s>>>(dw, dd.d, w, z, done);
+    CF_CHECK_LAUNCH("dic wavefront sweeps");
+    return CF_OK;
+}
+
+}  // namespace cf
