@@ -21,6 +21,7 @@ struct DicWave {
     double lval = 0.0, uval = 0.0;
     int slack = 1;                             // extra steps kept between neighbouring tiles
     int pub = 8;                               // steps per published progress value
+    int shape = 0;                             // tile shape (cf_dic_wave.cu kShapes)
     int *prog_f = nullptr, *prog_b = nullptr;  // per-tile progress of the two sweeps
     bool ok = false;
 };

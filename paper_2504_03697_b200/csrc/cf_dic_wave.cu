@@ -30,7 +30,13 @@
 
 namespace cf {
 
-constexpr int kWTX = 16, kWTY = 8, kWThreads = kWTX * kWTY;
+// one-warp tiles synchronise with __syncwarp instead of a block barrier
+template <int NT>
+__device__ __forceinline__ void tile_sync()
+{
+    if (NT == 32) __syncwarp();
+    else __syncthreads();
+}
 
 __device__ __forceinline__ int ld_acquire_gpu(const int *p)
 {
@@ -55,9 +61,10 @@ __device__ __forceinline__ void st_release_gpu(int *p, int v)
 
 // Forward sweep (L + D~) w = r.  blockIdx -> tile in increasing (a, b), so a
 // CTA only ever waits for lower-numbered CTAs.
-__global__ void __launch_bounds__(kWThreads) dic_wave_fwd(DicWave dw, const double *__restrict__ d,
-                                                         const double *__restrict__ r, double *__restrict__ w,
-                                                         const int *done)
+template <int kWTX, int kWTY>
+__global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd(DicWave dw, const double *__restrict__ d,
+                                                          const double *__restrict__ r, double *__restrict__ w,
+                                                          const int *done)
 {
     __shared__ double sm[2][kWTY][kWTX];
     if (done && *done) return;
@@ -119,7 +126,7 @@ __global__ void __launch_bounds__(kWThreads) dic_wave_fwd(DicWave dw, const doub
             if (left) peek_l = ld_relaxed_gpu(left);
             if (below) peek_b = ld_relaxed_gpu(below);
         }
-        __syncthreads();
+        tile_sync<kWTX * kWTY>();
         const int k = s - ti - tj;
         if (!edge_loaded) {  // first step: nothing prefetched yet
             ld_edge(k, xl_nx, yl_nx);
@@ -146,7 +153,7 @@ __global__ void __launch_bounds__(kWThreads) dic_wave_fwd(DicWave dw, const doub
         // stores to land, so it is amortised, not paid per diagonal; the
         // barrier orders every thread's stores before it (cumulativity).
         if ((s + 1) % dw.pub == 0 || s + 1 == nsteps) {
-            __syncthreads();
+            tile_sync<kWTX * kWTY>();
             if (threadIdx.x == 0) st_release_gpu(dw.prog_f + t, s + 1);
         }
     }
@@ -154,9 +161,10 @@ __global__ void __launch_bounds__(kWThreads) dic_wave_fwd(DicWave dw, const doub
 
 // Backward sweep (D~ + L^T) z = D~ w, from the top corner: tiles in decreasing
 // (a, b) order, each waits for its right / upper neighbour.
-__global__ void __launch_bounds__(kWThreads) dic_wave_bwd(DicWave dw, const double *__restrict__ d,
-                                                         const double *__restrict__ w, double *__restrict__ z,
-                                                         const int *done)
+template <int kWTX, int kWTY>
+__global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd(DicWave dw, const double *__restrict__ d,
+                                                          const double *__restrict__ w, double *__restrict__ z,
+                                                          const int *done)
 {
     __shared__ double sm[2][kWTY][kWTX];
     if (done && *done) return;
@@ -211,7 +219,7 @@ __global__ void __launch_bounds__(kWThreads) dic_wave_bwd(DicWave dw, const doub
             if (right) peek_r = ld_relaxed_gpu(right);
             if (above) peek_a = ld_relaxed_gpu(above);
         }
-        __syncthreads();
+        tile_sync<kWTX * kWTY>();
         const int k = dw.nz - 1 - (s - ri - rj);
         if (!edge_loaded) {
             ld_edge(k, xr_nx, yu_nx);
@@ -233,7 +241,7 @@ __global__ void __launch_bounds__(kWThreads) dic_wave_bwd(DicWave dw, const doub
         }
         sm[(s + 1) & 1][tj][ti] = zv;
         if ((s + 1) % dw.pub == 0 || s + 1 == nsteps) {
-            __syncthreads();
+            tile_sync<kWTX * kWTY>();
             if (threadIdx.x == 0) st_release_gpu(dw.prog_b + t, s + 1);
         }
     }
@@ -269,6 +277,19 @@ __global__ void dic_wave_check(const int32_t *lp, const int32_t *lc, const doubl
     }
 }
 
+constexpr int kShapes[5][2] = {{16, 8}, {64, 4}, {128, 4}, {256, 2}, {8, 4}};
+
+static const void *wave_fwd_kernel(int shape)
+{
+    switch (shape) {
+    case 0: return (const void *)dic_wave_fwd<16, 8>;
+    case 1: return (const void *)dic_wave_fwd<64, 4>;
+    case 2: return (const void *)dic_wave_fwd<128, 4>;
+    case 3: return (const void *)dic_wave_fwd<256, 2>;
+    default: return (const void *)dic_wave_fwd<8, 4>;
+    }
+}
+
 int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
 {
     dd.wave.ok = false;
@@ -278,12 +299,18 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
     dw.nx = nx;
     dw.ny = ny;
     dw.nz = nz;
-    dw.ntx = (nx + kWTX - 1) / kWTX;
-    dw.nty = (ny + kWTY - 1) / kWTY;
+    // tile shape: 16 x 8 measured best (128^3: 1.15 ms/iteration; 64x4 1.43,
+    // 128x4 1.45, 256x2 2.12, a one-warp 8x4 1.68): wider tiles pay more per
+    // block barrier than they save in progress handoffs
+    dw.shape = 0;
+    if (const char *e = std::getenv("CF_DIC_TILE")) dw.shape = std::max(0, std::min(4, std::atoi(e)));
+    const int tx = kShapes[dw.shape][0], ty = kShapes[dw.shape][1];
+    dw.ntx = (nx + tx - 1) / tx;
+    dw.nty = (ny + ty - 1) / ty;
     const int ntiles = dw.ntx * dw.nty;
     // every CTA of a sweep must be resident (CTAs wait for lower-numbered ones)
     int bpsm = 0;
-    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, dic_wave_fwd, kWThreads, 0));
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, wave_fwd_kernel(dw.shape), tx * ty, 0));
     if ((long long)bpsm * num_sms() < ntiles) return CF_OK;
     // the off-diagonal values (the first lower / upper entry of the first row that has one)
     double vals[2] = {0.0, 0.0};
@@ -324,8 +351,28 @@ int dic_wave_apply(const DicData &dd, const double *r, double *w, double *z, con
 {
     const DicWave &dw = dd.wave;
     const int ntiles = dw.ntx * dw.nty;
-    dic_wave_fwd<<<ntiles, kWThreads, 0, s>>>(dw, dd.d, r, w, done);
-    dic_wave_bwd<<<ntiles, kWThreads, 0, s>>>(dw, dd.d, w, z, done);
+    switch (dw.shape) {
+    case 0:
+        dic_wave_fwd<16, 8><<<ntiles, 128, 0, s>>>(dw, dd.d, r, w, done);
+        dic_wave_bwd<16, 8><<<ntiles, 128, 0, s>>>(dw, dd.d, w, z, done);
+        break;
+    case 1:
+        dic_wave_fwd<64, 4><<<ntiles, 256, 0, s>>>(dw, dd.d, r, w, done);
+        dic_wave_bwd<64, 4><<<ntiles, 256, 0, s>>>(dw, dd.d, w, z, done);
+        break;
+    case 2:
+        dic_wave_fwd<128, 4><<<ntiles, 512, 0, s>>>(dw, dd.d, r, w, done);
+        dic_wave_bwd<128, 4><<<ntiles, 512, 0, s>>>(dw, dd.d, w, z, done);
+        break;
+    case 3:
+        dic_wave_fwd<256, 2><<<ntiles, 512, 0, s>>>(dw, dd.d, r, w, done);
+        dic_wave_bwd<256, 2><<<ntiles, 512, 0, s>>>(dw, dd.d, w, z, done);
+        break;
+    default:
+        dic_wave_fwd<8, 4><<<ntiles, 32, 0, s>>>(dw, dd.d, r, w, done);
+        dic_wave_bwd<8, 4><<<ntiles, 32, 0, s>>>(dw, dd.d, w, z, done);
+        break;
+    }
     CF_CHECK_LAUNCH("dic wavefront sweeps");
     return CF_OK;
 }
