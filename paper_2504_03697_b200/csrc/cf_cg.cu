@@ -411,6 +411,117 @@ __global__ void __launch_bounds__(kSmallThreads) cg_small_kernel(Box bx, double 
     if (t == 0) *sc = s;
 }
 
+// Small grids with the simplified-DIC preconditioner (the reference's
+// default, src/sim.py:65): the whole solve in one block as above, the DIC
+// sweeps (src/precond.py:38-54) level by level (i+j+k = const) between block
+// barriers -- on the 7-point pattern verified at attach (one lower and one
+// upper value), every row in the reference's operand order.
+constexpr long long kSmallDicMaxCells = 5120;  // r, p, x, w, z: 200 KB of shared memory
+
+__device__ __forceinline__ void small_dic_apply(const double *r, double *w, double *z, const double *__restrict__ d,
+                                                const int32_t *__restrict__ rows,
+                                                const long long *__restrict__ lptr, int nlev, const Box &bx,
+                                                double lval, double uval)
+{
+    const int nx = bx.nx, ny = bx.ny, nz = bx.nz, pl = nx * ny;
+    for (int L = 0; L < nlev; ++L) {  // (L + D~) w = r
+        for (long long q = lptr[L] + threadIdx.x; q < lptr[L + 1]; q += kSmallThreads) {
+            const int c = rows[q];
+            const int i = c % nx, j = (c / nx) % ny, k = c / pl;
+            double acc = r[c];
+            if (k > 0) acc = acc - lval * w[c - pl];
+            if (j > 0) acc = acc - lval * w[c - nx];
+            if (i > 0) acc = acc - lval * w[c - 1];
+            w[c] = acc / d[c];
+        }
+        __syncthreads();
+    }
+    for (int L = nlev - 1; L >= 0; --L) {  // (D~ + L^T) z = D~ w
+        for (long long q = lptr[L] + threadIdx.x; q < lptr[L + 1]; q += kSmallThreads) {
+            const int c = rows[q];
+            const int i = c % nx, j = (c / nx) % ny, k = c / pl;
+            double acc = 0.0;
+            if (i < nx - 1) acc = acc + uval * z[c + 1];
+            if (j < ny - 1) acc = acc + uval * z[c + nx];
+            if (k < nz - 1) acc = acc + uval * z[c + pl];
+            z[c] = w[c] - acc / d[c];
+        }
+        __syncthreads();
+    }
+}
+
+template <int ORDER>
+__global__ void __launch_bounds__(kSmallThreads) cg_small_dic_kernel(Box bx, double off, double diag,
+                                                                     const double *__restrict__ b,
+                                                                     double *__restrict__ xout,
+                                                                     const double *__restrict__ d,
+                                                                     const int32_t *__restrict__ rows,
+                                                                     const long long *__restrict__ lptr, int nlev,
+                                                                     double lval, double uval, CgScalars *sc)
+{
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    __shared__ double bc[2];
+    const int n = (int)bx.cells();
+    double *r = sm, *p = sm + n, *x = sm + 2 * n, *w = sm + 3 * n, *z = sm + 4 * n;
+    const int t = threadIdx.x;
+    double bb = 0.0;
+    for (int c = t; c < n; c += kSmallThreads) {  // r = b, x = 0 (src/solver.py:130-140)
+        const double bi = b[c];
+        r[c] = bi;
+        x[c] = 0.0;
+        bb = bb + bi * bi;
+    }
+    __syncthreads();
+    small_dic_apply(r, w, z, d, rows, lptr, nlev, bx, lval, uval);  // z = M^-1 r (:141)
+    double rz = 0.0;
+    for (int c = t; c < n; c += kSmallThreads) rz = rz + r[c] * z[c];
+    bb = block_sum<kSmallThreads>(bb, red);
+    rz = block_sum<kSmallThreads>(rz, red);
+    if (t == 0) {
+        bc[0] = bb;
+        bc[1] = rz;
+    }
+    __syncthreads();
+    CgScalars s = *sc;
+    scalar_after_init(&s, bc[0], bc[1]);
+    while (!s.done) {
+        for (int c = t; c < n; c += kSmallThreads) p[c] = s.it == 0 ? z[c] : z[c] + s.beta * p[c];
+        __syncthreads();
+        double pap = 0.0;
+        for (int c = t; c < n; c += kSmallThreads) pap = pap + p[c] * small_ap<ORDER>(p, c, bx, off, diag);
+        pap = block_sum<kSmallThreads>(pap, red);
+        if (t == 0) bc[0] = pap;
+        __syncthreads();
+        scalar_after_dir(&s, bc[0]);
+        if (s.done) break;
+        const double alpha = s.alpha, malpha = -alpha;
+        double rr = 0.0;
+        for (int c = t; c < n; c += kSmallThreads) {
+            const double pc = p[c];
+            x[c] = x[c] + alpha * pc;
+            const double rn = r[c] + malpha * small_ap<ORDER>(p, c, bx, off, diag);
+            r[c] = rn;
+            rr = rr + rn * rn;
+        }
+        __syncthreads();
+        // z = M^-1 r and r.z before the stop test's beta (src/solver.py:163-166)
+        small_dic_apply(r, w, z, d, rows, lptr, nlev, bx, lval, uval);
+        rz = 0.0;
+        for (int c = t; c < n; c += kSmallThreads) rz = rz + r[c] * z[c];
+        rr = block_sum<kSmallThreads>(rr, red);
+        rz = block_sum<kSmallThreads>(rz, red);
+        if (t == 0) {
+            bc[0] = rr;
+            bc[1] = rz;
+        }
+        __syncthreads();
+        scalar_after_update<true>(&s, bc[0], bc[1]);
+    }
+    for (int c = t; c < n; c += kSmallThreads) xout[c] = x[c];
+    if (t == 0) *sc = s;
+}
+
 }  // namespace cf
 
 // ---------------------------------------------------------------- workspace
@@ -428,6 +539,7 @@ struct cf_cg {
     // DIC (CF_PRECOND_DIC): level-scheduled factor attached by cf_cg_set_dic
     bool has_dic = false;
     cf::DicData dic;
+    long long *dic_lptr = nullptr;  // device copy of the level pointers (small-grid DIC kernel)
     double *zbuf = nullptr, *wbuf = nullptr;
     // CF_CG_DIRECT=<batch> in the environment: host-driven loop instead of
     // the conditional graph (ncu cannot profile conditional-graph kernels)
@@ -689,6 +801,20 @@ template <int ORDER, int PK>
 static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, cudaStream_t s)
 {
     const char *ns = getenv("CF_NO_SMALL");
+    if (PK == PK_ZVEC && ws->n <= kSmallDicMaxCells && ws->dic.wave.ok && ws->dic_lptr && !x0 &&
+        !(ns && atoi(ns) > 0)) {
+        const size_t smem = 5 * (size_t)ws->n * sizeof(double);
+        CF_CUDA(cudaFuncSetAttribute(cg_small_dic_kernel<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        CF_CUDA(cudaEventRecord(ws->ev0, s));
+        const int nlev = (int)ws->dic.level_ptr.size() - 1;
+        cg_small_dic_kernel<ORDER><<<1, kSmallThreads, smem, s>>>(ws->bx, ws->off, ws->diag, b, ws->x, ws->dic.d,
+                                                                  ws->dic.rows, ws->dic_lptr, nlev,
+                                                                  ws->dic.wave.lval, ws->dic.wave.uval, ws->sc);
+        CF_CHECK_LAUNCH("cg_small_dic_kernel");
+        CF_CUDA(cudaEventRecord(ws->ev1, s));
+        return CF_OK;
+    }
     if (PK != PK_ZVEC && ws->n <= kSmallMaxCells && !(ns && atoi(ns) > 0)) {
         const size_t smem = 3 * (size_t)ws->n * sizeof(double);
         CF_CUDA(cudaFuncSetAttribute(cg_small_kernel<ORDER, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -897,6 +1023,7 @@ int cf_cg_destroy(cf_cg *ws)
     }
     for (double *b : {ws->r, ws->x, ws->p[0], ws->p[1], ws->jd, ws->partials, ws->zbuf, ws->wbuf, ws->r2})
         if (b) cudaFree(b);
+    if (ws->dic_lptr) cudaFree(ws->dic_lptr);
     if (ws->sc) cudaFree(ws->sc);
     if (ws->tk) cudaFree(ws->tk);
     if (ws->sc_host) cudaFreeHost(ws->sc_host);
@@ -983,6 +1110,13 @@ int cf_cg_set_dic(cf_cg *ws, const int32_t *lp, const int32_t *lc, const double 
     // the tiled-wavefront sweeps when the triangles are the grid's 7-point pattern
     int rcw = cf::dic_wave_setup(dd, ws->bx.nx, ws->bx.ny, ws->bx.nz, nullptr);
     if (rcw != CF_OK) return rcw;
+    if (ws->dic_lptr) cudaFree(ws->dic_lptr);
+    ws->dic_lptr = nullptr;
+    if (ws->n <= cf::kSmallDicMaxCells) {
+        CF_CUDA(cudaMalloc(&ws->dic_lptr, (size_t)(nlevels + 1) * sizeof(long long)));
+        CF_CUDA(cudaMemcpy(ws->dic_lptr, level_ptr_host, (size_t)(nlevels + 1) * sizeof(long long),
+                           cudaMemcpyHostToDevice));
+    }
     ws->has_dic = true;
     if (ws->exec[cf::PK_ZVEC]) {  // pointers changed: rebuild on the next solve
         cudaGraphExecDestroy(ws->exec[cf::PK_ZVEC]);
