@@ -78,11 +78,10 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd(DicWave dw, const dou
     if (threadIdx.x == 0) dw.prog_b[t] = 0;  // re-arm the backward sweep's counters (it runs after this launch)
     const int *left = a > 0 ? dw.prog_f + (t - 1) : nullptr;
     const int *below = b > 0 ? dw.prog_f + (t - ntx) : nullptr;
-    int seen_l = 0, seen_b = 0, peek_l = 0, peek_b = 0, last_l = 0, last_b = 0;
+    int seen_l = 0, seen_b = 0, peek_l = 0, peek_b = 0;
     double wk = 0.0;  // w at (i, j, k-1)
     const int nsteps = dw.nz + kWTX + kWTY - 2;
     // r and d of this thread's next cell (independent of the sweep: prefetched a step ahead)
-    const int kfirst = -ti - tj;  // k at step 0
     auto ld_rd = [&](int k, double &rv, double &dv) {
         if (col_ok && k >= 0 && k < dw.nz) {
             const long long o = base + pl * k;
@@ -91,7 +90,7 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd(DicWave dw, const dou
         }
     };
     double r_nx = 0.0, d_nx = 1.0;
-    ld_rd(kfirst, r_nx, d_nx);
+    ld_rd(-ti - tj, r_nx, d_nx);  // k at step 0
     // edge values from the neighbouring tiles, prefetched a step ahead; the
     // wait below keeps `slack` steps between the tiles so that both the
     // progress peek and these loads are normally satisfied a step early
@@ -110,21 +109,24 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd(DicWave dw, const dou
         // reads (a neighbour's counter ends at nsteps); the relaxed peeks were
         // issued a step earlier, a fence makes an accepted value an acquire
         if (threadIdx.x == 0) {
+            // A peek's value is only waited on when the cached counter no
+            // longer covers the diagonal; otherwise it stays in flight (with
+            // progress published every `pub` steps, one in ~pub steps is used)
             const int need_l = min(s + kWTX + slack, nsteps), need_b = min(s + kWTY + slack, nsteps);
             bool fresh = false;
-            if (left) {
+            if (left && seen_l < need_l) {
                 seen_l = max(seen_l, peek_l);
-                while (seen_l < need_l) seen_l = ld_relaxed_gpu(left), fresh = true;
+                while (seen_l < need_l) seen_l = ld_relaxed_gpu(left);
+                fresh = true;
+                peek_l = ld_relaxed_gpu(left);
             }
-            if (below) {
+            if (below && seen_b < need_b) {
                 seen_b = max(seen_b, peek_b);
-                while (seen_b < need_b) seen_b = ld_relaxed_gpu(below), fresh = true;
+                while (seen_b < need_b) seen_b = ld_relaxed_gpu(below);
+                fresh = true;
+                peek_b = ld_relaxed_gpu(below);
             }
-            if (fresh || seen_l != last_l || seen_b != last_b) fence_acq_rel_gpu();  // a newly observed value
-            last_l = seen_l;
-            last_b = seen_b;
-            if (left) peek_l = ld_relaxed_gpu(left);
-            if (below) peek_b = ld_relaxed_gpu(below);
+            if (fresh) fence_acq_rel_gpu();  // an accepted counter value acts as an acquire
         }
         tile_sync<kWTX * kWTY>();
         const int k = s - ti - tj;
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd(DicWave dw, const dou
     if (threadIdx.x == 0) dw.prog_f[t] = 0;  // re-arm the next forward sweep's counters
     const int *right = a < ntx - 1 ? dw.prog_b + (t + 1) : nullptr;
     const int *above = b < nty - 1 ? dw.prog_b + (t + ntx) : nullptr;
-    int seen_r = 0, seen_a = 0, peek_r = 0, peek_a = 0, last_r = 0, last_a = 0;
+    int seen_r = 0, seen_a = 0, peek_r = 0, peek_a = 0;
     double zk = 0.0;  // z at (i, j, k+1)
     const int nsteps = dw.nz + kWTX + kWTY - 2;
     // a tile's cells with the largest (i, j) start first: local distance from the top corner
@@ -205,19 +207,20 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd(DicWave dw, const dou
     for (int s = 0; s < nsteps; ++s) {
         if (threadIdx.x == 0) {
             const int need_r = min(s + kWTX + slack, nsteps), need_a = min(s + kWTY + slack, nsteps);
-            if (right) {
+            bool fresh = false;
+            if (right && seen_r < need_r) {
                 seen_r = max(seen_r, peek_r);
                 while (seen_r < need_r) seen_r = ld_relaxed_gpu(right);
+                fresh = true;
+                peek_r = ld_relaxed_gpu(right);
             }
-            if (above) {
+            if (above && seen_a < need_a) {
                 seen_a = max(seen_a, peek_a);
                 while (seen_a < need_a) seen_a = ld_relaxed_gpu(above);
+                fresh = true;
+                peek_a = ld_relaxed_gpu(above);
             }
-            if (seen_r != last_r || seen_a != last_a) fence_acq_rel_gpu();  // a newly observed value
-            last_r = seen_r;
-            last_a = seen_a;
-            if (right) peek_r = ld_relaxed_gpu(right);
-            if (above) peek_a = ld_relaxed_gpu(above);
+            if (fresh) fence_acq_rel_gpu();
         }
         tile_sync<kWTX * kWTY>();
         const int k = dw.nz - 1 - (s - ri - rj);
