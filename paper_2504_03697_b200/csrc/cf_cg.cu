@@ -547,7 +547,7 @@ struct cf_cg {
     // TMA-staged kernels (even nx >= 32; CF_NO_TMA=1 forces the LDG march)
     bool tma = false;
     // kernel form per CG kernel (cf::KernKind) and the pair-march geometry
-    int kind_dir = 0, kind_upd = 0;
+    int kind_dir = 0, kind_upd = 0, kind_upd_skip = -1;
     cf::PairGeom pg_dir{}, pg_upd{};
     cf::TmaGeom geom_dir{}, geom_upd{};
     CUtensorMap m_r{}, m_z{}, m_p[2]{}, m_ri{}, m_xi{}, m_pi[2]{};
@@ -579,7 +579,8 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
         double *p_new = ws->p[half ^ 1];
         // the TMA forms have no per-cell Jacobi vector
         const int kd = (PK == PK_JVEC && ws->kind_dir == KK_TMA) ? KK_PAIR : ws->kind_dir;
-        const int ku = (PK == PK_JVEC && ws->kind_upd == KK_TMA) ? KK_PAIR : ws->kind_upd;
+        int ku = (PK == PK_JVEC && ws->kind_upd == KK_TMA) ? KK_PAIR : ws->kind_upd;
+        if (half == 0 && ws->defer_x && ws->kind_upd_skip >= 0) ku = ws->kind_upd_skip;  // tuning override
         if (kd == KK_TMA) {
             const TmaGeom &gd = ws->geom_dir;
             cg_dir_tma<ORDER, PK><<<gd.ntx * gd.nty * gd.nchunk, kWSThreads, kDirSmem, s>>>(
@@ -933,6 +934,7 @@ static void set_grids(cf_cg *ws)
         cudaFuncSetAttribute(cg_pass_kernel<ORDER, PK_JCONST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kPassSmem);
     }
+    if (const char *e = getenv("CF_CG_UPD_SKIP")) ws->kind_upd_skip = kern_kind("CF_CG_UPD_SKIP", ws->kind_upd, ws->tma, pair_ok);
     const char *dx = getenv("CF_CG_DEFER_X");
     ws->defer_x = ws->kind_upd != KK_LDG && !(dx && atoi(dx) == 0);
 }
