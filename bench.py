@@ -203,7 +203,6 @@ def run_ours(args, rank, world, local_rank):
     cache = cf.PoissonCache()
     for _ in range(args.warmup):
         cf.step(state, cfg, cache)
-    ws = cache.operator(cfg)._cg_ws
 
     # ---- device-resident timed region
     barrier()
@@ -214,7 +213,7 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(args.steps):
             s = cf.step(state, cfg, cache)
             its.append(s.solve.iterations)
-            loop_ms += ws.last_loop_ms
+            loop_ms += cache.operator(cfg)._cg_ws.last_loop_ms
             # forces, advect, divergence, cg-init, correct + 2 kernels per iteration,
             # the while body is unrolled by two (an odd count adds 2 early-exit launches)
             launches += 5 + 4 * ((s.solve.iterations + 1) // 2)

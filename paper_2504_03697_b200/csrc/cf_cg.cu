@@ -281,18 +281,15 @@ PassGeom pass_geom(int nx, int ny, int nz)
 }
 
 // Host: geometry of the pair-march kernels -- 64 x kPairRows tiles, z cut into
-// chunks: at most ~kPairPlanes planes each (measured: enough CTAs in flight
-// to keep HBM busy at 256^3 / 512^3) and at least ~7 CTAs per SM in total
-// (the L2-resident 128^3 solve: 4 chunks 48 us/iteration, 16 chunks 36 us),
-// never below 4 planes.  env_name overrides the chunk count.
-constexpr int kPairPlanes = 32;
+// chunks by wave_chunks (8 resident 128-thread CTAs per SM, >= 4 planes per
+// chunk; measured 256^3: 9 chunks 2304 CTAs = 0.97 of two waves, vs 8 chunks
+// 207 -> 203 us per CG iteration; 5 chunks = 1280 CTAs, 1.08 waves, 240 us).
+// env_name overrides the chunk count.
 PairGeom pair_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, const char *env_name)
 {
     PairGeom g{nx, ny, nz, lo_halo, hi_halo, (nx + kPairX - 1) / kPairX, (ny + kPairRows - 1) / kPairRows, 1};
     const int tiles = g.ntx * g.nty;
-    const int by_planes = (nz + kPairPlanes - 1) / kPairPlanes;
-    const int by_ctas = (num_sms() * 7 + tiles - 1) / tiles;
-    int c = std::max(by_planes, std::min(by_ctas, std::max(1, nz / 4)));
+    int c = wave_chunks(tiles, nz, (long long)num_sms() * 8, 4);
     if (const char *e = env_name ? getenv(env_name) : nullptr) {
         const int v = atoi(e);
         if (v >= 1) c = v;
@@ -548,6 +545,9 @@ struct cf_cg {
     bool tma = false;
     // kernel form per CG kernel (cf::KernKind) and the pair-march geometry
     int kind_dir = 0, kind_upd = 0, kind_upd_skip = -1;
+    // pair-march direction kernel with the next plane's loads issued one
+    // iteration early (cf_cg_pair.cuh PF); CF_PAIR_PF=0/1 overrides
+    bool pair_pf = false;
     cf::PairGeom pg_dir{}, pg_upd{};
     cf::TmaGeom geom_dir{}, geom_upd{};
     CUtensorMap m_r{}, m_z{}, m_p[2]{}, m_ri{}, m_xi{}, m_pi[2]{};
@@ -588,9 +588,14 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
                 ws->partials, ws->tk, nullptr);
             CF_CHECK_LAUNCH("cg_dir_tma");
         } else if (kd == KK_PAIR) {
-            cg_dir_pair<ORDER, PK><<<ws->pg_dir.ctas(), kPairThreads, 0, s>>>(
-                ws->pg_dir, ws->off, ws->diag, PK == PK_ZVEC ? ws->zbuf : ws->r, ws->jd, p_old, p_new, zc, ws->sc,
-                ws->partials, ws->tk, nullptr);
+            if (ws->pair_pf)
+                cg_dir_pair<ORDER, PK, true><<<ws->pg_dir.ctas(), kPairThreads, 0, s>>>(
+                    ws->pg_dir, ws->off, ws->diag, PK == PK_ZVEC ? ws->zbuf : ws->r, ws->jd, p_old, p_new, zc, ws->sc,
+                    ws->partials, ws->tk, nullptr);
+            else
+                cg_dir_pair<ORDER, PK><<<ws->pg_dir.ctas(), kPairThreads, 0, s>>>(
+                    ws->pg_dir, ws->off, ws->diag, PK == PK_ZVEC ? ws->zbuf : ws->r, ws->jd, p_old, p_new, zc, ws->sc,
+                    ws->partials, ws->tk, nullptr);
             CF_CHECK_LAUNCH("cg_dir_pair");
         } else {
             cg_dir_kernel<ORDER, PK><<<ws->grid_dir, kMarchThreads, 0, s>>>(
@@ -921,6 +926,7 @@ static void set_grids(cf_cg *ws)
     ws->pg_upd = pair_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, "CF_PAIR_CHUNKS_UPD");
     ws->kind_dir = kern_kind("CF_CG_DIR", KK_PAIR, ws->tma, pair_ok);
     ws->kind_upd = kern_kind("CF_CG_UPD", KK_TMA, ws->tma, pair_ok);
+    if (const char *e = getenv("CF_PAIR_PF")) ws->pair_pf = atoi(e) != 0;
     // single-reduction CG (one kernel per iteration, cf_cg_pass.cuh): opt-in.
     // Measured at 256^3 it runs 215 us/iteration against 205 for the
     // two-kernel form (instruction-bound: ~64 % issue slots), so the default

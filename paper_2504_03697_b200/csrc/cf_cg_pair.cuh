@@ -108,7 +108,13 @@ __device__ __forceinline__ void pair_plane_step(const PairCoords &c, const PairG
 // directions between consecutive kernels (direction kernel down, update
 // kernel up), so each kernel starts on the planes its predecessor wrote
 // last -- the ones still resident in the 126 MB L2.
-template <int ORDER, bool REV, class Src, class Epi>
+//
+// PF: software-pipelined loads -- the raw operand of the next plane's far
+// neighbour (z-2 when marching down, z+2 up) is issued one iteration early, so
+// two planes' HBM reads are in flight per warp instead of one (the march is
+// long-scoreboard bound at ~45 % occupancy; r01b ncu).  Same values, same
+// arithmetic: results are bit-identical with or without PF.
+template <int ORDER, bool REV, class Src, class Epi, bool PF = false>
 __device__ __forceinline__ void pair_march(const PairCoords &c, const PairGeom &g, double off, double diag,
                                            const Src &src, Epi &epi)
 {
@@ -117,8 +123,10 @@ __device__ __forceinline__ void pair_march(const PairCoords &c, const PairGeom &
     if (REV) {
         const bool hzp1 = c.z1 <= c.zhi;
         const long long o1 = c.base + pl * (c.z1 - 1);
+        const int zstop = max(c.z0 - 1, c.zlo);  // lowest plane this chunk reads
         auto rp1 = src.raw2(hzp1 ? o1 + pl : o1);
         auto rc1 = src.raw2(o1);
+        auto rnx = src.raw2(PF && c.z1 - 2 >= zstop ? o1 - pl : o1);
         double2 cp = hzp1 ? src.form2(rp1, o1 + pl) : zero;
         double2 cc = src.form2(rc1, o1);
         if (hzp1 && c.z1 == g.nz) epi.halo(o1 + pl, cp);
@@ -126,7 +134,13 @@ __device__ __forceinline__ void pair_march(const PairCoords &c, const PairGeom &
             const long long o = c.base + pl * z;
             const bool hzm = z - 1 >= c.zlo;
             const long long om = hzm ? o - pl : o;
-            auto rm = src.raw2(om);
+            decltype(rnx) rm;
+            if (PF) {
+                rm = rnx;
+                rnx = src.raw2(z - 2 >= zstop ? o - 2 * pl : o);
+            } else {
+                rm = src.raw2(om);
+            }
             const double2 cm = hzm ? src.form2(rm, om) : zero;
             pair_plane_step<ORDER>(c, g, o, cm, cc, cp, off, diag, src, epi);
             if (hzm && z == 0) epi.halo(om, cm);
@@ -137,8 +151,10 @@ __device__ __forceinline__ void pair_march(const PairCoords &c, const PairGeom &
     }
     const bool hzm0 = c.z0 - 1 >= c.zlo;
     const long long o0 = c.base + pl * c.z0;
+    const int ztop = min(c.z1, c.zhi);  // highest plane this chunk reads
     auto rm0 = src.raw2(hzm0 ? o0 - pl : o0);
     auto rc0 = src.raw2(o0);
+    auto rnx = src.raw2(PF && c.z0 + 1 <= ztop ? o0 + pl : o0);
     double2 cm = hzm0 ? src.form2(rm0, o0 - pl) : zero;
     double2 cc = src.form2(rc0, o0);
     if (hzm0 && c.z0 - 1 == -1) epi.halo(o0 - pl, cm);
@@ -146,7 +162,13 @@ __device__ __forceinline__ void pair_march(const PairCoords &c, const PairGeom &
         const long long o = c.base + pl * z;
         const bool hzp = z + 1 <= c.zhi;
         const long long on = hzp ? o + pl : o;
-        auto rn = src.raw2(on);
+        decltype(rnx) rn;
+        if (PF) {
+            rn = rnx;
+            rnx = src.raw2(z + 2 <= ztop ? o + 2 * pl : o);
+        } else {
+            rn = src.raw2(on);
+        }
         const double2 cp = hzp ? src.form2(rn, on) : zero;
         pair_plane_step<ORDER>(c, g, o, cm, cc, cp, off, diag, src, epi);
         if (hzp && z + 1 == g.nz) epi.halo(on, cp);
@@ -212,7 +234,7 @@ struct UpdSrc {
 // recomputed from the exchanged r halo and stored so the update kernel's
 // stencil can read them (bit-identical to the neighbour's owned p).
 // The direction march of one block; returns the thread's partial p.Ap.
-template <int ORDER, int PK>
+template <int ORDER, int PK, bool PF = false>
 __device__ __forceinline__ double dir_pair_body(const PairGeom &g, int bid, double off, double diag,
                                                 const double *__restrict__ zsrc, const double *__restrict__ jd,
                                                 const double *__restrict__ p_old, double *__restrict__ p_new,
@@ -236,12 +258,12 @@ __device__ __forceinline__ double dir_pair_body(const PairGeom &g, int bid, doub
     } epi{p_new, c.valid, 0.0};
     if (c.row_ok) {
         const DirSrc<PK> src{zsrc, p_old, jd, zc, beta, first};
-        pair_march<ORDER, true>(c, g, off, diag, src, epi);
+        pair_march<ORDER, true, DirSrc<PK>, decltype(epi), PF>(c, g, off, diag, src, epi);
     }
     return epi.pap;
 }
 
-template <int ORDER, int PK>
+template <int ORDER, int PK, bool PF = false>
 __global__ void __launch_bounds__(kPairThreads, 8) cg_dir_pair(PairGeom g, double off, double diag,
                                                             const double *__restrict__ zsrc,
                                                             const double *__restrict__ jd,
@@ -252,7 +274,7 @@ __global__ void __launch_bounds__(kPairThreads, 8) cg_dir_pair(PairGeom g, doubl
     __shared__ double red[32];
     __shared__ int is_last;
     if (sc->done) return;
-    double pap = dir_pair_body<ORDER, PK>(g, blockIdx.x, off, diag, zsrc, jd, p_old, p_new, zc, sc->beta,
+    double pap = dir_pair_body<ORDER, PK, PF>(g, blockIdx.x, off, diag, zsrc, jd, p_old, p_new, zc, sc->beta,
                                           sc->it == 0);
     pap = block_sum<kPairThreads>(pap, red);
     if (threadIdx.x == 0) partials[blockIdx.x] = pap;

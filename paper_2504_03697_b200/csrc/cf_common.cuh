@@ -43,6 +43,9 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 int num_sms();
 // Resident blocks per SM for `kernel` at `threads` threads and `smem` bytes.
 int blocks_per_sm(const void *kernel, int threads, size_t smem);
+// z-chunk count for a z-march over `tiles` xy tiles and nz planes with
+// `slots` resident CTAs on the device: wave-quantisation aware (cf_runtime.cu).
+int wave_chunks(long long tiles, int nz, long long slots, int min_planes);
 
 // Per-process scratch for one-shot reductions (cf_dot etc.).
 constexpr size_t kScratchPartials = 1 << 16;

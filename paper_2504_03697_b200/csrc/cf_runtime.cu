@@ -36,6 +36,28 @@ int blocks_per_sm(const void *kernel, int threads, size_t smem)
     return b;
 }
 
+int wave_chunks(long long tiles, int nz, long long slots, int min_planes)
+{
+    // Each SM runs ceil(tiles*c / slots) waves of CTAs, each marching nz/c
+    // planes plus ~2 planes of halo / pipeline fill; pick the chunk count c
+    // with the least per-SM march length.  (256^3: a partly filled second
+    // wave -- e.g. 1280 pair CTAs on 1184 slots -- cost 15 % of the kernel.)
+    if (tiles < 1) tiles = 1;
+    if (slots < 1) slots = 1;
+    const int cmax = nz / (min_planes > 0 ? min_planes : 1) > 1 ? nz / (min_planes > 0 ? min_planes : 1) : 1;
+    int best = 1;
+    double best_cost = 1e300;
+    for (int c = 1; c <= cmax; ++c) {
+        const long long waves = (tiles * c + slots - 1) / slots;
+        const double cost = (double)waves * ((double)nz / c + 2.0);
+        if (cost < best_cost * 0.999) {
+            best_cost = cost;
+            best = c;
+        }
+    }
+    return best;
+}
+
 static std::mutex g_scratch_mu;
 static double *g_scratch = nullptr;
 static double *g_host_slot = nullptr;

@@ -52,12 +52,7 @@ TmaGeom tma_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, int blocks_pe
     g.nty = (ny + kTTY - 1) / kTTY;
     const long long tiles = (long long)g.ntx * g.nty;
     const long long cap = (long long)num_sms() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
-    // one resident wave: every z-chunk of every tile marches concurrently, so
-    // a tile's halo rows are read by its neighbours at about the same time
-    long long c = tiles <= cap ? cap / tiles : 1;
-    const long long max_c = nz / 8 > 0 ? nz / 8 : 1;  // keep >= 8 planes per chunk
-    if (c > max_c) c = max_c;
-    if (c < 1) c = 1;
+    long long c = wave_chunks(tiles, nz, cap, 8);
     if (const char *e = getenv("CF_TMA_CHUNKS")) {  // debugging / tuning override
         const int v = atoi(e);
         if (v >= 1 && v <= nz) c = v;
