@@ -168,9 +168,9 @@ def run_reference(args, rank):
 
 def load_traffic():
     """Per-iteration DRAM bytes of the fused CG kernels from the committed ncu summary."""
-    path = os.path.join(ROOT, "profiles", "ncu_cg_r01b.json")
-    if not os.path.exists(path):
-        path = os.path.join(ROOT, "profiles", "ncu_cg_r01.json")
+    import glob
+    found = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_cg_r*.json")))
+    path = found[-1] if found else os.path.join(ROOT, "profiles", "ncu_cg_r01.json")
     try:
         with open(path) as f:
             return json.load(f).get("dram_bytes_per_iteration")
@@ -282,7 +282,7 @@ def run_ours(args, rank, world, local_rank):
         "fused_iter_frac": achieved / peak,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "fused CG iteration (cg_dir_pair + cg_update_tma; x updated every 2nd iteration)",
+                     "kernel": "fused CG iteration (cg_dir_lean + cg_update_tma; x updated every 2nd iteration)",
                      "algorithmic_bytes_per_iteration": alg_bytes, "design_bytes_per_iteration": 60 * cells,
                      "peak_kind": peak_kind},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

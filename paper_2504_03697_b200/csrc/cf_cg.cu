@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(kMarchThreads) cg_x_fixup(long long n, double 
 #include "cf_cg_tma.cuh"
 #include "cf_cg_pair.cuh"
 #include "cf_cg_pass.cuh"
+#include "cf_cg_lean.cuh"
 
 // Host: single-reduction pass geometry (32 x 16 tiles; chunks of ~32 planes,
 // the 4-plane pipeline prologue amortised; CF_PASS_CHUNKS overrides).
@@ -298,12 +299,29 @@ PairGeom pair_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, const char 
     return g;
 }
 
-// Which form runs each CG kernel: the register pair march, the TMA pipeline,
-// or the scalar LDG march (odd nx).  Defaults (measured, tools/kernel_matrix.sh,
-// 256^3 / 512^3): direction = pair march run top-down, update = TMA -- 209.6 /
-// 1709 us per iteration against 217.3 / 1738 for TMA + TMA.
-// CF_CG_DIR / CF_CG_UPD = "pair" | "tma" | "ldg" override.
-enum KernKind { KK_LDG = 0, KK_TMA = 1, KK_PAIR = 2 };
+// Host: geometry of the lean kernels -- 64 x rows tiles (rows warps per CTA),
+// z chunks by wave_chunks over the resident CTAs (ctas4: resident 4-row CTAs
+// per SM; the register budget is per thread, so CTAs scale as 4 / rows).
+PairGeom lean_geom(int nx, int ny, int nz, int rows, int ctas4)
+{
+    PairGeom g{nx, ny, nz, 0, 0, (nx + kPairX - 1) / kPairX, (ny + rows - 1) / rows, 1};
+    const long long slots = (long long)num_sms() * std::max(1, ctas4 * kPairRows / rows);
+    g.nchunk = wave_chunks((long long)g.ntx * g.nty, nz, slots, 4);
+    if (const char *e = getenv("CF_LEAN_CHUNKS")) {
+        const int v = atoi(e);
+        if (v >= 1 && v <= nz) g.nchunk = v;
+    }
+    return g;
+}
+
+// Which form runs each CG kernel: the lean register march (cf_cg_lean.cuh),
+// the pair march, the TMA pipeline, or the scalar LDG march (odd nx).
+// Defaults (measured, tools/gpu_lean.sh, 256^3 / 512^3): direction = lean
+// march run top-down (8-row CTAs), update = TMA -- 193 / 1425 us per
+// iteration against 207 / 1525 with the pair-march direction kernel and
+// 198 / 1460 with the lean update kernel.
+// CF_CG_DIR / CF_CG_UPD = "lean" | "pair" | "tma" | "ldg" override.
+enum KernKind { KK_LDG = 0, KK_TMA = 1, KK_PAIR = 2, KK_LEAN = 3 };
 int kern_kind(const char *env_name, int deflt, bool tma_ok, bool pair_ok)
 {
     int k = deflt;
@@ -311,7 +329,9 @@ int kern_kind(const char *env_name, int deflt, bool tma_ok, bool pair_ok)
         if (!strcmp(e, "pair")) k = KK_PAIR;
         else if (!strcmp(e, "tma")) k = KK_TMA;
         else if (!strcmp(e, "ldg")) k = KK_LDG;
+        else if (!strcmp(e, "lean")) k = KK_LEAN;
     }
+    if (k == KK_LEAN && !pair_ok) k = KK_LDG;
     if (k == KK_TMA && !tma_ok) k = pair_ok ? KK_PAIR : KK_LDG;
     if (k == KK_PAIR && !pair_ok) k = KK_LDG;
     return k;
@@ -547,7 +567,10 @@ struct cf_cg {
     int kind_dir = 0, kind_upd = 0, kind_upd_skip = -1;
     // pair-march direction kernel with the next plane's loads issued one
     // iteration early (cf_cg_pair.cuh PF); CF_PAIR_PF=0/1 overrides
-    bool pair_pf = false;
+    int pair_pf = 0;
+    // lean kernels (cf_cg_lean.cuh): warps (tile rows) per CTA, CF_LEAN_ROWS
+    int lean_rows = 8;
+    cf::PairGeom lg_dir{}, lg_upd{};
     cf::PairGeom pg_dir{}, pg_upd{};
     cf::TmaGeom geom_dir{}, geom_upd{};
     CUtensorMap m_r{}, m_z{}, m_p[2]{}, m_ri{}, m_xi{}, m_pi[2]{};
@@ -571,6 +594,42 @@ struct cf_cg {
 
 namespace cf {
 
+template <int ORDER, int PK, int PF, int ROWS>
+static void dir_lean_go(cf_cg *ws, cudaStream_t s, const double *zs, const double *po, double *pn, double zc)
+{
+    cg_dir_lean<ORDER, PK, PF, ROWS><<<ws->lg_dir.ctas(), 32 * ROWS, 0, s>>>(ws->lg_dir, ws->off, ws->diag, zs, po, pn,
+                                                                          zc, ws->sc, ws->partials, ws->tk);
+}
+
+template <int ORDER, int PK>
+static void dir_lean_launch(cf_cg *ws, cudaStream_t s, const double *zs, const double *po, double *pn, double zc)
+{
+    switch (ws->lean_rows * 10 + ws->pair_pf) {
+    case 41: dir_lean_go<ORDER, PK, 1, 4>(ws, s, zs, po, pn, zc); break;
+    case 42: dir_lean_go<ORDER, PK, 2, 4>(ws, s, zs, po, pn, zc); break;
+    case 80: dir_lean_go<ORDER, PK, 0, 8>(ws, s, zs, po, pn, zc); break;
+    case 160: dir_lean_go<ORDER, PK, 0, 16>(ws, s, zs, po, pn, zc); break;
+    default: dir_lean_go<ORDER, PK, 0, 4>(ws, s, zs, po, pn, zc); break;
+    }
+}
+
+template <int ORDER, int PK, int XM, int ROWS>
+static void upd_lean_go(cf_cg *ws, cudaStream_t s, const double *p, const double *q, double zc, int use_cond,
+                        cudaGraphConditionalHandle cond)
+{
+    cg_update_lean<ORDER, PK, XM, ROWS><<<ws->lg_upd.ctas(), 32 * ROWS, 0, s>>>(
+        ws->lg_upd, ws->off, ws->diag, p, q, ws->r, ws->x, zc, ws->sc, ws->partials, ws->tk, use_cond, cond);
+}
+
+template <int ORDER, int PK, int XM>
+static void upd_lean_launch(cf_cg *ws, cudaStream_t s, const double *p, const double *q, double zc, int use_cond,
+                            cudaGraphConditionalHandle cond)
+{
+    if (ws->lean_rows == 8) upd_lean_go<ORDER, PK, XM, 8>(ws, s, p, q, zc, use_cond, cond);
+    else if (ws->lean_rows == 16) upd_lean_go<ORDER, PK, XM, 16>(ws, s, p, q, zc, use_cond, cond);
+    else upd_lean_go<ORDER, PK, XM, 4>(ws, s, p, q, zc, use_cond, cond);
+}
+
 template <int ORDER, int PK>
 static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond, int use_cond = 1)
 {
@@ -578,8 +637,9 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
         const double *p_old = ws->p[half];
         double *p_new = ws->p[half ^ 1];
         // the TMA forms have no per-cell Jacobi vector
-        const int kd = (PK == PK_JVEC && ws->kind_dir == KK_TMA) ? KK_PAIR : ws->kind_dir;
-        int ku = (PK == PK_JVEC && ws->kind_upd == KK_TMA) ? KK_PAIR : ws->kind_upd;
+        // the TMA and lean forms have no per-cell Jacobi vector
+        const int kd = (PK == PK_JVEC && (ws->kind_dir == KK_TMA || ws->kind_dir == KK_LEAN)) ? KK_PAIR : ws->kind_dir;
+        int ku = (PK == PK_JVEC && (ws->kind_upd == KK_TMA || ws->kind_upd == KK_LEAN)) ? KK_PAIR : ws->kind_upd;
         if (half == 0 && ws->defer_x && ws->kind_upd_skip >= 0) ku = ws->kind_upd_skip;  // tuning override
         if (kd == KK_TMA) {
             const TmaGeom &gd = ws->geom_dir;
@@ -587,6 +647,9 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
                 PK == PK_ZVEC ? ws->m_z : ws->m_r, ws->m_p[half], gd, ws->off, ws->diag, p_new, zc, ws->sc,
                 ws->partials, ws->tk, nullptr);
             CF_CHECK_LAUNCH("cg_dir_tma");
+        } else if (kd == KK_LEAN) {
+            dir_lean_launch<ORDER, PK>(ws, s, PK == PK_ZVEC ? ws->zbuf : ws->r, p_old, p_new, zc);
+            CF_CHECK_LAUNCH("cg_dir_lean");
         } else if (kd == KK_PAIR) {
             if (ws->pair_pf)
                 cg_dir_pair<ORDER, PK, true><<<ws->pg_dir.ctas(), kPairThreads, 0, s>>>(
@@ -619,6 +682,11 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
                     ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc,
                     ws->sc, ws->partials, ws->tk, use_cond, cond, nullptr);
             CF_CHECK_LAUNCH("cg_update_tma");
+        } else if (ku == KK_LEAN) {
+            if (!ws->defer_x) upd_lean_launch<ORDER, PK, XM_EACH>(ws, s, p_new, p_old, zc, use_cond, cond);
+            else if (half == 0) upd_lean_launch<ORDER, PK, XM_SKIP>(ws, s, p_new, p_old, zc, use_cond, cond);
+            else upd_lean_launch<ORDER, PK, XM_DOUBLE>(ws, s, p_new, p_old, zc, use_cond, cond);
+            CF_CHECK_LAUNCH("cg_update_lean");
         } else if (ku == KK_PAIR) {
             const int nb = ws->pg_upd.ctas();
             if (!ws->defer_x)
@@ -924,9 +992,15 @@ static void set_grids(cf_cg *ws)
     const bool pair_ok = ws->bx.nx % 2 == 0 && !(no_tma && atoi(no_tma) > 0);
     ws->pg_dir = pair_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, "CF_PAIR_CHUNKS_DIR");
     ws->pg_upd = pair_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, "CF_PAIR_CHUNKS_UPD");
-    ws->kind_dir = kern_kind("CF_CG_DIR", KK_PAIR, ws->tma, pair_ok);
+    ws->kind_dir = kern_kind("CF_CG_DIR", KK_LEAN, ws->tma, pair_ok);
     ws->kind_upd = kern_kind("CF_CG_UPD", KK_TMA, ws->tma, pair_ok);
-    if (const char *e = getenv("CF_PAIR_PF")) ws->pair_pf = atoi(e) != 0;
+    if (const char *e = getenv("CF_PAIR_PF")) ws->pair_pf = atoi(e);
+    // 32-bit cell indices in the lean kernel
+    if (ws->kind_dir == KK_LEAN && ws->n + kLeanPad >= (1LL << 32)) ws->kind_dir = KK_PAIR;
+    if (ws->kind_upd == KK_LEAN && ws->n + kLeanPad >= (1LL << 32)) ws->kind_upd = KK_PAIR;
+    if (const char *e = getenv("CF_LEAN_ROWS")) ws->lean_rows = atoi(e) == 4 ? 4 : (atoi(e) == 16 ? 16 : 8);
+    ws->lg_dir = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, ws->pair_pf >= 2 ? 6 : 8);
+    ws->lg_upd = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);
     // single-reduction CG (one kernel per iteration, cf_cg_pass.cuh): opt-in.
     // Measured at 256^3 it runs 215 us/iteration against 205 for the
     // two-kernel form (instruction-bound: ~64 % issue slots), so the default
@@ -990,11 +1064,17 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
         if (g2 > maxg) maxg = g2;
     }
     maxg = std::max(maxg, std::max(ws->pg_dir.ctas(), ws->pg_upd.ctas()));
+    maxg = std::max(maxg, std::max(ws->lg_dir.ctas(), ws->lg_upd.ctas()));
     if (ws->pass) maxg = std::max(maxg, ws->pass_g.ctas());
     size_t vec = (size_t)ws->n * sizeof(double);
     cudaError_t e = cudaSuccess;
-    for (double **b : {&ws->r, &ws->x, &ws->p[0], &ws->p[1]})
-        if (e == cudaSuccess) e = cudaMalloc(b, vec);
+    // every CG vector carries kLeanPad zeroed doubles after its n cells (the
+    // lean direction kernel reads out-of-domain neighbours there)
+    const size_t pad = cf::kLeanPad * sizeof(double);
+    for (double **b : {&ws->r, &ws->x, &ws->p[0], &ws->p[1]}) {
+        if (e == cudaSuccess) e = cudaMalloc(b, vec + pad);
+        if (e == cudaSuccess) e = cudaMemsetAsync(reinterpret_cast<char *>(*b) + vec, 0, pad, cf::as_stream(stream));
+    }
     if (e == cudaSuccess) e = cudaMalloc(&ws->partials, sizeof(double) * 3 * (size_t)maxg);
     if (e == cudaSuccess && ws->pass) e = cudaMalloc(&ws->r2, vec);
     if (e == cudaSuccess) e = cudaMalloc(&ws->sc, sizeof(cf::CgScalars));
@@ -1104,7 +1184,10 @@ int cf_cg_set_dic(cf_cg *ws, const int32_t *lp, const int32_t *lc, const double 
                "cf_cg_set_dic: null argument");
     CF_REQUIRE(level_ptr_host[nlevels] == ws->n, "cf_cg_set_dic: level schedule does not cover the grid");
     std::lock_guard<std::mutex> lk(ws->mu);
-    if (!ws->zbuf) CF_CUDA(cudaMalloc(&ws->zbuf, (size_t)ws->n * sizeof(double)));
+    if (!ws->zbuf) {
+        CF_CUDA(cudaMalloc(&ws->zbuf, (size_t)(ws->n + cf::kLeanPad) * sizeof(double)));
+        CF_CUDA(cudaMemset(ws->zbuf + ws->n, 0, cf::kLeanPad * sizeof(double)));
+    }
     if (!ws->wbuf) CF_CUDA(cudaMalloc(&ws->wbuf, (size_t)ws->n * sizeof(double)));
     if (ws->tma && !cf::make_map(&ws->m_z, ws->zbuf, ws->bx.nx, ws->bx.ny, ws->bx.nz, cf::kHX, cf::kHY))
         ws->tma = false;
