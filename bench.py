@@ -22,8 +22,10 @@ cpu_baseline: the oracle port (oracle/, the reference's algorithm in C with
           the reference's WorkerPool chunking) on a bounded sample: 256^3
           Jacobi PCG iterations with the symmetric SpMV, all host threads.
 --impl reference: that CPU path alone, as the driver's reference arm.
---gpus N > 1 (torchrun): the same 256^3 problem z-slab sharded one slab per
-          GPU (strong scaling; NCCL all-reduce + halo send/recv), max over ranks.
+--gpus N > 1 (torchrun): z-slab decomposition, one slab per GPU, max over
+          ranks.  Default --scaling weak: the cavity extruded to 256x256x(256*N),
+          one 256^3 slab per GPU (value in 256^3-equivalent CG iterations/s);
+          --scaling strong: the 256^3 cube split over the GPUs.
 """
 
 from __future__ import annotations
@@ -155,8 +157,12 @@ def run_reference(args, rank):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cavity-{n}^3 pressure solve (CPU sample)", "n": n, "tol": 1e-8},
+        "higher_is_better": True, "scaling": args.scaling if args.gpus > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cavity-{n}^3 pressure solve (CPU sample)", "n": n, "tol": 1e-8,
+                   # CPU cost per iteration is linear in cells, so the n^3 rate is
+                   # also the n^3-equivalent rate of the weak-scaling boxes
+                   "value_normalisation": "n^3-equivalent CG iterations/s"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -299,11 +305,18 @@ def run_ours(args, rank, world, local_rank):
 
 
 def run_slabs(args, cfg, rank, world, local_rank, barrier):
-    """N > 1: the same 256^3 cavity z-slab sharded over the ranks (strong
-    scaling), one slab per GPU: velocity/pressure halos by NCCL P2P; the CG
-    with its collectives fused into the kernels over peer memory (cf_pcg,
-    default) or as NCCL all-reduce + r-halo send/recv (cf_dcg,
-    --collective nccl)."""
+    """N > 1: the cavity z-slab sharded over the ranks, one slab per GPU:
+    velocity/pressure halos by NCCL P2P; the CG with its collectives fused
+    into the kernels over peer memory (cf_pcg, default) or as NCCL all-reduce
+    + r-halo send/recv (cf_dcg, --collective nccl).
+
+    --scaling weak (default): the config-4 cavity extruded in z to
+    n x n x (n*N) cells, one n^3 slab per GPU (the per-GPU work of the N=1
+    run; BASELINE config 5's weak-scaling form).  value = global CG
+    iterations/s x cells / n^3, i.e. n^3-equivalent iterations/s, the N=1
+    unit.  --scaling strong: the n^3 cube split over the N GPUs."""
+    import dataclasses
+
     import torch
     import torch.distributed as dist
 
@@ -311,7 +324,12 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
     from paper_2504_03697_b200.parallel import SlabDecomposition
 
     n = cfg.n
-    dec = SlabDecomposition(n, n, n, world, rank)
+    weak = args.scaling == "weak"
+    nz = n * world if weak else n
+    if weak:
+        cfg = dataclasses.replace(cfg, shape=(n, n, nz))
+    norm = nz / n  # cells / n^3
+    dec = SlabDecomposition(n, n, nz, world, rank)
     sim = SlabSim(cfg, [dec.z0, dec.z1], distributed=True, collective=args.collective)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -331,21 +349,20 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
     t = torch.tensor([ms, loop_ms], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, loop_max = float(t[0]), float(t[1])
-    value = sum(its) / (ms_max / 1e3)  # global CG iterations (every rank runs the same ones)
-    # e2e: each rank's slab state through pinned host memory every step
+    value = norm * sum(its) / (ms_max / 1e3)  # global CG iterations (every rank runs the same ones)
+    # e2e: each rank's slab state through pinned host memory every step --
+    # upload u, v, w (the cold-start pressure solve's inputs), read u, v, w, p back
     sl = sim.slabs[0]
-    pinned = None
+    phys = [*sl.vel[sl.cur], sl.p]
+    pinned = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in phys]
+    for h_, d_ in zip(pinned, phys):
+        h_.copy_(d_)
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     e2.record(stream)
     e2e_its = 0
     for _ in range(args.steps):
-        phys = [*sl.vel[sl.cur], sl.p]
-        if pinned is None:
-            pinned = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in phys]
-            for h_, d_ in zip(pinned, phys):
-                h_.copy_(d_)
-        for h_, d_ in zip(pinned, phys):
+        for h_, d_ in zip(pinned[:3], [*sl.vel[sl.cur]]):
             d_.copy_(h_, non_blocking=True)
         s = sim.step()
         e2e_its += s.solve.iterations
@@ -355,8 +372,9 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
     barrier()
     t2 = torch.tensor([e2.elapsed_time(e3)], device="cuda", dtype=torch.float64)
     dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-    e2e_value = e2e_its / (float(t2[0]) / 1e3)
-    bytes_rank = sum(x.numel() * x.element_size() for x in [*sl.vel[sl.cur], sl.p])
+    e2e_value = norm * e2e_its / (float(t2[0]) / 1e3)
+    bytes_in = sum(x.numel() * x.element_size() for x in phys[:3])
+    bytes_out = sum(x.numel() * x.element_size() for x in phys)
     if rank != 0:
         return 0
     peak, peak_kind = peaks()
@@ -366,9 +384,13 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
     print(json.dumps({
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"lid-driven cavity {n}^3 (BASELINE config 4), z-slab over {world} GPUs",
-                   "n": n, "h": 1.0 / n, "dt": args.dt, "tol": 1e-8, "preconditioner": "jacobi",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": (f"lid-driven cavity {n}x{n}x{nz} (BASELINE config 4 extruded in z), one {n}^3 "
+                                f"z-slab per GPU" if weak else
+                                f"lid-driven cavity {n}^3 (BASELINE config 4), z-slab over {world} GPUs"),
+                   "shape": [n, n, nz], "n": n, "h": 1.0 / n,
+                   "value_normalisation": ("global CG iterations/s x cells/n^3 (n^3-equivalent iterations/s)"
+                                           if weak else "global CG iterations/s"), "dt": args.dt, "tol": 1e-8, "preconditioner": "jacobi",
                    "variant": "optimized", "physics": "reference (lid acceleration, inviscid)",
                    "parallelism": f"zslab{world}", "collective": args.collective, "l2": "inputs larger than L2 (no flush needed)"},
         "sim_steps_per_s": args.steps / (ms_max / 1e3), "cg_iterations": its,
@@ -376,8 +398,8 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "kernel": f"per-GPU z-slab CG iteration (dir + update + all-reduces + r halo; {args.collective})",
                      "algorithmic_bytes_per_iteration": 88 * cells_rank, "peak_kind": peak_kind},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_rank * world,
-                "d2h_bytes_per_step": bytes_rank * world},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_in * world,
+                "d2h_bytes_per_step": bytes_out * world},
         "gpu_launches": sum(6 * i + 10 for i in its),
         "clocks": clocks.summary(),
     }))
@@ -397,6 +419,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--collective", choices=("p2p", "nccl"), default="p2p",
                     help="z-slab CG collectives (N > 1): fused peer-memory kernels, or NCCL calls")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="N > 1: one n^3 slab per GPU (weak, default) or the n^3 cube split over the GPUs (strong)")
     ap.add_argument("--force-slabs", action="store_true",
                     help="run the z-slab/NCCL path even on one rank (plumbing check)")
     args = ap.parse_args()
