@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(kMarchThreads) cg_x_fixup(long long n, double 
 #include "cf_cg_pair.cuh"
 #include "cf_cg_pass.cuh"
 #include "cf_cg_lean.cuh"
+#include "cf_cg_lpass.cuh"
 
 // Host: single-reduction pass geometry (32 x 16 tiles; chunks of ~32 planes,
 // the 4-plane pipeline prologue amortised; CF_PASS_CHUNKS overrides).
@@ -579,6 +580,9 @@ struct cf_cg {
     // single-reduction CG (cf_cg_pass.cuh): one kernel per iteration; r ping-pongs
     bool pass = false;
     cf::PassGeom pass_g{};
+    // lean pass kernel (cf_cg_lpass.cuh; CF_PASS_FORM=old selects cg_pass_kernel)
+    int pass_form = 1;  // 0 cg_pass_kernel, 1 / 2 cg_lpass_kernel with 8 / 16-row tiles (CF_PASS_FORM=old|lean|lean16)
+    cf::PairGeom lpass_g{};
     double *r2 = nullptr;
     cudaGraphExec_t exec_pass[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaGraph_t graph_pass[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -796,6 +800,20 @@ static int pass_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphConditionalH
     for (int half = 0; half < 2; ++half) {
         const double *r_in = half ? ws->r2 : ws->r;
         double *r_out = half ? ws->r : ws->r2;
+        if (ws->pass_form == 2) {
+            cg_lpass_kernel<ORDER, PK, 16><<<ws->lpass_g.ctas(), Lp<16>::Threads, Lp<16>::Smem, s>>>(
+                ws->lpass_g, ws->off, ws->diag, zc, r_in, r_out, ws->p[half], ws->p[half ^ 1], ws->x, ws->sc,
+                ws->partials, ws->tk, use_cond, cond);
+            CF_CHECK_LAUNCH("cg_lpass_kernel");
+            continue;
+        }
+        if (ws->pass_form == 1) {
+            cg_lpass_kernel<ORDER, PK, 8><<<ws->lpass_g.ctas(), Lp<8>::Threads, Lp<8>::Smem, s>>>(
+                ws->lpass_g, ws->off, ws->diag, zc, r_in, r_out, ws->p[half], ws->p[half ^ 1], ws->x, ws->sc,
+                ws->partials, ws->tk, use_cond, cond);
+            CF_CHECK_LAUNCH("cg_lpass_kernel");
+            continue;
+        }
         cg_pass_kernel<ORDER, PK><<<g.ctas(), kPassThreads, kPassSmem, s>>>(
             g, ws->off, ws->diag, zc, r_in, r_out, ws->p[half], ws->p[half ^ 1], ws->x, ws->sc, ws->partials, ws->tk,
             use_cond, cond);
@@ -1013,6 +1031,31 @@ static void set_grids(cf_cg *ws)
                              (int)kPassSmem);
         cudaFuncSetAttribute(cg_pass_kernel<ORDER, PK_JCONST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kPassSmem);
+        const char *pf = getenv("CF_PASS_FORM");
+        ws->pass_form = pf && !strcmp(pf, "old") ? 0 : (pf && !strcmp(pf, "lean16") ? 2 : 1);
+        if (ws->n + kLeanPad >= (1LL << 32)) ws->pass_form = 0;
+        cudaFuncSetAttribute(cg_lpass_kernel<ORDER, PK_NONE, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Lp<8>::Smem);
+        cudaFuncSetAttribute(cg_lpass_kernel<ORDER, PK_JCONST, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Lp<8>::Smem);
+        cudaFuncSetAttribute(cg_lpass_kernel<ORDER, PK_NONE, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Lp<16>::Smem);
+        cudaFuncSetAttribute(cg_lpass_kernel<ORDER, PK_JCONST, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Lp<16>::Smem);
+        const int rows = ws->pass_form == 2 ? 16 : 8;
+        PairGeom lg{ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, (ws->bx.nx + kPairX - 1) / kPairX,
+                    (ws->bx.ny + rows - 1) / rows, 1};
+        const int bps = ws->pass_form == 2
+                            ? blocks_per_sm((const void *)cg_lpass_kernel<ORDER, PK_JCONST, 16>, Lp<16>::Threads,
+                                            Lp<16>::Smem)
+                            : blocks_per_sm((const void *)cg_lpass_kernel<ORDER, PK_JCONST, 8>, Lp<8>::Threads,
+                                            Lp<8>::Smem);
+        lg.nchunk = wave_chunks((long long)lg.ntx * lg.nty, lg.nz, (long long)num_sms() * bps, 8);
+        if (const char *e = getenv("CF_PASS_CHUNKS")) {
+            const int v = atoi(e);
+            if (v >= 1 && v <= lg.nz) lg.nchunk = v;
+        }
+        ws->lpass_g = lg;
     }
     if (const char *e = getenv("CF_CG_UPD_SKIP")) ws->kind_upd_skip = kern_kind("CF_CG_UPD_SKIP", ws->kind_upd, ws->tma, pair_ok);
     const char *dx = getenv("CF_CG_DEFER_X");
@@ -1065,7 +1108,7 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
     }
     maxg = std::max(maxg, std::max(ws->pg_dir.ctas(), ws->pg_upd.ctas()));
     maxg = std::max(maxg, std::max(ws->lg_dir.ctas(), ws->lg_upd.ctas()));
-    if (ws->pass) maxg = std::max(maxg, ws->pass_g.ctas());
+    if (ws->pass) maxg = std::max(maxg, std::max(ws->pass_g.ctas(), ws->lpass_g.ctas()));
     size_t vec = (size_t)ws->n * sizeof(double);
     cudaError_t e = cudaSuccess;
     // every CG vector carries kLeanPad zeroed doubles after its n cells (the
@@ -1076,7 +1119,9 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
         if (e == cudaSuccess) e = cudaMemsetAsync(reinterpret_cast<char *>(*b) + vec, 0, pad, cf::as_stream(stream));
     }
     if (e == cudaSuccess) e = cudaMalloc(&ws->partials, sizeof(double) * 3 * (size_t)maxg);
-    if (e == cudaSuccess && ws->pass) e = cudaMalloc(&ws->r2, vec);
+    if (e == cudaSuccess && ws->pass) e = cudaMalloc(&ws->r2, vec + pad);
+    if (e == cudaSuccess && ws->pass)
+        e = cudaMemsetAsync(reinterpret_cast<char *>(ws->r2) + vec, 0, pad, cf::as_stream(stream));
     if (e == cudaSuccess) e = cudaMalloc(&ws->sc, sizeof(cf::CgScalars));
     if (e == cudaSuccess) e = cudaMalloc(&ws->tk, sizeof(cf::CgTickets));
     if (e == cudaSuccess) e = cudaMemsetAsync(ws->tk, 0, sizeof(cf::CgTickets), cf::as_stream(stream));
