@@ -608,13 +608,15 @@ static void dir_lean_go(cf_cg *ws, cudaStream_t s, const double *zs, const doubl
 template <int ORDER, int PK>
 static void dir_lean_launch(cf_cg *ws, cudaStream_t s, const double *zs, const double *po, double *pn, double zc)
 {
-    switch (ws->lean_rows * 10 + ws->pair_pf) {
-    case 41: dir_lean_go<ORDER, PK, 1, 4>(ws, s, zs, po, pn, zc); break;
-    case 42: dir_lean_go<ORDER, PK, 2, 4>(ws, s, zs, po, pn, zc); break;
-    case 80: dir_lean_go<ORDER, PK, 0, 8>(ws, s, zs, po, pn, zc); break;
-    case 160: dir_lean_go<ORDER, PK, 0, 16>(ws, s, zs, po, pn, zc); break;
-    default: dir_lean_go<ORDER, PK, 0, 4>(ws, s, zs, po, pn, zc); break;
-    }
+    // the geometry (lg_dir) is built for lean_rows; PF variants exist for 4 / 8 rows
+    const int pf = ws->lean_rows == 16 ? 0 : ws->pair_pf;
+    if (ws->lean_rows == 16) dir_lean_go<ORDER, PK, 0, 16>(ws, s, zs, po, pn, zc);
+    else if (ws->lean_rows == 8 && pf == 1) dir_lean_go<ORDER, PK, 1, 8>(ws, s, zs, po, pn, zc);
+    else if (ws->lean_rows == 8 && pf == 2) dir_lean_go<ORDER, PK, 2, 8>(ws, s, zs, po, pn, zc);
+    else if (ws->lean_rows == 8) dir_lean_go<ORDER, PK, 0, 8>(ws, s, zs, po, pn, zc);
+    else if (pf == 1) dir_lean_go<ORDER, PK, 1, 4>(ws, s, zs, po, pn, zc);
+    else if (pf == 2) dir_lean_go<ORDER, PK, 2, 4>(ws, s, zs, po, pn, zc);
+    else dir_lean_go<ORDER, PK, 0, 4>(ws, s, zs, po, pn, zc);
 }
 
 template <int ORDER, int PK, int XM, int ROWS>
@@ -1017,7 +1019,7 @@ static void set_grids(cf_cg *ws)
     if (ws->kind_dir == KK_LEAN && ws->n + kLeanPad >= (1LL << 32)) ws->kind_dir = KK_PAIR;
     if (ws->kind_upd == KK_LEAN && ws->n + kLeanPad >= (1LL << 32)) ws->kind_upd = KK_PAIR;
     if (const char *e = getenv("CF_LEAN_ROWS")) ws->lean_rows = atoi(e) == 4 ? 4 : (atoi(e) == 16 ? 16 : 8);
-    ws->lg_dir = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, ws->pair_pf >= 2 ? 6 : 8);
+    ws->lg_dir = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);
     ws->lg_upd = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);
     // single-reduction CG (one kernel per iteration, cf_cg_pass.cuh): opt-in.
     // Measured at 256^3 it runs 215 us/iteration against 205 for the

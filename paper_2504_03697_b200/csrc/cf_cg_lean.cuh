@@ -19,6 +19,31 @@
 
 constexpr int kLeanPad = 64;  // >= 2 * 32 lanes: one zero pair per lane
 
+// 16-byte loads the compiler may not move (volatile asm).  The next plane's
+// loads are issued right AFTER this plane's values are consumed: issued before
+// the first use (as plain __ldg code placed them), they shared a scoreboard
+// with the values in use, and that first use waited for the new loads too
+// (ncu: 29 % of all stall samples on that one DMUL).
+__device__ __forceinline__ double2 ldg2_pinned(const double *p)
+{
+    double2 v;
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ldg1_pinned(const double *p)
+{
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ld2_pinned(const double *p)
+{
+    double2 v;
+    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
+
 template <int PK, bool FIRST>
 __device__ __forceinline__ double lean_form(double z, double q, double zc, double beta)
 {
@@ -57,12 +82,28 @@ struct LeanSrc {
         return r;
     }
     __device__ __forceinline__ double form1(const Raw1 &r) const { return lean_form<PK, FIRST>(r.z, r.q, zc, beta); }
+    // the same loads, pinned in place (volatile): software pipelining (PF 2)
+    __device__ __forceinline__ Raw raw_pinned(unsigned k) const
+    {
+        Raw r;
+        r.z = ldg2_pinned(zs + k);
+        if (!FIRST) r.q = ldg2_pinned(po + k);
+        return r;
+    }
+    __device__ __forceinline__ Raw1 one_pinned(unsigned k) const
+    {
+        Raw1 r;
+        r.z = ldg1_pinned(zs + k);
+        r.q = FIRST ? 0.0 : ldg1_pinned(po + k);
+        return r;
+    }
 };
 
 // One block's top-down march (the update kernel marches bottom-up, so this
 // one starts on the planes it wrote last, still in L2).  Returns the thread's
 // partial p.Ap.  PF (software pipelining): 1 = the next plane's far operand
-// is loaded one iteration early, 2 = every load of the next plane is.
+// is loaded one iteration early, 2 = every load of the next plane is, issued
+// (volatile) only after this plane's loaded values are consumed.
 template <int ORDER, int PK, bool FIRST, int PF, int ROWS>
 __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, double off, double diag,
                                                  const double *__restrict__ zs, const double *__restrict__ po,
@@ -88,9 +129,15 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
     const LeanSrc<PK, FIRST> src{zs, po, zc, beta};
     // the in-plane loads of plane index k (c = its centre index)
     auto in_plane = [&](unsigned k, Raw &ym, Raw &yp, Raw1 &e) {
-        ym = src.raw(hym ? k - nx : zero);
-        yp = src.raw(hyp ? k + nx : zero);
-        if (eload) e = src.one(he ? k + de : zero);
+        if (PF >= 2) {
+            ym = src.raw_pinned(hym ? k - nx : zero);
+            yp = src.raw_pinned(hyp ? k + nx : zero);
+            if (eload) e = src.one_pinned(he ? k + de : zero);
+        } else {
+            ym = src.raw(hym ? k - nx : zero);
+            yp = src.raw(hyp ? k + nx : zero);
+            if (eload) e = src.one(he ? k + de : zero);
+        }
     };
 
     unsigned c = (unsigned)i + nx * (unsigned)j + pl * (unsigned)(z1 - 1);
@@ -98,13 +145,18 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
     double2 cc = src.form(src.raw(valid ? c : zero));
     Raw rnx, nym, nyp;
     Raw1 ne{0.0, 0.0};
-    if (PF >= 1) rnx = src.raw(valid && z1 - 1 >= 1 ? c - pl : zero);
-    if (PF >= 2) in_plane(c, nym, nyp, ne);
+    if (PF == 1) rnx = src.raw(valid && z1 - 1 >= 1 ? c - pl : zero);
+    if (PF >= 2) {
+        rnx = src.raw_pinned(valid && z1 - 1 >= 1 ? c - pl : zero);
+        in_plane(c, nym, nyp, ne);
+    }
     double pap = 0.0;
     for (int z = z1 - 1; z >= z0; --z, c -= pl) {
         Raw rm, rym, ryp;
         Raw1 re{0.0, 0.0};
-        if (PF >= 1) {
+        if (PF >= 2) {
+            rm = rnx;
+        } else if (PF == 1) {
             rm = rnx;
             rnx = src.raw(valid && z >= 2 && z > z0 ? c - 2 * pl : zero);  // plane z-2, if the next iteration runs
         } else {
@@ -114,13 +166,16 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
             rym = nym;
             ryp = nyp;
             re = ne;
-            if (z > z0) in_plane(c - pl, nym, nyp, ne);
         } else {
             in_plane(c, rym, ryp, re);
         }
         const double2 cm = src.form(rm);
         const double2 ym = src.form(rym), yp = src.form(ryp);
         const double e = eload ? src.form1(re) : 0.0;
+        if (PF >= 2 && z > z0) {  // every load of the next plane, now that this one is consumed
+            rnx = src.raw_pinned(valid && z >= 2 ? c - 2 * pl : zero);
+            in_plane(c - pl, nym, nyp, ne);
+        }
         double xl = __shfl_up_sync(0xffffffffu, cc.y, 1);
         double xr = __shfl_down_sync(0xffffffffu, cc.x, 1);
         xl = lane == 0 ? e : xl;
@@ -139,7 +194,7 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
 }
 
 template <int ORDER, int PK, int PF, int ROWS = kPairRows>
-__global__ void __launch_bounds__(32 * ROWS, (PF >= 2 ? 6 : 8) * kPairRows / ROWS) cg_dir_lean(PairGeom g, double off, double diag,
+__global__ void __launch_bounds__(32 * ROWS, 8 * kPairRows / ROWS) cg_dir_lean(PairGeom g, double off, double diag,
                                                             const double *__restrict__ zs,
                                                             const double *__restrict__ p_old,
                                                             double *__restrict__ p_new, double zc, CgScalars *sc,

@@ -33,24 +33,6 @@ template <int R> struct Lp {
 // r' box (2), Q = z' on the r' box (3): 47 KB at R = 8 (four CTAs per SM),
 // 82 KB at R = 16 (two)
 
-// 16-byte loads the compiler may not move (volatile asm).  The next plane's
-// loads are issued right AFTER this plane's values are consumed: issued before
-// the first use (as plain __ldg code placed them), they shared a scoreboard
-// with the values in use, and that first use waited for the new loads too
-// (ncu: 29 % of all stall samples on that one DMUL).
-__device__ __forceinline__ double2 ldg2_pinned(const double *p)
-{
-    double2 v;
-    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ double2 ld2_pinned(const double *p)
-{
-    double2 v;
-    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    return v;
-}
-
 template <int ORDER, int PK, bool FIRST, int R>
 __device__ __forceinline__ void lpass_body(const PairGeom &g, double off, double diag, double zc,
                                            const double *__restrict__ r_in, double *__restrict__ r_out,
