@@ -571,6 +571,8 @@ struct cf_cg {
     int pair_pf = 0;
     // lean kernels (cf_cg_lean.cuh): warps (tile rows) per CTA, CF_LEAN_ROWS
     int lean_rows = 8;
+    // programmatic dependent launch between the loop kernels (CF_PDL)
+    bool pdl = false;
     cf::PairGeom lg_dir{}, lg_upd{};
     cf::PairGeom pg_dir{}, pg_upd{};
     cf::TmaGeom geom_dir{}, geom_upd{};
@@ -598,11 +600,30 @@ struct cf_cg {
 
 namespace cf {
 
+// Launch with the PDL attribute when the workspace enables it (the kernels call
+// griddep_enter() first, so they are correct either way).
+template <typename... K, typename... A>
+static void launch_k(const cf_cg *ws, void (*kern)(K...), int grid, int block, size_t smem, cudaStream_t s,
+                     A &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = ws->pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
+
 template <int ORDER, int PK, int PF, int ROWS>
 static void dir_lean_go(cf_cg *ws, cudaStream_t s, const double *zs, const double *po, double *pn, double zc)
 {
-    cg_dir_lean<ORDER, PK, PF, ROWS><<<ws->lg_dir.ctas(), 32 * ROWS, 0, s>>>(ws->lg_dir, ws->off, ws->diag, zs, po, pn,
-                                                                          zc, ws->sc, ws->partials, ws->tk);
+    launch_k(ws, cg_dir_lean<ORDER, PK, PF, ROWS>, ws->lg_dir.ctas(), 32 * ROWS, 0, s, ws->lg_dir, ws->off, ws->diag,
+             zs, po, pn, zc, ws->sc, ws->partials, ws->tk);
 }
 
 template <int ORDER, int PK>
@@ -623,8 +644,8 @@ template <int ORDER, int PK, int XM, int ROWS>
 static void upd_lean_go(cf_cg *ws, cudaStream_t s, const double *p, const double *q, double zc, int use_cond,
                         cudaGraphConditionalHandle cond)
 {
-    cg_update_lean<ORDER, PK, XM, ROWS><<<ws->lg_upd.ctas(), 32 * ROWS, 0, s>>>(
-        ws->lg_upd, ws->off, ws->diag, p, q, ws->r, ws->x, zc, ws->sc, ws->partials, ws->tk, use_cond, cond);
+    launch_k(ws, cg_update_lean<ORDER, PK, XM, ROWS>, ws->lg_upd.ctas(), 32 * ROWS, 0, s, ws->lg_upd, ws->off,
+             ws->diag, p, q, ws->r, ws->x, zc, ws->sc, ws->partials, ws->tk, use_cond, cond);
 }
 
 template <int ORDER, int PK, int XM>
@@ -676,17 +697,17 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
             const TmaGeom &gu = ws->geom_upd;
             const int nb = gu.ntx * gu.nty * gu.nchunk;
             if (!ws->defer_x)
-                cg_update_tma<ORDER, PK, XM_EACH><<<nb, kWSThreads, kUpdSmem, s>>>(
-                    ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc,
-                    ws->sc, ws->partials, ws->tk, use_cond, cond, nullptr);
+                launch_k(ws, cg_update_tma<ORDER, PK, XM_EACH>, nb, kWSThreads, kUpdSmem, s, ws->m_p[half ^ 1], ws->m_ri,
+                         ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc, ws->partials,
+                         ws->tk, use_cond, cond, (double *)nullptr);
             else if (half == 0)
-                cg_update_tma<ORDER, PK, XM_SKIP><<<nb, kWSThreads, kUpdSmem, s>>>(
-                    ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc,
-                    ws->sc, ws->partials, ws->tk, use_cond, cond, nullptr);
+                launch_k(ws, cg_update_tma<ORDER, PK, XM_SKIP>, nb, kWSThreads, kUpdSmem, s, ws->m_p[half ^ 1], ws->m_ri,
+                         ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc, ws->partials,
+                         ws->tk, use_cond, cond, (double *)nullptr);
             else
-                cg_update_tma<ORDER, PK, XM_DOUBLE><<<nb, kWSThreads, kUpdSmem, s>>>(
-                    ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc,
-                    ws->sc, ws->partials, ws->tk, use_cond, cond, nullptr);
+                launch_k(ws, cg_update_tma<ORDER, PK, XM_DOUBLE>, nb, kWSThreads, kUpdSmem, s, ws->m_p[half ^ 1], ws->m_ri,
+                         ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc, ws->partials,
+                         ws->tk, use_cond, cond, (double *)nullptr);
             CF_CHECK_LAUNCH("cg_update_tma");
         } else if (ku == KK_LEAN) {
             if (!ws->defer_x) upd_lean_launch<ORDER, PK, XM_EACH>(ws, s, p_new, p_old, zc, use_cond, cond);
@@ -1018,6 +1039,7 @@ static void set_grids(cf_cg *ws)
     // 32-bit cell indices in the lean kernel
     if (ws->kind_dir == KK_LEAN && ws->n + kLeanPad >= (1LL << 32)) ws->kind_dir = KK_PAIR;
     if (ws->kind_upd == KK_LEAN && ws->n + kLeanPad >= (1LL << 32)) ws->kind_upd = KK_PAIR;
+    if (const char *e = getenv("CF_PDL")) ws->pdl = atoi(e) != 0;
     if (const char *e = getenv("CF_LEAN_ROWS")) ws->lean_rows = atoi(e) == 4 ? 4 : (atoi(e) == 16 ? 16 : 8);
     ws->lg_dir = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);
     ws->lg_upd = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);

@@ -202,10 +202,12 @@ __global__ void __launch_bounds__(32 * ROWS, 8 * kPairRows / ROWS) cg_dir_lean(P
 {
     __shared__ double red[32];
     __shared__ int is_last;
+    griddep_enter();
     if (sc->done) return;
     double pap = sc->it == 0
                      ? dir_lean_march<ORDER, PK, true, PF, ROWS>(g, blockIdx.x, off, diag, zs, p_old, p_new, zc, 0.0)
                      : dir_lean_march<ORDER, PK, false, PF, ROWS>(g, blockIdx.x, off, diag, zs, p_old, p_new, zc, sc->beta);
+    griddep_trigger();  // this CTA's sweep is done: the next kernel may start launching
     pap = block_sum<32 * ROWS>(pap, red);
     if (threadIdx.x == 0) partials[blockIdx.x] = pap;
     if (last_block(&tk->dir, &is_last)) {
@@ -297,12 +299,14 @@ __global__ void __launch_bounds__(32 * ROWS, 8 * kPairRows / ROWS) cg_update_lea
 {
     __shared__ double red[32];
     __shared__ int is_last;
+    griddep_enter();
     if (sc->done) {
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
         return;
     }
     double rr = 0.0, rz = 0.0;
     upd_lean_march<ORDER, PK, XM, ROWS>(g, blockIdx.x, off, diag, p, p_prev, r, x, zc, sc->alpha, sc->alpha_prev, rr, rz);
+    griddep_trigger();
     rr = block_sum<32 * ROWS>(rr, red);
     rz = PK != PK_ZVEC ? block_sum<32 * ROWS>(rz, red) : 0.0;
     if (threadIdx.x == 0) {

@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kWSThreads) cg_update_tma(
 {
     __shared__ double red[32];
     __shared__ int is_last;
+    griddep_enter();
     if (sc->done) {
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
         return;
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(kWSThreads) cg_update_tma(
     double rr, rz;
     update_tma_body<ORDER, PK, XM>(&mp, &mr, &mx, &mq, g, blockIdx.x, off, diag, r, x, zc, sc->alpha, sc->alpha_prev,
                                    nullptr, nullptr, red, rr, rz);
+    griddep_trigger();
     if (threadIdx.x == 0) {
         partials[2 * blockIdx.x] = rr;
         partials[2 * blockIdx.x + 1] = rz;
