@@ -330,7 +330,14 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
         cfg = dataclasses.replace(cfg, shape=(n, n, nz))
     norm = nz / n  # cells / n^3
     dec = SlabDecomposition(n, n, nz, world, rank)
-    sim = SlabSim(cfg, [dec.z0, dec.z1], distributed=True, collective=args.collective)
+    from paper_2504_03697_b200.distributed import PeerLinkError
+
+    try:
+        sim = SlabSim(cfg, [dec.z0, dec.z1], distributed=True, collective=args.collective)
+    except PeerLinkError as err:  # all ranks raise alike: the NCCL form on every rank
+        print(f"[bench] {err}; using the NCCL collective form", file=sys.stderr)
+        args.collective = "nccl"
+        sim = SlabSim(cfg, [dec.z0, dec.z1], distributed=True, collective="nccl")
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         sim.step()

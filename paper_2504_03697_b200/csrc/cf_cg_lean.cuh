@@ -109,6 +109,10 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
                                                  const double *__restrict__ zs, const double *__restrict__ po,
                                                  double *__restrict__ pn, double zc, double beta)
 {
+    // z-slab halos (multi-GPU, cf_p2p.cu): planes -1 / nz exist in memory when
+    // lo_halo / hi_halo; indices count from the lowest plane present, and the
+    // zero pad follows the highest
+    const int lo = g.lo_halo ? 1 : 0, hi = g.hi_halo ? 1 : 0;
     using Raw = typename LeanSrc<PK, FIRST>::Raw;
     using Raw1 = typename LeanSrc<PK, FIRST>::Raw1;
     const int lane = threadIdx.x & 31;
@@ -120,7 +124,10 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
     const int z0 = (int)((long long)g.nz * chunk / g.nchunk);
     const int z1 = (int)((long long)g.nz * (chunk + 1) / g.nchunk);
     const unsigned nx = (unsigned)g.nx, pl = nx * (unsigned)g.ny;
-    const unsigned zero = pl * (unsigned)g.nz + 2u * (unsigned)lane;  // this lane's zero pair
+    const unsigned zero = pl * (unsigned)(g.nz + lo + hi) + 2u * (unsigned)lane;  // this lane's zero pair
+    zs -= (size_t)lo * pl;
+    po -= (size_t)lo * pl;
+    pn -= (size_t)lo * pl;
     const bool valid = i < g.nx;
     const bool hym = valid && j > 0, hyp = valid && j + 1 < g.ny;
     const bool eload = lane == 0 || lane == 31;  // lanes that need the tile-edge cell
@@ -140,14 +147,18 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
         }
     };
 
-    unsigned c = (unsigned)i + nx * (unsigned)j + pl * (unsigned)(z1 - 1);
-    double2 cp = src.form(src.raw(valid && z1 < g.nz ? c + pl : zero));
+    unsigned c = (unsigned)i + nx * (unsigned)j + pl * (unsigned)(z1 - 1 + lo);
+    const bool hzp1 = valid && z1 < g.nz + hi;
+    double2 cp = src.form(src.raw(hzp1 ? c + pl : zero));
     double2 cc = src.form(src.raw(valid ? c : zero));
+    // the slab's top halo plane of p, recomputed from the exchanged r halo
+    // (bit-identical to the neighbour's own p) for the update kernel's stencil
+    if (hi && hzp1 && z1 == g.nz) *reinterpret_cast<double2 *>(pn + c + pl) = cp;
     Raw rnx, nym, nyp;
     Raw1 ne{0.0, 0.0};
-    if (PF == 1) rnx = src.raw(valid && z1 - 1 >= 1 ? c - pl : zero);
+    if (PF == 1) rnx = src.raw(valid && z1 - 1 + lo >= 1 ? c - pl : zero);
     if (PF >= 2) {
-        rnx = src.raw_pinned(valid && z1 - 1 >= 1 ? c - pl : zero);
+        rnx = src.raw_pinned(valid && z1 - 1 + lo >= 1 ? c - pl : zero);
         in_plane(c, nym, nyp, ne);
     }
     double pap = 0.0;
@@ -158,9 +169,9 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
             rm = rnx;
         } else if (PF == 1) {
             rm = rnx;
-            rnx = src.raw(valid && z >= 2 && z > z0 ? c - 2 * pl : zero);  // plane z-2, if the next iteration runs
+            rnx = src.raw(valid && z + lo >= 2 && z > z0 ? c - 2 * pl : zero);  // plane z-2, if the next iteration runs
         } else {
-            rm = src.raw(valid && z >= 1 ? c - pl : zero);
+            rm = src.raw(valid && z + lo >= 1 ? c - pl : zero);
         }
         if (PF >= 2) {
             rym = nym;
@@ -173,7 +184,7 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
         const double2 ym = src.form(rym), yp = src.form(ryp);
         const double e = eload ? src.form1(re) : 0.0;
         if (PF >= 2 && z > z0) {  // every load of the next plane, now that this one is consumed
-            rnx = src.raw_pinned(valid && z >= 2 ? c - 2 * pl : zero);
+            rnx = src.raw_pinned(valid && z + lo >= 2 ? c - 2 * pl : zero);
             in_plane(c - pl, nym, nyp, ne);
         }
         double xl = __shfl_up_sync(0xffffffffu, cc.y, 1);
@@ -186,6 +197,7 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
             *reinterpret_cast<double2 *>(pn + c) = cc;
             pap = pap + cc.x * a0;
             pap = pap + cc.y * a1;
+            if (lo && z == 0) *reinterpret_cast<double2 *>(pn + c - pl) = cm;  // bottom halo plane of p
         }
         cp = cc;
         cc = cm;

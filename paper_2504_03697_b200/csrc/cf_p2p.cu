@@ -49,6 +49,7 @@ namespace cf {
 
 #include "cf_cg_tma.cuh"
 #include "cf_cg_pair.cuh"
+#include "cf_cg_lean.cuh"
 
 constexpr int kMaxRanks = 8;
 
@@ -249,13 +250,20 @@ __global__ void __launch_bounds__(kPairThreads, 8) p2p_dir(const P2PSet *__restr
     CgScalars *sc = sl.sc;
     if (sc->done) return;
     double pap;
+    // the lean march (cf_cg_lean.cuh) at the pair geometry's 4-row tiles: the
+    // same values and block partials as dir_pair_body, ~half the instructions
     if constexpr (SINGLE) {
-        pap = dir_pair_body<ORDER, PK>(g1, bid, off, diag, r1, nullptr, half ? p1_1 : p0_1, half ? p0_1 : p1_1, zc,
-                                       sc->beta, sc->it == 0);
+        const double *po = half ? p1_1 : p0_1;
+        double *pn = half ? p0_1 : p1_1;
+        pap = sc->it == 0 ? dir_lean_march<ORDER, PK, true, 0, kPairRows>(g1, bid, off, diag, r1, po, pn, zc, 0.0)
+                          : dir_lean_march<ORDER, PK, false, 0, kPairRows>(g1, bid, off, diag, r1, po, pn, zc, sc->beta);
     } else {
         const PairGeom g = sl.gd;
-        pap = dir_pair_body<ORDER, PK>(g, bid, off, diag, sl.r, nullptr, half ? sl.p1 : sl.p0, half ? sl.p0 : sl.p1,
-                                       zc, sc->beta, sc->it == 0);
+        const double *po = half ? sl.p1 : sl.p0;
+        double *pn = half ? sl.p0 : sl.p1;
+        pap = sc->it == 0 ? dir_lean_march<ORDER, PK, true, 0, kPairRows>(g, bid, off, diag, sl.r, po, pn, zc, 0.0)
+                          : dir_lean_march<ORDER, PK, false, 0, kPairRows>(g, bid, off, diag, sl.r, po, pn, zc,
+                                                                            sc->beta);
     }
     pap = block_sum<kPairThreads>(pap, red);
     if (threadIdx.x == 0) sl.partials[bid] = pap;
@@ -691,8 +699,11 @@ int cf_pcg_create(cf_pcg **out, int nx, int ny, int nz, double h, int order, int
         sb.hi = grank < nranks - 1 ? 1 : 0;
         const size_t planes = (size_t)sb.nzl + sb.lo + sb.hi;
         for (int a = 0; a < 4 && e == cudaSuccess; ++a) {
-            e = cudaMalloc(&sb.alloc[a], planes * pl * sizeof(double));
-            if (e == cudaSuccess) e = cudaMemsetAsync(sb.alloc[a], 0, planes * pl * sizeof(double), s);
+            // + kLeanPad zeroed doubles: the lean direction march reads out-of-domain
+            // neighbours there (cf_cg_lean.cuh)
+            const size_t bytes = (planes * pl + cf::kLeanPad) * sizeof(double);
+            e = cudaMalloc(&sb.alloc[a], bytes);
+            if (e == cudaSuccess) e = cudaMemsetAsync(sb.alloc[a], 0, bytes, s);
         }
         cf::P2PSlab &d = ws->set.s[k];
         d.gd = cf::pair_geom(nx, ny, sb.nzl, sb.lo, sb.hi, "CF_PAIR_CHUNKS_DIR");

@@ -91,6 +91,11 @@ class SlabCG:
             pass
 
 
+class PeerLinkError(RuntimeError):
+    """The ranks could not link their CG vectors through CUDA IPC (raised on
+    every rank alike, so a caller can fall back to the NCCL form together)."""
+
+
 class PeerSlabCG:
     """CG over z-slabs with the collectives fused into the kernels over peer
     memory (cf_pcg_*, csrc/cf_p2p.cu): one slab per rank (GPU) linked through
@@ -131,7 +136,15 @@ class PeerSlabCG:
             blobs = [None] * nranks
             dist.all_gather_object(blobs, blob.raw)
             allb = ctypes.create_string_buffer(b"".join(blobs), size * nranks)
-            _lib.check(lib.cf_pcg_import(self._h, allb, nranks), "cf_pcg_import")
+            rc = lib.cf_pcg_import(self._h, allb, nranks)
+            why = _lib.last_error() if rc != 0 else ""
+            # every rank must agree: a rank that linked would otherwise wait on
+            # mailboxes a failed rank never writes
+            dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else "cpu"
+            ok = torch.tensor([1 if rc == 0 else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0:
+                raise PeerLinkError(f"peer-memory CG linking failed on at least one rank ({why or 'another rank'})")
             dist.barrier()
 
     def solve(self, b_slabs, tol: float = 1e-6, max_iter: int = 1000, precond: str | None = "jacobi"):
