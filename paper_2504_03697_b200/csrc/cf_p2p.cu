@@ -162,6 +162,10 @@ constexpr int ST_PEER_TIMEOUT = 4;
 __device__ __forceinline__ void p2p_allreduce(const P2PSet &ps, const P2PSlab &sl, int ncomp, const double *v,
                                               double *out)
 {
+    if (ps.nranks == 1) {  // one rank (single-slab run): nothing to exchange
+        for (int c = 0; c < ncomp; ++c) out[c] = 0.0 + v[c];
+        return;
+    }
     const unsigned long long ph = ++sl.sc->phase;
     const int par = (int)(ph & 1ull), me = sl.rank;
     for (int q = 0; q < ps.nranks; ++q)
