@@ -22,6 +22,7 @@ struct DicWave {
     int slack = 1;                             // extra steps kept between neighbouring tiles
     int pub = 8;                               // steps per published progress value
     int shape = 0;                             // tile shape (cf_dic_wave.cu kShapes)
+    int depth = 0;                             // cp.async pipeline depth of the 16x8 sweeps (0: one-step prefetch)
     int *prog_f = nullptr, *prog_b = nullptr;  // per-tile progress of the two sweeps
     bool ok = false;
 };

@@ -27,6 +27,7 @@
 
 #include "cf_common.cuh"
 #include "cf_dic.cuh"
+#include "cf_tma.cuh"
 
 namespace cf {
 
@@ -250,6 +251,199 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd(DicWave dw, const dou
     }
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined form (D-deep): every load a step needs -- this thread's r (or w)
+// and d, and the neighbouring tiles' edge values -- is copied into a shared
+// ring by cp.async D-1 steps ahead, so a diagonal step no longer waits for a
+// memory round trip (the one-step-ahead prefetch above left each step at the
+// ~1.3 us load latency; the DAG depth is only ~1.1x the 3n-2 diagonals).
+// Edges fetched D-1 steps ahead need the neighbour D-1 steps further on: the
+// slack is D-1.  Same arithmetic in the same order: bit-identical results.
+__device__ __forceinline__ void cp_async8_ca(double *dst, const double *src, int src_bytes)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async16_cg(void *dst, const double *src, int src_bytes)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_grp() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_grp() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// wait (thread 0) until a neighbour's published progress covers `need`
+__device__ __forceinline__ bool wave_wait(const int *nb, int need, int &seen, int &peek)
+{
+    if (!nb || seen >= need) return false;
+    seen = max(seen, peek);
+    while (seen < need) seen = ld_relaxed_gpu(nb);
+    peek = ld_relaxed_gpu(nb);
+    return true;
+}
+
+template <int kWTX, int kWTY, int D>
+__global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd_p(DicWave dw, const double *__restrict__ d,
+                                                            const double *__restrict__ r, double *__restrict__ w,
+                                                            const int *done)
+{
+    constexpr int NT = kWTX * kWTY;
+    __shared__ double sm[2][kWTY][kWTX];
+    __shared__ __align__(16) double ring_r[D][NT], ring_d[D][NT];
+    __shared__ __align__(16) double2 ring_x[D][kWTY], ring_y[D][kWTX];  // left / lower edge pairs
+    if (done && *done) return;
+    const int ntx = dw.ntx;
+    const int t = blockIdx.x, a = t % ntx, b = t / ntx;
+    const int tid = threadIdx.x, ti = tid % kWTX, tj = tid / kWTX;
+    const int i = a * kWTX + ti, j = b * kWTY + tj;
+    const bool col_ok = i < dw.nx && j < dw.ny;
+    const long long pl = (long long)dw.nx * dw.ny;
+    const long long base = (long long)i + (long long)dw.nx * j;
+    if (tid == 0) dw.prog_b[t] = 0;  // re-arm the backward sweep's counters
+    const int *left = a > 0 ? dw.prog_f + (t - 1) : nullptr;
+    const int *below = b > 0 ? dw.prog_f + (t - ntx) : nullptr;
+    int seen_l = 0, seen_b = 0, peek_l = 0, peek_b = 0;
+    const int nsteps = dw.nz + kWTX + kWTY - 2;
+    auto issue = [&](int s2) {  // this thread's copies for step s2
+        const int k = s2 - ti - tj, q = s2 % D;
+        const bool in = col_ok && k >= 0 && k < dw.nz;
+        const long long o = base + pl * (in ? k : 0);
+        cp_async8_ca(&ring_r[q][tid], r + o, in ? 8 : 0);
+        cp_async8_ca(&ring_d[q][tid], d + o, in ? 8 : 0);
+        if (ti == 0 && i > 0) cp_async16_cg(&ring_x[q][tj], w + ((o - 1) & ~1ll), in ? 16 : 0);
+        if (tj == 0 && j > 0) cp_async16_cg(&ring_y[q][ti], w + ((o - dw.nx) & ~1ll), in ? 16 : 0);
+        cp_async_commit_grp();
+    };
+    double wk = 0.0;  // w at (i, j, k-1)
+    for (int s = -(D - 1); s < nsteps; ++s) {
+        const int s2 = s + D - 1;  // the step whose copies are issued now
+        if (tid == 0 && s2 < nsteps) {
+            const bool f1 = wave_wait(left, min(s2 + kWTX, nsteps), seen_l, peek_l);
+            const bool f2 = wave_wait(below, min(s2 + kWTY, nsteps), seen_b, peek_b);
+            if (f1 || f2) fence_acq_rel_gpu();  // an accepted counter value acts as an acquire
+        }
+        tile_sync<NT>();
+        if (s2 < nsteps) issue(s2);
+        else cp_async_commit_grp();  // keep one group per step
+        if (s < 0) continue;
+        cp_async_wait_grp<D - 1>();  // step s's copies (this thread's) have landed
+        const int k = s - ti - tj, q = s % D;
+        double wv = 0.0;
+        if (col_ok && k >= 0 && k < dw.nz) {
+            const long long o = base + pl * k;
+            double acc = ring_r[q][tid];
+            if (k > 0) acc = acc - dw.lval * wk;  // column i - pl
+            if (j > 0) {
+                double yl = 0.0;
+                if (tj == 0) {
+                    const double2 e = ring_y[q][ti];
+                    yl = ((o - dw.nx) & 1) ? e.y : e.x;
+                }
+                acc = acc - dw.lval * (tj > 0 ? sm[s & 1][tj - 1][ti] : yl);  // i - nx
+            }
+            if (i > 0) {
+                double xl = 0.0;
+                if (ti == 0) {
+                    const double2 e = ring_x[q][tj];
+                    xl = ((o - 1) & 1) ? e.y : e.x;
+                }
+                acc = acc - dw.lval * (ti > 0 ? sm[s & 1][tj][ti - 1] : xl);  // i - 1
+            }
+            wv = acc / ring_d[q][tid];
+            w[o] = wv;
+            wk = wv;
+        }
+        sm[(s + 1) & 1][tj][ti] = wv;
+        if ((s + 1) % dw.pub == 0 || s + 1 == nsteps) {
+            tile_sync<NT>();
+            if (tid == 0) st_release_gpu(dw.prog_f + t, s + 1);
+        }
+    }
+    cp_async_wait_grp<0>();
+}
+
+template <int kWTX, int kWTY, int D>
+__global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd_p(DicWave dw, const double *__restrict__ d,
+                                                            const double *__restrict__ w, double *__restrict__ z,
+                                                            const int *done)
+{
+    constexpr int NT = kWTX * kWTY;
+    __shared__ double sm[2][kWTY][kWTX];
+    __shared__ __align__(16) double ring_w[D][NT], ring_d[D][NT];
+    __shared__ __align__(16) double2 ring_x[D][kWTY], ring_y[D][kWTX];  // right / upper edge pairs
+    if (done && *done) return;
+    const int ntx = dw.ntx, nty = dw.nty;
+    const int t = ntx * nty - 1 - blockIdx.x, a = t % ntx, b = t / ntx;
+    const int tid = threadIdx.x, ti = tid % kWTX, tj = tid / kWTX;
+    const int i = a * kWTX + ti, j = b * kWTY + tj;
+    const bool col_ok = i < dw.nx && j < dw.ny;
+    const long long pl = (long long)dw.nx * dw.ny;
+    const long long base = (long long)i + (long long)dw.nx * j;
+    if (tid == 0) dw.prog_f[t] = 0;  // re-arm the next forward sweep's counters
+    const int *right = a < ntx - 1 ? dw.prog_b + (t + 1) : nullptr;
+    const int *above = b < nty - 1 ? dw.prog_b + (t + ntx) : nullptr;
+    int seen_r = 0, seen_a = 0, peek_r = 0, peek_a = 0;
+    const int nsteps = dw.nz + kWTX + kWTY - 2;
+    const int ri = kWTX - 1 - ti, rj = kWTY - 1 - tj;
+    auto issue = [&](int s2) {
+        const int k = dw.nz - 1 - (s2 - ri - rj), q = s2 % D;
+        const bool in = col_ok && k >= 0 && k < dw.nz;
+        const long long o = base + pl * (in ? k : 0);
+        cp_async8_ca(&ring_w[q][tid], w + o, in ? 8 : 0);  // written by the forward launch
+        cp_async8_ca(&ring_d[q][tid], d + o, in ? 8 : 0);
+        if (ti == kWTX - 1 && i < dw.nx - 1) cp_async16_cg(&ring_x[q][tj], z + ((o + 1) & ~1ll), in ? 16 : 0);
+        if (tj == kWTY - 1 && j < dw.ny - 1) cp_async16_cg(&ring_y[q][ti], z + ((o + dw.nx) & ~1ll), in ? 16 : 0);
+        cp_async_commit_grp();
+    };
+    double zk = 0.0;  // z at (i, j, k+1)
+    for (int s = -(D - 1); s < nsteps; ++s) {
+        const int s2 = s + D - 1;
+        if (tid == 0 && s2 < nsteps) {
+            const bool f1 = wave_wait(right, min(s2 + kWTX, nsteps), seen_r, peek_r);
+            const bool f2 = wave_wait(above, min(s2 + kWTY, nsteps), seen_a, peek_a);
+            if (f1 || f2) fence_acq_rel_gpu();
+        }
+        tile_sync<NT>();
+        if (s2 < nsteps) issue(s2);
+        else cp_async_commit_grp();
+        if (s < 0) continue;
+        cp_async_wait_grp<D - 1>();
+        const int k = dw.nz - 1 - (s - ri - rj), q = s % D;
+        double zv = 0.0;
+        if (col_ok && k >= 0 && k < dw.nz) {
+            const long long o = base + pl * k;
+            double acc = 0.0;
+            if (i < dw.nx - 1) {
+                double xr = 0.0;
+                if (ti == kWTX - 1) {
+                    const double2 e = ring_x[q][tj];
+                    xr = ((o + 1) & 1) ? e.y : e.x;
+                }
+                acc = acc + dw.uval * (ti < kWTX - 1 ? sm[s & 1][tj][ti + 1] : xr);
+            }
+            if (j < dw.ny - 1) {
+                double yu = 0.0;
+                if (tj == kWTY - 1) {
+                    const double2 e = ring_y[q][ti];
+                    yu = ((o + dw.nx) & 1) ? e.y : e.x;
+                }
+                acc = acc + dw.uval * (tj < kWTY - 1 ? sm[s & 1][tj + 1][ti] : yu);
+            }
+            if (k < dw.nz - 1) acc = acc + dw.uval * zk;
+            zv = ring_w[q][tid] - acc / ring_d[q][tid];
+            z[o] = zv;
+            zk = zv;
+        }
+        sm[(s + 1) & 1][tj][ti] = zv;
+        if ((s + 1) % dw.pub == 0 || s + 1 == nsteps) {
+            tile_sync<NT>();
+            if (tid == 0) st_release_gpu(dw.prog_b + t, s + 1);
+        }
+    }
+    cp_async_wait_grp<0>();
+}
+
 // Verify that the triangles are exactly the 7-point pattern of the grid with
 // one value each; any mismatch clears *ok.
 __global__ void dic_wave_check(const int32_t *lp, const int32_t *lc, const double *lv, const int32_t *up,
@@ -346,6 +540,12 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
     if (const char *e = std::getenv("CF_DIC_SLACK")) dw.slack = std::max(1, std::atoi(e));  // >= 1: edges are prefetched a step ahead
     dw.pub = 8;
     if (const char *e = std::getenv("CF_DIC_PUBLISH")) dw.pub = std::max(1, std::atoi(e));
+    // pipelined sweeps, depth 2 (measured at 256^3: one-step prefetch 2.63 ms per
+    // DIC-PCG iteration, depth 2 2.43, 3 2.61, 4 2.74 -- the tiles mostly wait at
+    // the barrier for their neighbours' progress, and deeper rings widen the
+    // slack between tiles)
+    dw.depth = dw.shape == 0 ? 2 : 0;
+    if (const char *e = std::getenv("CF_DIC_DEPTH")) dw.depth = std::max(0, std::atoi(e));
     dw.ok = true;
     return CF_OK;
 }
@@ -354,6 +554,23 @@ int dic_wave_apply(const DicData &dd, const double *r, double *w, double *z, con
 {
     const DicWave &dw = dd.wave;
     const int ntiles = dw.ntx * dw.nty;
+    if (dw.shape == 0 && dw.depth >= 2) {
+        if (dw.depth == 2) {
+            dic_wave_fwd_p<16, 8, 2><<<ntiles, 128, 0, s>>>(dw, dd.d, r, w, done);
+            dic_wave_bwd_p<16, 8, 2><<<ntiles, 128, 0, s>>>(dw, dd.d, w, z, done);
+        } else if (dw.depth == 3) {
+            dic_wave_fwd_p<16, 8, 3><<<ntiles, 128, 0, s>>>(dw, dd.d, r, w, done);
+            dic_wave_bwd_p<16, 8, 3><<<ntiles, 128, 0, s>>>(dw, dd.d, w, z, done);
+        } else if (dw.depth == 4) {
+            dic_wave_fwd_p<16, 8, 4><<<ntiles, 128, 0, s>>>(dw, dd.d, r, w, done);
+            dic_wave_bwd_p<16, 8, 4><<<ntiles, 128, 0, s>>>(dw, dd.d, w, z, done);
+        } else {
+            dic_wave_fwd_p<16, 8, 6><<<ntiles, 128, 0, s>>>(dw, dd.d, r, w, done);
+            dic_wave_bwd_p<16, 8, 6><<<ntiles, 128, 0, s>>>(dw, dd.d, w, z, done);
+        }
+        CF_CHECK_LAUNCH("dic wavefront sweeps (pipelined)");
+        return CF_OK;
+    }
     switch (dw.shape) {
     case 0:
         dic_wave_fwd<16, 8><<<ntiles, 128, 0, s>>>(dw, dd.d, r, w, done);
