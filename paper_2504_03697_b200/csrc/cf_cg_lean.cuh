@@ -104,7 +104,7 @@ struct LeanSrc {
 // partial p.Ap.  PF (software pipelining): 1 = the next plane's far operand
 // is loaded one iteration early, 2 = every load of the next plane is, issued
 // (volatile) only after this plane's loaded values are consumed.
-template <int ORDER, int PK, bool FIRST, int PF, int ROWS>
+template <int ORDER, int PK, bool FIRST, int PF, int ROWS, bool HALO = false>
 __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, double off, double diag,
                                                  const double *__restrict__ zs, const double *__restrict__ po,
                                                  double *__restrict__ pn, double zc, double beta)
@@ -112,7 +112,10 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
     // z-slab halos (multi-GPU, cf_p2p.cu): planes -1 / nz exist in memory when
     // lo_halo / hi_halo; indices count from the lowest plane present, and the
     // zero pad follows the highest
-    const int lo = g.lo_halo ? 1 : 0, hi = g.hi_halo ? 1 : 0;
+    // HALO: the caller passes zs / po / pn at the LOWEST plane in memory (plane
+    // -1 when lo_halo).  (Shifting them in here made the compiler rebuild every
+    // address in 64-bit arithmetic; HALO = false is the single-domain kernel.)
+    const int lo = HALO && g.lo_halo ? 1 : 0, hi = HALO && g.hi_halo ? 1 : 0;
     using Raw = typename LeanSrc<PK, FIRST>::Raw;
     using Raw1 = typename LeanSrc<PK, FIRST>::Raw1;
     const int lane = threadIdx.x & 31;
@@ -125,9 +128,6 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
     const int z1 = (int)((long long)g.nz * (chunk + 1) / g.nchunk);
     const unsigned nx = (unsigned)g.nx, pl = nx * (unsigned)g.ny;
     const unsigned zero = pl * (unsigned)(g.nz + lo + hi) + 2u * (unsigned)lane;  // this lane's zero pair
-    zs -= (size_t)lo * pl;
-    po -= (size_t)lo * pl;
-    pn -= (size_t)lo * pl;
     const bool valid = i < g.nx;
     const bool hym = valid && j > 0, hyp = valid && j + 1 < g.ny;
     const bool eload = lane == 0 || lane == 31;  // lanes that need the tile-edge cell

@@ -255,19 +255,23 @@ __global__ void __launch_bounds__(kPairThreads, 8) p2p_dir(const P2PSet *__restr
     if (sc->done) return;
     double pap;
     // the lean march (cf_cg_lean.cuh) at the pair geometry's 4-row tiles: the
-    // same values and block partials as dir_pair_body, ~half the instructions
+    // same values and block partials as dir_pair_body, ~half the instructions.
+    // SINGLE: r1 / p0_1 / p1_1 point at the slab's lowest plane in memory.
     if constexpr (SINGLE) {
         const double *po = half ? p1_1 : p0_1;
         double *pn = half ? p0_1 : p1_1;
-        pap = sc->it == 0 ? dir_lean_march<ORDER, PK, true, 0, kPairRows>(g1, bid, off, diag, r1, po, pn, zc, 0.0)
-                          : dir_lean_march<ORDER, PK, false, 0, kPairRows>(g1, bid, off, diag, r1, po, pn, zc, sc->beta);
+        pap = sc->it == 0 ? dir_lean_march<ORDER, PK, true, 0, kPairRows, true>(g1, bid, off, diag, r1, po, pn, zc, 0.0)
+                          : dir_lean_march<ORDER, PK, false, 0, kPairRows, true>(g1, bid, off, diag, r1, po, pn, zc,
+                                                                                  sc->beta);
     } else {
         const PairGeom g = sl.gd;
-        const double *po = half ? sl.p1 : sl.p0;
-        double *pn = half ? sl.p0 : sl.p1;
-        pap = sc->it == 0 ? dir_lean_march<ORDER, PK, true, 0, kPairRows>(g, bid, off, diag, sl.r, po, pn, zc, 0.0)
-                          : dir_lean_march<ORDER, PK, false, 0, kPairRows>(g, bid, off, diag, sl.r, po, pn, zc,
-                                                                            sc->beta);
+        const size_t sh = g.lo_halo ? (size_t)g.nx * g.ny : 0;
+        const double *po = (half ? sl.p1 : sl.p0) - sh;
+        double *pn = (half ? sl.p0 : sl.p1) - sh;
+        pap = sc->it == 0
+                  ? dir_lean_march<ORDER, PK, true, 0, kPairRows, true>(g, bid, off, diag, sl.r - sh, po, pn, zc, 0.0)
+                  : dir_lean_march<ORDER, PK, false, 0, kPairRows, true>(g, bid, off, diag, sl.r - sh, po, pn, zc,
+                                                                          sc->beta);
     }
     pap = block_sum<kPairThreads>(pap, red);
     if (threadIdx.x == 0) sl.partials[bid] = pap;
@@ -523,8 +527,9 @@ static int p2p_body_t(cf_pcg *ws, cudaStream_t s, double zc, cudaGraphConditiona
 {
     const P2PSlab &d = ws->set.s[0];
     for (int half = 0; half < 2; ++half) {
+        const size_t sh = d.gd.lo_halo ? (size_t)d.gd.nx * d.gd.ny : 0;  // lowest plane in memory
         p2p_dir<ORDER, PK, SINGLE><<<ws->grid_dir, kPairThreads, 0, s>>>(ws->d_set, half, ws->off, ws->diag, zc, d.gd,
-                                                                        d.r, d.p0, d.p1);
+                                                                        d.r - sh, d.p0 - sh, d.p1 - sh);
         CF_CHECK_LAUNCH("p2p_dir");
         if (ws->tma) {
             if (half == 0)
