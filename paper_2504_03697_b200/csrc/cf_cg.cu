@@ -571,6 +571,8 @@ struct cf_cg {
     int pair_pf = 0;
     // lean kernels (cf_cg_lean.cuh): warps (tile rows) per CTA, CF_LEAN_ROWS
     int lean_rows = 8;
+    // TMA ring depth of the skip-x update kernel (3 = the shared layout; CF_SKIP_STAGES=4/6)
+    int skip_stages = 4;  // measured 3 / 4 / 6: 192.6 / 191.7 / 192.3 us (256^3), 1403 / 1389 / 1396 (512^3)
     // programmatic dependent launch between the loop kernels (CF_PDL)
     bool pdl = false;
     cf::PairGeom lg_dir{}, lg_upd{};
@@ -700,6 +702,14 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
                 launch_k(ws, cg_update_tma<ORDER, PK, XM_EACH>, nb, kWSThreads, kUpdSmem, s, ws->m_p[half ^ 1], ws->m_ri,
                          ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc, ws->partials,
                          ws->tk, use_cond, cond, (double *)nullptr);
+            else if (half == 0 && ws->skip_stages == 4)
+                launch_k(ws, cg_update_tma<ORDER, PK, XM_SKIP, 4>, nb, kWSThreads, upd_skip_smem<4>(), s,
+                         ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x,
+                         zc, ws->sc, ws->partials, ws->tk, use_cond, cond, (double *)nullptr);
+            else if (half == 0 && ws->skip_stages == 6)
+                launch_k(ws, cg_update_tma<ORDER, PK, XM_SKIP, 6>, nb, kWSThreads, upd_skip_smem<6>(), s,
+                         ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x,
+                         zc, ws->sc, ws->partials, ws->tk, use_cond, cond, (double *)nullptr);
             else if (half == 0)
                 launch_k(ws, cg_update_tma<ORDER, PK, XM_SKIP>, nb, kWSThreads, kUpdSmem, s, ws->m_p[half ^ 1], ws->m_ri,
                          ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc, ws->partials,
@@ -1023,6 +1033,12 @@ static void set_grids(cf_cg *ws)
         set_upd_smem<ORDER, XM_EACH>();
         set_upd_smem<ORDER, XM_SKIP>();
         set_upd_smem<ORDER, XM_DOUBLE>();
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_NONE, XM_SKIP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_skip_smem<4>());
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_JCONST, XM_SKIP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_skip_smem<4>());
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_ZVEC, XM_SKIP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_skip_smem<4>());
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_NONE, XM_SKIP, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_skip_smem<6>());
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_JCONST, XM_SKIP, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_skip_smem<6>());
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_ZVEC, XM_SKIP, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_skip_smem<6>());
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bd, cg_dir_tma<ORDER, PK_JCONST>, kWSThreads, kDirSmem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, cg_update_tma<ORDER, PK_JCONST>, kWSThreads, kUpdSmem);
         ws->geom_dir = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bd > 0 ? bd : 1);
@@ -1040,6 +1056,7 @@ static void set_grids(cf_cg *ws)
     if (ws->kind_dir == KK_LEAN && ws->n + kLeanPad >= (1LL << 32)) ws->kind_dir = KK_PAIR;
     if (ws->kind_upd == KK_LEAN && ws->n + kLeanPad >= (1LL << 32)) ws->kind_upd = KK_PAIR;
     if (const char *e = getenv("CF_PDL")) ws->pdl = atoi(e) != 0;
+    if (const char *e = getenv("CF_SKIP_STAGES")) ws->skip_stages = atoi(e) == 3 ? 3 : (atoi(e) == 6 ? 6 : 4);
     if (const char *e = getenv("CF_LEAN_ROWS")) ws->lean_rows = atoi(e) == 4 ? 4 : (atoi(e) == 16 ? 16 : 8);
     ws->lg_dir = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);
     ws->lg_upd = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);

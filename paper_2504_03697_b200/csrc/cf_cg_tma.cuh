@@ -150,7 +150,7 @@ __host__ __device__ constexpr int upd_interiors() { return XM == XM_SKIP ? 1 : (
 // streams the p halo box and the interior boxes through the mbarrier ring,
 // consumers run the stencil + epilogue.  Returns the block sums (rr, rz) on
 // thread 0.  Maps may live in the parameter block or in global memory.
-template <int ORDER, int PK, int XM>
+template <int ORDER, int PK, int XM, int S = kStages>
 __device__ __forceinline__ void update_tma_body(const CUtensorMap *mp, const CUtensorMap *mr, const CUtensorMap *mx,
                                              const CUtensorMap *mq, const TmaGeom g, int bid, double off, double diag,
                                              double *__restrict__ r, double *__restrict__ x, double zc, double alpha,
@@ -158,22 +158,22 @@ __device__ __forceinline__ void update_tma_body(const CUtensorMap *mp, const CUt
                                              double *red, double &rr_out, double &rz_out)
 {
     extern __shared__ unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    __shared__ __align__(8) uint64_t full[S], empty[S];
     double *const sp = aligned_smem(smem_raw);
-    double *const sr = sp + kStages * kBoxStride;
-    double *const sx = sr + kStages * kInt;
-    double *const sq = sx + kStages * kInt;
+    double *const sr = sp + S * kBoxStride;
+    double *const sx = sr + S * kInt;
+    double *const sq = sx + S * kInt;
     const MarchCoords m = march_coords(g, bid);
     UpdPolicy<PK, XM> pol{sp,  sr,   sx,   sq,   alpha,   -alpha, zc, alpha_prev, r, x, g.nx, (long long)g.nx * g.ny,
                           lo_r, hi_r, g.nz - 1};
-    init_ws_bars(full, empty);
+    init_ws_bars<S>(full, empty);
     if (threadIdx.x >= kPThreads) {  // producer warp
         if (threadIdx.x == kPThreads) {
             prefetch_map(mp);
             prefetch_map(mr);
             if (XM != XM_SKIP) prefetch_map(mx);
             if (XM == XM_DOUBLE) prefetch_map(mq);
-            ws_produce(m.nplanes, full, empty, [&](int q, int s, uint64_t *bar) {
+            auto issue = [&](int q, int s, uint64_t *bar) {
                 const int z = m.zs + q;
                 const bool own = z >= m.z0 && z < m.z1;  // r, x, p_prev only for owned planes
                 mbar_expect_tx(bar, kBoxBytes + (own ? upd_interiors<XM>() * kIntBytes : 0));
@@ -183,16 +183,17 @@ __device__ __forceinline__ void update_tma_body(const CUtensorMap *mp, const CUt
                     if (XM != XM_SKIP) tma_load_3d(sx + s * kInt, mx, m.x0, m.y0, z + g.lo_halo, bar);
                     if (XM == XM_DOUBLE) tma_load_3d(sq + s * kInt, mq, m.x0, m.y0, z + g.lo_halo, bar);
                 }
-            });
+            };
+            ws_produce<decltype(issue), S>(m.nplanes, full, empty, issue);
         }
     } else {
-        ws_consume<ORDER>(g, m, off, diag, pol, full, empty);
+        ws_consume<ORDER, UpdPolicy<PK, XM>, S>(g, m, off, diag, pol, full, empty);
     }
     rr_out = block_sum<kWSThreads>(pol.rr, red);
     rz_out = PK != PK_ZVEC ? block_sum<kWSThreads>(pol.rz, red) : 0.0;
 }
 
-template <int ORDER, int PK, int XM = XM_EACH>
+template <int ORDER, int PK, int XM = XM_EACH, int S = kStages>
 __global__ void __launch_bounds__(kWSThreads) cg_update_tma(
     const __grid_constant__ CUtensorMap mp, const __grid_constant__ CUtensorMap mr,
     const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mq, TmaGeom g, double off,
@@ -207,8 +208,8 @@ __global__ void __launch_bounds__(kWSThreads) cg_update_tma(
         return;
     }
     double rr, rz;
-    update_tma_body<ORDER, PK, XM>(&mp, &mr, &mx, &mq, g, blockIdx.x, off, diag, r, x, zc, sc->alpha, sc->alpha_prev,
-                                   nullptr, nullptr, red, rr, rz);
+    update_tma_body<ORDER, PK, XM, S>(&mp, &mr, &mx, &mq, g, blockIdx.x, off, diag, r, x, zc, sc->alpha,
+                                      sc->alpha_prev, nullptr, nullptr, red, rr, rz);
     griddep_trigger();
     if (threadIdx.x == 0) {
         partials[2 * blockIdx.x] = rr;
@@ -230,3 +231,6 @@ __global__ void __launch_bounds__(kWSThreads) cg_update_tma(
 
 constexpr size_t kDirSmem = 2 * kStages * kBoxStride * sizeof(double) + 128;
 constexpr size_t kUpdSmem = kStages * (kBoxStride + 3 * kInt) * sizeof(double) + 128;
+// the skip-x update stages only the p halo box and the r box: deeper rings fit
+template <int S>
+constexpr size_t upd_skip_smem() { return (size_t)S * (kBoxStride + kInt) * sizeof(double) + 128; }

@@ -167,10 +167,11 @@ __device__ __forceinline__ void staged_pair_march(const TmaGeom &g, double off, 
 constexpr int kConsumerWarps = kPThreads / 32;
 constexpr int kWSThreads = kPThreads + 32;
 
+template <int S = kStages>
 __device__ __forceinline__ void init_ws_bars(uint64_t *full, uint64_t *empty)
 {
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kConsumerWarps);
         }
@@ -180,55 +181,56 @@ __device__ __forceinline__ void init_ws_bars(uint64_t *full, uint64_t *empty)
 }
 
 // Producer loop (run by one elected lane of warp 8).
-template <class Issue>
+template <class Issue, int S = kStages>
 __device__ __forceinline__ void ws_produce(int nplanes, uint64_t *full, uint64_t *empty, Issue issue)
 {
     for (int q = 0; q < nplanes; ++q) {
-        const int s = q % kStages;
-        if (q >= kStages) mbar_wait(&empty[s], (uint32_t)(((q / kStages) - 1) & 1));
+        const int s = q % S;
+        if (q >= S) mbar_wait(&empty[s], (uint32_t)(((q / S) - 1) & 1));
         issue(q, s, &full[s]);
     }
 }
 
 // Consumer: this warp is done with slot q.
+template <int S = kStages>
 __device__ __forceinline__ void ws_release(uint64_t *empty, int q)
 {
     fence_proxy_async_smem();
     __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[q % kStages]);
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[q % S]);
 }
 
 // Consumer march over the block's planes.  Pol: value(slot, offset) ->
 // operand at a box offset (may compute it), box geometry as in
 // staged_pair_march; epi(slot, m, z, centre pair, a0, a1).
-template <int ORDER, class Pol>
+template <int ORDER, class Pol, int S = kStages>
 __device__ __forceinline__ void ws_consume(const TmaGeom &g, const MarchCoords &m, double off, double diag, Pol &pol,
                                            uint64_t *full, uint64_t *empty)
 {
     const bool hxl = m.i > 0, hxr = m.i + 2 < g.nx, hym = m.j > 0, hyp = m.j < g.ny - 1;
     const bool inplane_fast = hxl && hxr && hym && hyp;
-    auto wait = [&](int q) { mbar_wait(&full[q % kStages], (uint32_t)((q / kStages) & 1)); };
+    auto wait = [&](int q) { mbar_wait(&full[q % S], (uint32_t)((q / S) & 1)); };
     int q = 0;
     double2 cprev = make_double2(0.0, 0.0);
     wait(0);
     if (m.zs < m.z0) {
         cprev = pol.value2(0, m.o);
         pol.halo(m, m.zs, cprev);
-        ws_release(empty, 0);
+        ws_release<S>(empty, 0);
         q = 1;
         wait(1);
     }
-    double2 ccur = pol.value2(q % kStages, m.o);
+    double2 ccur = pol.value2(q % S, m.o);
     const double2 zero = make_double2(0.0, 0.0);
     for (int z = m.z0; z < m.z1; ++z, ++q) {
         const bool hzm = z - 1 >= m.zlo, hzp = z + 1 <= m.zhi;
         double2 cnext = zero;
         if (hzp) {
             wait(q + 1);
-            cnext = pol.value2((q + 1) % kStages, m.o);
+            cnext = pol.value2((q + 1) % S, m.o);
             if (z + 1 == m.z1) pol.halo(m, z + 1, cnext);
         }
-        const int s = q % kStages;
+        const int s = q % S;
         if (m.valid) {
             double a0, a1;
             if (inplane_fast && hzm && hzp) {
@@ -244,12 +246,12 @@ __device__ __forceinline__ void ws_consume(const TmaGeom &g, const MarchCoords &
             }
             pol.epi(s, m, z, ccur, a0, a1);
         }
-        ws_release(empty, q);
+        ws_release<S>(empty, q);
         cprev = ccur;
         ccur = cnext;
     }
     // the last staged plane (z1, read as cnext) is released too
-    if (q < m.nplanes) ws_release(empty, q);
+    if (q < m.nplanes) ws_release<S>(empty, q);
 }
 
 }  // namespace cf
