@@ -191,3 +191,31 @@ def test_peer_slabs_oracle_box_and_edges(cuda):
     assert rel(xq, x1) <= 1e-9
     with pytest.raises(ValueError):
         PeerSlabCG(33, 8, 8, 1.0)  # odd nx
+
+
+@pytest.mark.parametrize("collective", ["p2p", "nccl"])
+def test_weak_scaling_box_slabs(cuda, collective):
+    """The bench's weak-scaling geometry scaled down: the cavity extruded to
+    n x n x (n*G) with one n^3 slab per "GPU" (G = 3, emulated in one
+    process) against the single-domain box run."""
+    from paper_2504_03697_b200.distributed import SlabSim
+    from paper_2504_03697_b200.parallel import SlabDecomposition
+
+    n, g = 32, 3
+    cfg = cuda.SimConfig(n=n, h=1.0 / n, dt=0.01, t_end=0.02, tol=1e-12, max_iter=20000, variant="optimized",
+                         preconditioner="jacobi", shape=(n, n, n * g))
+    ref = cuda.initial_state(cfg)
+    cache = cuda.PoissonCache()
+    bounds = SlabDecomposition.bounds(n * g, g).tolist()
+    assert bounds == [0, n, 2 * n, 3 * n]
+    sim = SlabSim(cfg, bounds, collective=collective)
+    for _ in range(cfg.num_steps):
+        a = cuda.step(ref, cfg, cache)
+        b = sim.step()
+        assert abs(a.solve.iterations - b.solve.iterations) <= 2
+        assert b.div_pre == pytest.approx(a.div_pre, rel=1e-12)
+    su, sv, sw, sp = sim.gather()
+    ru, rv, rw = ref.vel.numpy()
+    assert rel(np.concatenate([su.ravel(), sv.ravel(), sw.ravel()]),
+               np.concatenate([ru.ravel(), rv.ravel(), rw.ravel()])) <= 1e-10
+    assert rel(sp, ref.p.numpy()) <= 1e-9
