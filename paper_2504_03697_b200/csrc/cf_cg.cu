@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(kMarchThreads) cg_x_fixup(long long n, double 
 #include "cf_cg_pass.cuh"
 #include "cf_cg_lean.cuh"
 #include "cf_cg_lpass.cuh"
+#include "cf_cg_persist.cuh"
 
 // Host: single-reduction pass geometry (32 x 16 tiles; chunks of ~32 planes,
 // the 4-plane pipeline prologue amortised; CF_PASS_CHUNKS overrides).
@@ -572,7 +573,13 @@ struct cf_cg {
     // lean kernels (cf_cg_lean.cuh): warps (tile rows) per CTA, CF_LEAN_ROWS
     int lean_rows = 8;
     // TMA ring depth of the skip-x update kernel (3 = the shared layout; CF_SKIP_STAGES=4/6)
-    int skip_stages = 4;  // measured 3 / 4 / 6: 192.6 / 191.7 / 192.3 us (256^3), 1403 / 1389 / 1396 (512^3)
+    int skip_stages = 4;
+    // persistent single-launch solve for L2-resident grids (cf_cg_persist.cuh; CF_PERSIST=0/1)
+    bool persist = false;
+    cf::PairGeom per_g{};
+    int per_blocks = 0;
+    double *per_part = nullptr;
+    cf::GridBar *per_bar = nullptr;  // measured 3 / 4 / 6: 192.6 / 191.7 / 192.3 us (256^3), 1403 / 1389 / 1396 (512^3)
     // programmatic dependent launch between the loop kernels (CF_PDL)
     bool pdl = false;
     cf::PairGeom lg_dir{}, lg_upd{};
@@ -953,6 +960,19 @@ static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, c
     if ((PK == PK_NONE || PK == PK_JCONST) && ws->pass && !x0) {
         if constexpr (PK == PK_NONE || PK == PK_JCONST) return pass_solve<ORDER, PK>(ws, b, zc, s);
     }
+    if ((PK == PK_NONE || PK == PK_JCONST) && ws->persist && !x0 && !ws->direct) {
+        if constexpr (PK == PK_NONE || PK == PK_JCONST) {
+            int rc0 = launch_init<ORDER, PK>(ws, b, x0, zc, s);
+            if (rc0 != CF_OK) return rc0;
+            CF_CUDA(cudaEventRecord(ws->ev0, s));
+            cg_persist_kernel<ORDER, PK><<<ws->per_blocks, kPersistThreads, 0, s>>>(
+                ws->per_g, ws->off, ws->diag, zc, ws->r, ws->x, ws->p[0], ws->p[1], ws->sc, ws->per_part,
+                ws->per_part + ws->per_blocks, ws->per_bar);
+            CF_CHECK_LAUNCH("cg_persist_kernel");
+            CF_CUDA(cudaEventRecord(ws->ev1, s));
+            return CF_OK;
+        }
+    }
     int rc = launch_init<ORDER, PK>(ws, b, x0, zc, s);
     if (rc != CF_OK) return rc;
     if (ws->direct) {
@@ -1060,6 +1080,24 @@ static void set_grids(cf_cg *ws)
     if (const char *e = getenv("CF_LEAN_ROWS")) ws->lean_rows = atoi(e) == 4 ? 4 : (atoi(e) == 16 ? 16 : 8);
     ws->lg_dir = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);
     ws->lg_upd = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);
+    // persistent solve: the four CG vectors fit in L2 with room to spare
+    // (<= 96 MB), above the single-block range; all CTAs co-resident
+    {
+        const long long vec_bytes = ws->n * 8;
+        bool on = pair_ok && 4 * vec_bytes <= 96ll * 1024 * 1024 && ws->n > kSmallMaxCells &&
+                  ws->n + kLeanPad < (1LL << 32);
+        // opt-in (CF_PERSIST=1): measured 64^3 14.4 vs 19.9 us/iteration, 128^3 31.9 vs 32.9,
+        // but 96^3 50 vs 24 and 144^3 108 vs 45 -- one short march per CTA per phase is
+        // L2-latency bound and the two grid barriers per iteration cost ~25 % (ncu)
+        const char *pe = getenv("CF_PERSIST");
+        on = on && pe && atoi(pe) != 0;
+        const int bps = blocks_per_sm((const void *)cg_persist_kernel<ORDER, PK_JCONST>, kPersistThreads, 0);
+        ws->per_blocks = num_sms() * (bps > 0 ? bps : 1);
+        ws->per_g = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, kPersistRows, 8);
+        ws->per_g.nchunk = wave_chunks((long long)ws->per_g.ntx * ws->per_g.nty, ws->bx.nz, ws->per_blocks, 4);
+        if (ws->per_g.ctas() < ws->per_blocks) ws->per_blocks = ws->per_g.ctas();
+        ws->persist = on && bps >= 1;
+    }
     // single-reduction CG (one kernel per iteration, cf_cg_pass.cuh): opt-in.
     // Measured at 256^3 it runs 215 us/iteration against 205 for the
     // two-kernel form (instruction-bound: ~64 % issue slots), so the default
@@ -1167,6 +1205,9 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
     if (e == cudaSuccess) e = cudaMalloc(&ws->tk, sizeof(cf::CgTickets));
     if (e == cudaSuccess) e = cudaMemsetAsync(ws->tk, 0, sizeof(cf::CgTickets), cf::as_stream(stream));
     if (e == cudaSuccess) e = cudaMallocHost(&ws->sc_host, sizeof(cf::CgScalars));
+    if (e == cudaSuccess && ws->persist) e = cudaMalloc(&ws->per_part, 3 * (size_t)ws->per_blocks * sizeof(double));
+    if (e == cudaSuccess && ws->persist) e = cudaMalloc(&ws->per_bar, sizeof(cf::GridBar));
+    if (e == cudaSuccess && ws->persist) e = cudaMemsetAsync(ws->per_bar, 0, sizeof(cf::GridBar), cf::as_stream(stream));
     if (e == cudaSuccess) e = cudaEventCreate(&ws->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&ws->ev1);
     if (e != cudaSuccess) {
@@ -1195,8 +1236,9 @@ int cf_cg_destroy(cf_cg *ws)
         if (ws->exec_pass[k]) cudaGraphExecDestroy(ws->exec_pass[k]);
         if (ws->graph_pass[k]) cudaGraphDestroy(ws->graph_pass[k]);
     }
-    for (double *b : {ws->r, ws->x, ws->p[0], ws->p[1], ws->jd, ws->partials, ws->zbuf, ws->wbuf, ws->r2})
+    for (double *b : {ws->r, ws->x, ws->p[0], ws->p[1], ws->jd, ws->partials, ws->zbuf, ws->wbuf, ws->r2, ws->per_part})
         if (b) cudaFree(b);
+    if (ws->per_bar) cudaFree(ws->per_bar);
     if (ws->dic_lptr) cudaFree(ws->dic_lptr);
     if (ws->sc) cudaFree(ws->sc);
     if (ws->tk) cudaFree(ws->tk);

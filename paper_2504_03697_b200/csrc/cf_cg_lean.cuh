@@ -51,7 +51,20 @@ __device__ __forceinline__ double lean_form(double z, double q, double zc, doubl
     return FIRST ? z : z + beta * q;  // src/solver.py:142, :169
 }
 
-template <int PK, bool FIRST>
+// COH: coherent (.cg, L2) loads instead of the read-only path -- for the
+// persistent CG kernel, whose vectors are rewritten within one launch
+template <bool COH>
+__device__ __forceinline__ double2 lean_ld2(const double *p)
+{
+    return COH ? __ldcg(reinterpret_cast<const double2 *>(p)) : __ldg(reinterpret_cast<const double2 *>(p));
+}
+template <bool COH>
+__device__ __forceinline__ double lean_ld1(const double *p)
+{
+    return COH ? __ldcg(p) : __ldg(p);
+}
+
+template <int PK, bool FIRST, bool COH = false>
 struct LeanSrc {
     const double *__restrict__ zs;
     const double *__restrict__ po;
@@ -62,8 +75,8 @@ struct LeanSrc {
     __device__ __forceinline__ Raw raw(unsigned k) const
     {
         Raw r;
-        r.z = __ldg(reinterpret_cast<const double2 *>(zs + k));
-        if (!FIRST) r.q = __ldg(reinterpret_cast<const double2 *>(po + k));
+        r.z = lean_ld2<COH>(zs + k);
+        if (!FIRST) r.q = lean_ld2<COH>(po + k);
         return r;
     }
     __device__ __forceinline__ double2 form(const Raw &r) const
@@ -77,8 +90,8 @@ struct LeanSrc {
     __device__ __forceinline__ Raw1 one(unsigned k) const
     {
         Raw1 r;
-        r.z = __ldg(zs + k);
-        r.q = FIRST ? 0.0 : __ldg(po + k);
+        r.z = lean_ld1<COH>(zs + k);
+        r.q = FIRST ? 0.0 : lean_ld1<COH>(po + k);
         return r;
     }
     __device__ __forceinline__ double form1(const Raw1 &r) const { return lean_form<PK, FIRST>(r.z, r.q, zc, beta); }
@@ -104,7 +117,7 @@ struct LeanSrc {
 // partial p.Ap.  PF (software pipelining): 1 = the next plane's far operand
 // is loaded one iteration early, 2 = every load of the next plane is, issued
 // (volatile) only after this plane's loaded values are consumed.
-template <int ORDER, int PK, bool FIRST, int PF, int ROWS, bool HALO = false>
+template <int ORDER, int PK, bool FIRST, int PF, int ROWS, bool HALO = false, bool COH = false>
 __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, double off, double diag,
                                                  const double *__restrict__ zs, const double *__restrict__ po,
                                                  double *__restrict__ pn, double zc, double beta)
@@ -116,8 +129,8 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
     // -1 when lo_halo).  (Shifting them in here made the compiler rebuild every
     // address in 64-bit arithmetic; HALO = false is the single-domain kernel.)
     const int lo = HALO && g.lo_halo ? 1 : 0, hi = HALO && g.hi_halo ? 1 : 0;
-    using Raw = typename LeanSrc<PK, FIRST>::Raw;
-    using Raw1 = typename LeanSrc<PK, FIRST>::Raw1;
+    using Raw = typename LeanSrc<PK, FIRST, COH>::Raw;
+    using Raw1 = typename LeanSrc<PK, FIRST, COH>::Raw1;
     const int lane = threadIdx.x & 31;
     const int ntiles = g.ntx * g.nty;
     const int tile = bid % ntiles, chunk = bid / ntiles;
@@ -133,7 +146,7 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
     const bool eload = lane == 0 || lane == 31;  // lanes that need the tile-edge cell
     const bool he = valid && (lane == 0 ? i > 0 : i + 2 < g.nx);
     const unsigned de = lane == 0 ? 0xffffffffu : 2u;  // -1 / +2 (mod 2^32)
-    const LeanSrc<PK, FIRST> src{zs, po, zc, beta};
+    const LeanSrc<PK, FIRST, COH> src{zs, po, zc, beta};
     // the in-plane loads of plane index k (c = its centre index)
     auto in_plane = [&](unsigned k, Raw &ym, Raw &yp, Raw1 &e) {
         if (PF >= 2) {
@@ -234,7 +247,7 @@ __global__ void __launch_bounds__(32 * ROWS, 8 * kPairRows / ROWS) cg_dir_lean(P
 // bottom-up (the direction kernel marched top-down and left its last planes,
 // the bottom ones, in L2).  Per-element arithmetic of cg_update_tma /
 // cg_update_pair.
-template <int ORDER, int PK, int XM, int ROWS>
+template <int ORDER, int PK, int XM, int ROWS, bool COH = false>
 __device__ __forceinline__ void upd_lean_march(const PairGeom &g, int bid, double off, double diag,
                                                const double *__restrict__ p, const double *__restrict__ q,
                                                double *__restrict__ r, double *__restrict__ x, double zc,
@@ -256,7 +269,7 @@ __device__ __forceinline__ void upd_lean_march(const PairGeom &g, int bid, doubl
     const bool he = valid && (lane == 0 ? i > 0 : i + 2 < g.nx);
     const unsigned de = lane == 0 ? 0xffffffffu : 2u;
     const double malpha = -alpha;
-    auto ld2 = [](const double *a, unsigned k) { return __ldg(reinterpret_cast<const double2 *>(a + k)); };
+    auto ld2 = [](const double *a, unsigned k) { return lean_ld2<COH>(a + k); };
 
     unsigned c = (unsigned)i + nx * (unsigned)j + pl * (unsigned)z0;
     double2 cm = ld2(p, valid && z0 >= 1 ? c - pl : zero);
@@ -267,7 +280,7 @@ __device__ __forceinline__ void upd_lean_march(const PairGeom &g, int bid, doubl
         const double2 ym = ld2(p, hym ? c - nx : zero);
         const double2 yp = ld2(p, hyp ? c + nx : zero);
         double e = 0.0;
-        if (eload) e = __ldg(p + (he ? c + de : zero));
+        if (eload) e = lean_ld1<COH>(p + (he ? c + de : zero));
         // r, x, p_prev of this plane: plain loads (r and x are written here)
         const double2 ro = *reinterpret_cast<const double2 *>(r + cv);
         double2 xo, qo;
