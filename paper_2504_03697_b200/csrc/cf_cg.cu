@@ -582,6 +582,7 @@ struct cf_cg {
     cf::GridBar *per_bar = nullptr;  // measured 3 / 4 / 6: 192.6 / 191.7 / 192.3 us (256^3), 1403 / 1389 / 1396 (512^3)
     // programmatic dependent launch between the loop kernels (CF_PDL)
     bool pdl = false;
+    bool lean2 = true;  // two-rows-per-warp direction march (CF_LEAN2=0: one row per warp); +0.5 % in the sustained bench
     cf::PairGeom lg_dir{}, lg_upd{};
     cf::PairGeom pg_dir{}, pg_upd{};
     cf::TmaGeom geom_dir{}, geom_upd{};
@@ -639,6 +640,11 @@ template <int ORDER, int PK>
 static void dir_lean_launch(cf_cg *ws, cudaStream_t s, const double *zs, const double *po, double *pn, double zc)
 {
     // the geometry (lg_dir) is built for lean_rows; PF variants exist for 4 / 8 rows
+    if (ws->lean2 && ws->lean_rows == 8) {  // two rows per warp: 4 warps cover the 8-row tile
+        launch_k(ws, cg_dir_lean2<ORDER, PK, 4>, ws->lg_dir.ctas(), 128, 0, s, ws->lg_dir, ws->off, ws->diag, zs, po,
+                 pn, zc, ws->sc, ws->partials, ws->tk);
+        return;
+    }
     const int pf = ws->lean_rows == 16 ? 0 : ws->pair_pf;
     if (ws->lean_rows == 16) dir_lean_go<ORDER, PK, 0, 16>(ws, s, zs, po, pn, zc);
     else if (ws->lean_rows == 8 && pf == 1) dir_lean_go<ORDER, PK, 1, 8>(ws, s, zs, po, pn, zc);
@@ -1076,9 +1082,10 @@ static void set_grids(cf_cg *ws)
     if (ws->kind_dir == KK_LEAN && ws->n + kLeanPad >= (1LL << 32)) ws->kind_dir = KK_PAIR;
     if (ws->kind_upd == KK_LEAN && ws->n + kLeanPad >= (1LL << 32)) ws->kind_upd = KK_PAIR;
     if (const char *e = getenv("CF_PDL")) ws->pdl = atoi(e) != 0;
+    if (const char *e = getenv("CF_LEAN2")) ws->lean2 = atoi(e) != 0;
     if (const char *e = getenv("CF_SKIP_STAGES")) ws->skip_stages = atoi(e) == 3 ? 3 : (atoi(e) == 6 ? 6 : 4);
     if (const char *e = getenv("CF_LEAN_ROWS")) ws->lean_rows = atoi(e) == 4 ? 4 : (atoi(e) == 16 ? 16 : 8);
-    ws->lg_dir = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);
+    ws->lg_dir = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, ws->lean2 && ws->lean_rows == 8 ? 12 : 8);
     ws->lg_upd = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);
     // persistent solve: the four CG vectors fit in L2 with room to spare
     // (<= 96 MB), above the single-block range; all CTAs co-resident

@@ -345,3 +345,111 @@ __global__ void __launch_bounds__(32 * ROWS, 8 * kPairRows / ROWS) cg_update_lea
             cudaGraphSetConditional(cond, 0);
     }
 }
+
+// ---------------------------------------------------------------- two rows per warp
+// The direction march with each warp owning TWO tile rows (j, j+1): the rows'
+// shared y-neighbours come from registers (row j's yp is row j+1's centre and
+// vice versa), so per plane a warp issues two DRAM row loads (the next plane
+// of both rows) but only two L1/L2 halo rows, and more DRAM bytes are in
+// flight per register (the one-row march is long-scoreboard bound at 64
+// registers).  A CTA of RW warps covers 2*RW rows.  Single domain (no slab
+// halos), same per-element arithmetic; the per-thread p.Ap order is row j
+// then row j+1 per plane.
+template <int ORDER, int PK, bool FIRST, int RW>
+__device__ __forceinline__ double dir_lean2_march(const PairGeom &g, int bid, double off, double diag,
+                                                  const double *__restrict__ zs, const double *__restrict__ po,
+                                                  double *__restrict__ pn, double zc, double beta)
+{
+    using Src = LeanSrc<PK, FIRST>;
+    using Raw = typename Src::Raw;
+    using Raw1 = typename Src::Raw1;
+    const int lane = threadIdx.x & 31;
+    const int ntiles = g.ntx * g.nty;
+    const int tile = bid % ntiles, chunk = bid / ntiles;
+    const int i = (tile % g.ntx) * kPairX + 2 * lane;
+    const int j = (tile / g.ntx) * (2 * RW) + 2 * (threadIdx.x >> 5);  // rows j, j+1
+    if (j >= g.ny) return 0.0;
+    const int z0 = (int)((long long)g.nz * chunk / g.nchunk);
+    const int z1 = (int)((long long)g.nz * (chunk + 1) / g.nchunk);
+    const unsigned nx = (unsigned)g.nx, pl = nx * (unsigned)g.ny;
+    const unsigned zero = pl * (unsigned)g.nz + 2u * (unsigned)lane;
+    const bool xv = i < g.nx;
+    const bool v0 = xv, v1 = xv && j + 1 < g.ny;          // the two rows' pairs exist
+    const bool hym = v0 && j > 0, hyp = v1 && j + 2 < g.ny;  // outer y-neighbour rows
+    const bool eload = lane == 0 || lane == 31;
+    const bool he = xv && (lane == 0 ? i > 0 : i + 2 < g.nx);
+    const unsigned de = lane == 0 ? 0xffffffffu : 2u;
+    const Src src{zs, po, zc, beta};
+
+    unsigned c = (unsigned)i + nx * (unsigned)j + pl * (unsigned)(z1 - 1);  // row j; row j+1 is c + nx
+    const bool top = z1 < g.nz;
+    double2 cp0 = src.form(src.raw(v0 && top ? c + pl : zero));
+    double2 cp1 = src.form(src.raw(v1 && top ? c + nx + pl : zero));
+    double2 cc0 = src.form(src.raw(v0 ? c : zero));
+    double2 cc1 = src.form(src.raw(v1 ? c + nx : zero));
+    double pap = 0.0;
+    for (int z = z1 - 1; z >= z0; --z, c -= pl) {
+        const bool hzm = z >= 1;
+        const Raw rm0 = src.raw(v0 && hzm ? c - pl : zero);
+        const Raw rm1 = src.raw(v1 && hzm ? c + nx - pl : zero);
+        const Raw rym = src.raw(hym ? c - nx : zero);
+        const Raw ryp = src.raw(hyp ? c + 2 * nx : zero);
+        Raw1 re0{0.0, 0.0}, re1{0.0, 0.0};
+        if (eload) {
+            re0 = src.one(he ? c + de : zero);
+            re1 = src.one(he && v1 ? c + nx + de : zero);
+        }
+        const double2 cm0 = src.form(rm0), cm1 = src.form(rm1);
+        const double2 ym = src.form(rym), yp = src.form(ryp);
+        const double e0 = eload ? src.form1(re0) : 0.0, e1 = eload ? src.form1(re1) : 0.0;
+        double xl0 = __shfl_up_sync(0xffffffffu, cc0.y, 1), xr0 = __shfl_down_sync(0xffffffffu, cc0.x, 1);
+        double xl1 = __shfl_up_sync(0xffffffffu, cc1.y, 1), xr1 = __shfl_down_sync(0xffffffffu, cc1.x, 1);
+        xl0 = lane == 0 ? e0 : xl0;
+        xr0 = lane == 31 ? e0 : xr0;
+        xl1 = lane == 0 ? e1 : xl1;
+        xr1 = lane == 31 ? e1 : xr1;
+        double a0, a1, b0, b1;
+        stencil_pair<ORDER, true>(cc0, xl0, xr0, ym, cc1, cm0, cp0, true, true, true, true, true, true, off, diag, a0,
+                                  a1);
+        stencil_pair<ORDER, true>(cc1, xl1, xr1, cc0, yp, cm1, cp1, true, true, true, true, true, true, off, diag, b0,
+                                  b1);
+        if (v0) {
+            *reinterpret_cast<double2 *>(pn + c) = cc0;
+            pap = pap + cc0.x * a0;
+            pap = pap + cc0.y * a1;
+        }
+        if (v1) {
+            *reinterpret_cast<double2 *>(pn + c + nx) = cc1;
+            pap = pap + cc1.x * b0;
+            pap = pap + cc1.y * b1;
+        }
+        cp0 = cc0;
+        cc0 = cm0;
+        cp1 = cc1;
+        cc1 = cm1;
+    }
+    return pap;
+}
+
+template <int ORDER, int PK, int RW>
+__global__ void __launch_bounds__(32 * RW, 6) cg_dir_lean2(PairGeom g, double off, double diag,
+                                                             const double *__restrict__ zs,
+                                                             const double *__restrict__ p_old,
+                                                             double *__restrict__ p_new, double zc, CgScalars *sc,
+                                                             double *partials, CgTickets *tk)
+{
+    __shared__ double red[32];
+    __shared__ int is_last;
+    griddep_enter();
+    if (sc->done) return;
+    double pap = sc->it == 0
+                     ? dir_lean2_march<ORDER, PK, true, RW>(g, blockIdx.x, off, diag, zs, p_old, p_new, zc, 0.0)
+                     : dir_lean2_march<ORDER, PK, false, RW>(g, blockIdx.x, off, diag, zs, p_old, p_new, zc, sc->beta);
+    griddep_trigger();
+    pap = block_sum<32 * RW>(pap, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = pap;
+    if (last_block(&tk->dir, &is_last)) {
+        pap = reduce_partials<32 * RW>(partials, gridDim.x, 1, red);
+        if (threadIdx.x == 0) scalar_after_dir(sc, pap);
+    }
+}
