@@ -288,8 +288,13 @@ def run_ours(args, rank, world, local_rank):
         "fused_iter_frac": achieved / peak,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "fused CG iteration (cg_dir_lean + cg_update_tma; x updated every 2nd iteration)",
+                     "kernel": "fused CG iteration (cg_dir_lean2 + cg_update_tma; x updated every 2nd iteration)",
                      "algorithmic_bytes_per_iteration": alg_bytes, "design_bytes_per_iteration": 60 * cells,
+                     # the same iteration time against the bytes this design moves (60 N) and
+                     # against the DRAM traffic ncu measured per iteration (frac above uses the
+                     # reference op sequence's 88 N, hence > 1)
+                     "design_frac": 60 * cells / iter_s / 1e9 / peak,
+                     "dram_frac": (traffic / iter_s / 1e9 / peak) if traffic else None,
                      "peak_kind": peak_kind},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
