@@ -432,7 +432,7 @@ __device__ __forceinline__ double dir_lean2_march(const PairGeom &g, int bid, do
 }
 
 template <int ORDER, int PK, int RW>
-__global__ void __launch_bounds__(32 * RW, 6) cg_dir_lean2(PairGeom g, double off, double diag,
+__global__ void __launch_bounds__(32 * RW, 24 / RW) cg_dir_lean2(PairGeom g, double off, double diag,
                                                              const double *__restrict__ zs,
                                                              const double *__restrict__ p_old,
                                                              double *__restrict__ p_new, double zc, CgScalars *sc,
