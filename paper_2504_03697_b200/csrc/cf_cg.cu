@@ -687,7 +687,8 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
         // the TMA and lean forms have no per-cell Jacobi vector
         const int kd = (PK == PK_JVEC && (ws->kind_dir == KK_TMA || ws->kind_dir == KK_LEAN)) ? KK_PAIR : ws->kind_dir;
         int ku = (PK == PK_JVEC && (ws->kind_upd == KK_TMA || ws->kind_upd == KK_LEAN)) ? KK_PAIR : ws->kind_upd;
-        if (half == 0 && ws->defer_x && ws->kind_upd_skip >= 0) ku = ws->kind_upd_skip;  // tuning override
+        if (half == 0 && ws->defer_x && ws->kind_upd_skip >= 0)  // tuning override (no per-cell Jacobi in TMA / lean forms)
+            ku = (PK == PK_JVEC && ws->kind_upd_skip != KK_PAIR && ws->kind_upd_skip != KK_LDG) ? KK_PAIR : ws->kind_upd_skip;
         if (kd == KK_TMA) {
             const TmaGeom &gd = ws->geom_dir;
             cg_dir_tma<ORDER, PK><<<gd.ntx * gd.nty * gd.nchunk, kWSThreads, kDirSmem, s>>>(
