@@ -361,7 +361,9 @@ __global__ void __launch_bounds__(kPairThreads, 8) p2p_update(const P2PSet *__re
 
 // update, TMA form: the single-domain pipeline (update_tma_body) with the
 // boundary r planes also stored into the neighbours' halo planes
-template <int ORDER, int PK, int XM, bool SINGLE>
+// (S: TMA ring depth; the skip-x form stages only p and r, 4 deep as in the
+// single-domain loop)
+template <int ORDER, int PK, int XM, bool SINGLE, int S = (XM == XM_SKIP ? 4 : kStages)>
 __global__ void __launch_bounds__(kWSThreads, 4) p2p_update_tma(
     const P2PSet *__restrict__ psp, int half, double off, double diag, double zc, int use_cond,
     cudaGraphConditionalHandle cond, const __grid_constant__ CUtensorMap mp0, const __grid_constant__ CUtensorMap mp1,
@@ -386,13 +388,13 @@ __global__ void __launch_bounds__(kWSThreads, 4) p2p_update_tma(
     double rr, rz;
     int nchunk, ntiles;
     if constexpr (SINGLE) {
-        update_tma_body<ORDER, PK, XM>(half ? &mp0 : &mp1, &mr, &mx, half ? &mq1 : &mq0, g1, bid, off, diag, r1, x1,
+        update_tma_body<ORDER, PK, XM, S>(half ? &mp0 : &mp1, &mr, &mx, half ? &mq1 : &mq0, g1, bid, off, diag, r1, x1,
                                        zc, sc->alpha, sc->alpha_prev, lo1, hi1, red, rr, rz);
         nchunk = g1.nchunk;
         ntiles = g1.ntx * g1.nty;
     } else {
         const TmaGeom g = sl.gt;
-        update_tma_body<ORDER, PK, XM>(&sl.m_p[half ^ 1], &sl.m_ri, &sl.m_xi, &sl.m_pi[half], g, bid, off, diag, sl.r,
+        update_tma_body<ORDER, PK, XM, S>(&sl.m_p[half ^ 1], &sl.m_ri, &sl.m_xi, &sl.m_pi[half], g, bid, off, diag, sl.r,
                                        sl.x, zc, sc->alpha, sc->alpha_prev, sl.lo_r, sl.hi_r, red, rr, rz);
         nchunk = g.nchunk;
         ntiles = g.ntx * g.nty;
@@ -432,11 +434,11 @@ template <int ORDER, bool SINGLE>
 static void p2p_tma_attrs1()
 {
     cudaFuncSetAttribute(p2p_update_tma<ORDER, PK_NONE, XM_SKIP, SINGLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kUpdSmem);
+                         (int)upd_skip_smem<4>());
     cudaFuncSetAttribute(p2p_update_tma<ORDER, PK_NONE, XM_DOUBLE, SINGLE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem);
     cudaFuncSetAttribute(p2p_update_tma<ORDER, PK_JCONST, XM_SKIP, SINGLE>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_skip_smem<4>());
     cudaFuncSetAttribute(p2p_update_tma<ORDER, PK_JCONST, XM_DOUBLE, SINGLE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmem);
 }
@@ -533,7 +535,7 @@ static int p2p_body_t(cf_pcg *ws, cudaStream_t s, double zc, cudaGraphConditiona
         CF_CHECK_LAUNCH("p2p_dir");
         if (ws->tma) {
             if (half == 0)
-                p2p_update_tma<ORDER, PK, XM_SKIP, SINGLE><<<ws->grid_updt, kWSThreads, kUpdSmem, s>>>(
+                p2p_update_tma<ORDER, PK, XM_SKIP, SINGLE><<<ws->grid_updt, kWSThreads, upd_skip_smem<4>(), s>>>(
                     ws->d_set, half, ws->off, ws->diag, zc, use_cond, cond, d.m_p[0], d.m_p[1], d.m_ri, d.m_xi,
                     d.m_pi[0], d.m_pi[1], d.gt, d.r, d.x, d.lo_r, d.hi_r);
             else
