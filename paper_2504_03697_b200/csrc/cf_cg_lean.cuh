@@ -355,11 +355,14 @@ __global__ void __launch_bounds__(32 * ROWS, 8 * kPairRows / ROWS) cg_update_lea
 // registers).  A CTA of RW warps covers 2*RW rows.  Single domain (no slab
 // halos), same per-element arithmetic; the per-thread p.Ap order is row j
 // then row j+1 per plane.
-template <int ORDER, int PK, bool FIRST, int RW>
+template <int ORDER, int PK, bool FIRST, int RW, bool HALO = false>
 __device__ __forceinline__ double dir_lean2_march(const PairGeom &g, int bid, double off, double diag,
                                                   const double *__restrict__ zs, const double *__restrict__ po,
                                                   double *__restrict__ pn, double zc, double beta)
 {
+    // HALO (z-slab, cf_p2p.cu): as in dir_lean_march, pointers at the lowest
+    // plane in memory, halo planes of p recomputed and stored
+    const int lo = HALO && g.lo_halo ? 1 : 0, hi = HALO && g.hi_halo ? 1 : 0;
     using Src = LeanSrc<PK, FIRST>;
     using Raw = typename Src::Raw;
     using Raw1 = typename Src::Raw1;
@@ -372,7 +375,7 @@ __device__ __forceinline__ double dir_lean2_march(const PairGeom &g, int bid, do
     const int z0 = (int)((long long)g.nz * chunk / g.nchunk);
     const int z1 = (int)((long long)g.nz * (chunk + 1) / g.nchunk);
     const unsigned nx = (unsigned)g.nx, pl = nx * (unsigned)g.ny;
-    const unsigned zero = pl * (unsigned)g.nz + 2u * (unsigned)lane;
+    const unsigned zero = pl * (unsigned)(g.nz + lo + hi) + 2u * (unsigned)lane;
     const bool xv = i < g.nx;
     const bool v0 = xv, v1 = xv && j + 1 < g.ny;          // the two rows' pairs exist
     const bool hym = v0 && j > 0, hyp = v1 && j + 2 < g.ny;  // outer y-neighbour rows
@@ -381,15 +384,19 @@ __device__ __forceinline__ double dir_lean2_march(const PairGeom &g, int bid, do
     const unsigned de = lane == 0 ? 0xffffffffu : 2u;
     const Src src{zs, po, zc, beta};
 
-    unsigned c = (unsigned)i + nx * (unsigned)j + pl * (unsigned)(z1 - 1);  // row j; row j+1 is c + nx
-    const bool top = z1 < g.nz;
+    unsigned c = (unsigned)i + nx * (unsigned)j + pl * (unsigned)(z1 - 1 + lo);  // row j; row j+1 is c + nx
+    const bool top = z1 < g.nz + hi;
     double2 cp0 = src.form(src.raw(v0 && top ? c + pl : zero));
     double2 cp1 = src.form(src.raw(v1 && top ? c + nx + pl : zero));
     double2 cc0 = src.form(src.raw(v0 ? c : zero));
     double2 cc1 = src.form(src.raw(v1 ? c + nx : zero));
+    if (hi && z1 == g.nz) {  // the slab's top halo plane of p
+        if (v0) *reinterpret_cast<double2 *>(pn + c + pl) = cp0;
+        if (v1) *reinterpret_cast<double2 *>(pn + c + nx + pl) = cp1;
+    }
     double pap = 0.0;
     for (int z = z1 - 1; z >= z0; --z, c -= pl) {
-        const bool hzm = z >= 1;
+        const bool hzm = z + lo >= 1;
         const Raw rm0 = src.raw(v0 && hzm ? c - pl : zero);
         const Raw rm1 = src.raw(v1 && hzm ? c + nx - pl : zero);
         const Raw rym = src.raw(hym ? c - nx : zero);
@@ -422,6 +429,10 @@ __device__ __forceinline__ double dir_lean2_march(const PairGeom &g, int bid, do
             *reinterpret_cast<double2 *>(pn + c + nx) = cc1;
             pap = pap + cc1.x * b0;
             pap = pap + cc1.y * b1;
+        }
+        if (lo && z == 0) {  // bottom halo plane of p
+            if (v0) *reinterpret_cast<double2 *>(pn + c - pl) = cm0;
+            if (v1) *reinterpret_cast<double2 *>(pn + c + nx - pl) = cm1;
         }
         cp0 = cc0;
         cc0 = cm0;

@@ -33,6 +33,8 @@ struct PairGeom {
 // Host: geometry for an nx*ny*nz block (z-slab halos lo/hi), z cut into
 // chunks of ~32 planes (env_name: override of the chunk count).  cf_cg.cu.
 PairGeom pair_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, const char *env_name);
+// Host: lean-march geometry -- 64 x rows tiles, wave-aware z chunks (cf_cg.cu).
+PairGeom lean_geom(int nx, int ny, int nz, int rows, int ctas4);
 
 struct PairCoords {
     int lane, i, j, z0, z1, zlo, zhi;

@@ -236,8 +236,10 @@ __global__ void __launch_bounds__(256) p2p_init(const P2PSet *__restrict__ psp, 
 // come as kernel parameters, so the compiler sees constant-bank geometry and
 // __restrict__ pointers exactly as in the single-domain kernels; the
 // multi-slab emulation reads them from the descriptor.
+// direction CTAs: 4 warps x 2 rows (dir_lean2_march), 8-row tiles
+constexpr int kP2PDirRows = 8;
 template <int ORDER, int PK, bool SINGLE>
-__global__ void __launch_bounds__(kPairThreads, 8) p2p_dir(const P2PSet *__restrict__ psp, int half, double off,
+__global__ void __launch_bounds__(kPairThreads, 6) p2p_dir(const P2PSet *__restrict__ psp, int half, double off,
                                                           double diag, double zc, PairGeom g1,
                                                           const double *__restrict__ r1, double *__restrict__ p0_1,
                                                           double *__restrict__ p1_1)
@@ -260,18 +262,16 @@ __global__ void __launch_bounds__(kPairThreads, 8) p2p_dir(const P2PSet *__restr
     if constexpr (SINGLE) {
         const double *po = half ? p1_1 : p0_1;
         double *pn = half ? p0_1 : p1_1;
-        pap = sc->it == 0 ? dir_lean_march<ORDER, PK, true, 0, kPairRows, true>(g1, bid, off, diag, r1, po, pn, zc, 0.0)
-                          : dir_lean_march<ORDER, PK, false, 0, kPairRows, true>(g1, bid, off, diag, r1, po, pn, zc,
-                                                                                  sc->beta);
+        pap = sc->it == 0 ? dir_lean2_march<ORDER, PK, true, 4, true>(g1, bid, off, diag, r1, po, pn, zc, 0.0)
+                          : dir_lean2_march<ORDER, PK, false, 4, true>(g1, bid, off, diag, r1, po, pn, zc, sc->beta);
     } else {
         const PairGeom g = sl.gd;
         const size_t sh = g.lo_halo ? (size_t)g.nx * g.ny : 0;
         const double *po = (half ? sl.p1 : sl.p0) - sh;
         double *pn = (half ? sl.p0 : sl.p1) - sh;
         pap = sc->it == 0
-                  ? dir_lean_march<ORDER, PK, true, 0, kPairRows, true>(g, bid, off, diag, sl.r - sh, po, pn, zc, 0.0)
-                  : dir_lean_march<ORDER, PK, false, 0, kPairRows, true>(g, bid, off, diag, sl.r - sh, po, pn, zc,
-                                                                          sc->beta);
+                  ? dir_lean2_march<ORDER, PK, true, 4, true>(g, bid, off, diag, sl.r - sh, po, pn, zc, 0.0)
+                  : dir_lean2_march<ORDER, PK, false, 4, true>(g, bid, off, diag, sl.r - sh, po, pn, zc, sc->beta);
     }
     pap = block_sum<kPairThreads>(pap, red);
     if (threadIdx.x == 0) sl.partials[bid] = pap;
@@ -717,7 +717,9 @@ int cf_pcg_create(cf_pcg **out, int nx, int ny, int nz, double h, int order, int
             if (e == cudaSuccess) e = cudaMemsetAsync(sb.alloc[a], 0, bytes, s);
         }
         cf::P2PSlab &d = ws->set.s[k];
-        d.gd = cf::pair_geom(nx, ny, sb.nzl, sb.lo, sb.hi, "CF_PAIR_CHUNKS_DIR");
+        d.gd = cf::lean_geom(nx, ny, sb.nzl, cf::kP2PDirRows, 12);  // 6 resident 128-thread CTAs per SM
+        d.gd.lo_halo = sb.lo;
+        d.gd.hi_halo = sb.hi;
         d.gu = cf::pair_geom(nx, ny, sb.nzl, sb.lo, sb.hi, "CF_PAIR_CHUNKS_UPD");
         d.blk_dir = bd;
         d.blk_upd = bu;
