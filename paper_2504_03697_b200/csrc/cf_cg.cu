@@ -573,6 +573,7 @@ struct cf_cg {
     // lean kernels (cf_cg_lean.cuh): warps (tile rows) per CTA, CF_LEAN_ROWS
     int lean_rows = 16;  // with lean2: 8 warps x 2 rows (measured +0.4 % over 8-row tiles in the sustained bench)
     // TMA ring depth of the skip-x update kernel (3 = the shared layout; CF_SKIP_STAGES=4/6)
+    int double_stages = 4;  // double-x update ring depth: 4 (70 KB, 3 CTAs/SM; +0.3 % sustained over 3; CF_DOUBLE_STAGES=3)
     int skip_stages = 4;
     // persistent single-launch solve for L2-resident grids (cf_cg_persist.cuh; CF_PERSIST=0/1)
     bool persist = false;
@@ -733,6 +734,10 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
                 launch_k(ws, cg_update_tma<ORDER, PK, XM_SKIP>, nb, kWSThreads, kUpdSmem, s, ws->m_p[half ^ 1], ws->m_ri,
                          ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc, ws->partials,
                          ws->tk, use_cond, cond, (double *)nullptr);
+            else if (ws->double_stages == 4)
+                launch_k(ws, cg_update_tma<ORDER, PK, XM_DOUBLE, 4>, nb, kWSThreads, upd_full_smem<4>(), s,
+                         ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x,
+                         zc, ws->sc, ws->partials, ws->tk, use_cond, cond, (double *)nullptr);
             else
                 launch_k(ws, cg_update_tma<ORDER, PK, XM_DOUBLE>, nb, kWSThreads, kUpdSmem, s, ws->m_p[half ^ 1], ws->m_ri,
                          ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc, ws->partials,
@@ -1065,6 +1070,9 @@ static void set_grids(cf_cg *ws)
         set_upd_smem<ORDER, XM_EACH>();
         set_upd_smem<ORDER, XM_SKIP>();
         set_upd_smem<ORDER, XM_DOUBLE>();
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_NONE, XM_DOUBLE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_full_smem<4>());
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_JCONST, XM_DOUBLE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_full_smem<4>());
+        cudaFuncSetAttribute(cg_update_tma<ORDER, PK_ZVEC, XM_DOUBLE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_full_smem<4>());
         cudaFuncSetAttribute(cg_update_tma<ORDER, PK_NONE, XM_SKIP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_skip_smem<4>());
         cudaFuncSetAttribute(cg_update_tma<ORDER, PK_JCONST, XM_SKIP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_skip_smem<4>());
         cudaFuncSetAttribute(cg_update_tma<ORDER, PK_ZVEC, XM_SKIP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_skip_smem<4>());
@@ -1089,6 +1097,7 @@ static void set_grids(cf_cg *ws)
     if (ws->kind_upd == KK_LEAN && ws->n + kLeanPad >= (1LL << 32)) ws->kind_upd = KK_PAIR;
     if (const char *e = getenv("CF_PDL")) ws->pdl = atoi(e) != 0;
     if (const char *e = getenv("CF_LEAN2")) ws->lean2 = atoi(e) != 0;
+    if (const char *e = getenv("CF_DOUBLE_STAGES")) ws->double_stages = atoi(e) == 3 ? 3 : 4;
     if (const char *e = getenv("CF_SKIP_STAGES")) ws->skip_stages = atoi(e) == 3 ? 3 : (atoi(e) == 6 ? 6 : 4);
     if (const char *e = getenv("CF_LEAN_ROWS")) ws->lean_rows = atoi(e) == 4 ? 4 : (atoi(e) == 8 ? 8 : 16);
     ws->lg_dir = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows,

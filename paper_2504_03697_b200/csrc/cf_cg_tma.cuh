@@ -234,3 +234,5 @@ constexpr size_t kUpdSmem = kStages * (kBoxStride + 3 * kInt) * sizeof(double) +
 // the skip-x update stages only the p halo box and the r box: deeper rings fit
 template <int S>
 constexpr size_t upd_skip_smem() { return (size_t)S * (kBoxStride + kInt) * sizeof(double) + 128; }
+template <int S>
+constexpr size_t upd_full_smem() { return (size_t)S * (kBoxStride + 3 * kInt) * sizeof(double) + 128; }
