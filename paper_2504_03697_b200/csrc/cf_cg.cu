@@ -573,7 +573,7 @@ struct cf_cg {
     // lean kernels (cf_cg_lean.cuh): warps (tile rows) per CTA, CF_LEAN_ROWS
     int lean_rows = 16;  // with lean2: 8 warps x 2 rows (measured +0.4 % over 8-row tiles in the sustained bench)
     // TMA ring depth of the skip-x update kernel (3 = the shared layout; CF_SKIP_STAGES=4/6)
-    int double_stages = 4;  // double-x update ring depth: 4 (70 KB, 3 CTAs/SM; +0.3 % sustained over 3; CF_DOUBLE_STAGES=3)
+    int double_stages = 4;  // double-x update ring depth: 4 (70 KB, 3 CTAs/SM, own geometry; within noise of 3 in the sustained bench; CF_DOUBLE_STAGES=3)
     int skip_stages = 4;
     // persistent single-launch solve for L2-resident grids (cf_cg_persist.cuh; CF_PERSIST=0/1)
     bool persist = false;
@@ -586,7 +586,7 @@ struct cf_cg {
     bool lean2 = true;  // two-rows-per-warp direction march (CF_LEAN2=0: one row per warp); +0.5 % in the sustained bench
     cf::PairGeom lg_dir{}, lg_upd{};
     cf::PairGeom pg_dir{}, pg_upd{};
-    cf::TmaGeom geom_dir{}, geom_upd{};
+    cf::TmaGeom geom_dir{}, geom_upd{}, geom_dbl{};  // geom_dbl: the 4-deep double-x update (3 CTAs/SM)
     CUtensorMap m_r{}, m_z{}, m_p[2]{}, m_ri{}, m_xi{}, m_pi[2]{};
     // x updated once per two iterations (XM_SKIP / XM_DOUBLE, cf_cg_common.cuh)
     bool defer_x = false;
@@ -735,9 +735,10 @@ static int capture_body(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCondition
                          ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc, ws->partials,
                          ws->tk, use_cond, cond, (double *)nullptr);
             else if (ws->double_stages == 4)
-                launch_k(ws, cg_update_tma<ORDER, PK, XM_DOUBLE, 4>, nb, kWSThreads, upd_full_smem<4>(), s,
-                         ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x,
-                         zc, ws->sc, ws->partials, ws->tk, use_cond, cond, (double *)nullptr);
+                launch_k(ws, cg_update_tma<ORDER, PK, XM_DOUBLE, 4>, ws->geom_dbl.ntx * ws->geom_dbl.nty * ws->geom_dbl.nchunk,
+                         kWSThreads, upd_full_smem<4>(), s, ws->m_p[half ^ 1], ws->m_ri, ws->m_xi, ws->m_pi[half],
+                         ws->geom_dbl, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc, ws->partials, ws->tk, use_cond,
+                         cond, (double *)nullptr);
             else
                 launch_k(ws, cg_update_tma<ORDER, PK, XM_DOUBLE>, nb, kWSThreads, kUpdSmem, s, ws->m_p[half ^ 1], ws->m_ri,
                          ws->m_xi, ws->m_pi[half], gu, ws->off, ws->diag, ws->r, ws->x, zc, ws->sc, ws->partials,
@@ -1085,6 +1086,10 @@ static void set_grids(cf_cg *ws)
         ws->geom_upd = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bu > 0 ? bu : 1);
         if (const char *e = getenv("CF_TMA_CHUNKS_DIR")) ws->geom_dir.nchunk = atoi(e) > 0 ? atoi(e) : 1;
         if (const char *e = getenv("CF_TMA_CHUNKS_UPD")) ws->geom_upd.nchunk = atoi(e) > 0 ? atoi(e) : 1;
+        int bdb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bdb, cg_update_tma<ORDER, PK_JCONST, XM_DOUBLE, 4>, kWSThreads,
+                                                      upd_full_smem<4>());
+        ws->geom_dbl = tma_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, bdb > 0 ? bdb : 1);
     }
     const bool pair_ok = ws->bx.nx % 2 == 0 && !(no_tma && atoi(no_tma) > 0);
     ws->pg_dir = pair_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, 0, 0, "CF_PAIR_CHUNKS_DIR");
@@ -1203,7 +1208,8 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
     if (ws->grid_init > maxg) maxg = ws->grid_init;
     if (ws->grid_init_x0 > maxg) maxg = ws->grid_init_x0;
     if (ws->tma) {
-        const cf::TmaGeom &gd = ws->geom_dir, &gu = ws->geom_upd;
+        const cf::TmaGeom &gd = ws->geom_dir, &gu = ws->geom_upd, &gb = ws->geom_dbl;
+        maxg = std::max(maxg, gb.ntx * gb.nty * gb.nchunk);
         int g1 = gd.ntx * gd.nty * gd.nchunk, g2 = gu.ntx * gu.nty * gu.nchunk;
         if (g1 > maxg) maxg = g1;
         if (g2 > maxg) maxg = g2;
