@@ -208,13 +208,14 @@ __global__ void __launch_bounds__(kCellThreads) divergence_kernel(Vel3 in, SlabZ
     __shared__ double red[32];
     __shared__ int is_last;
     const int nx = sz.nx, ny = sz.ny;
-    const long long total = (long long)nx * ny * (sz.z1 - sz.z0);
-    const long long stride = (long long)gridDim.x * kCellThreads;
+    // 32-bit cell index (a slab's cells < 2^31, checked by pitches_ok)
+    const int total = nx * ny * (sz.z1 - sz.z0);
+    const int stride = gridDim.x * kCellThreads;
     double mx = 0.0;
-    for (long long c = (long long)blockIdx.x * kCellThreads + threadIdx.x; c < total; c += stride) {
-        const int i = (int)(c % nx);
-        const long long rest = c / nx;
-        const int j = (int)(rest % ny), k = sz.z0 + (int)(rest / ny);
+    for (int c = blockIdx.x * kCellThreads + threadIdx.x; c < total; c += stride) {
+        const int i = c % nx;
+        const int rest = c / nx;
+        const int j = rest % ny, k = sz.z0 + rest / ny;
         double t = in.c[0].at(i + 1, j, k) - in.c[0].at(i, j, k);
         t = t + in.c[1].at(i, j + 1, k);
         t = t - in.c[1].at(i, j, k);
@@ -250,14 +251,15 @@ __global__ void __launch_bounds__(kCellThreads) correct_kernel(Vel3 in, double *
     __shared__ double red[32];
     __shared__ int is_last;
     const int nx = sz.nx, ny = sz.ny, nz = sz.nz;
-    const long long total = (long long)nx * ny * (sz.z1 - sz.z0);
-    const long long stride = (long long)gridDim.x * kCellThreads;
-    const long long pl = (long long)nx * ny;
+    // 32-bit (signed: the slab's p halo plane sits at c - pl < 0) cell index
+    const int total = nx * ny * (sz.z1 - sz.z0);
+    const int stride = gridDim.x * kCellThreads;
+    const int pl = nx * ny;
     double mx = 0.0;
-    for (long long c = (long long)blockIdx.x * kCellThreads + threadIdx.x; c < total; c += stride) {
-        const int i = (int)(c % nx);
-        const long long rest = c / nx;
-        const int j = (int)(rest % ny), k = sz.z0 + (int)(rest / ny);
+    for (int c = blockIdx.x * kCellThreads + threadIdx.x; c < total; c += stride) {
+        const int i = c % nx;
+        const int rest = c / nx;
+        const int j = rest % ny, k = sz.z0 + rest / ny;
         const double pc = __ldg(p + c);
         // lower face: interior -> coef*(p - p_prev); wall -> coef*p
         // upper face: interior -> coef*(p_next - p); wall -> coef*(0.0 - p)
@@ -454,10 +456,10 @@ static int grid_for(long long work, int threads, int per_sm)
 static bool pitches_ok(const SlabZ &sz, int ldu, int ldv, int ldw)
 {
     // stored planes of the widest component (w: the slab plus its halos and the
-    // top face) must stay below 2^32 elements: the kernels index in 32 bits
+    // top face) must stay below 2^31 elements: the kernels index in 32 bits
     const long long planes = (long long)(sz.z1 - sz.z0) + 2LL * sz.H + 1;
     const long long big = (long long)std::max(ldu, std::max(ldv, ldw)) * (sz.ny + 1) * planes;
-    return ldu >= sz.nx + 1 && ldv >= sz.nx && ldw >= sz.nx && big < (1LL << 32);
+    return ldu >= sz.nx + 1 && ldv >= sz.nx && ldw >= sz.nx && big < (1LL << 31);
 }
 
 static bool slab_ok(const SlabZ &s)
