@@ -360,6 +360,49 @@ __device__ __forceinline__ double small_ap(const double *v, int c, const Box &bx
                            hzm, hzp, off, diag);
 }
 
+// block_sum (cf_common.cuh) whose result every thread receives, in ONE
+// barrier: every warp repeats warp 0's final tree over the per-warp partials
+// (the same operations in the same order, so the same bits), then broadcasts
+// lane 0.  buf must not be reused before every thread has passed the next
+// barrier (the callers rotate buffers).
+template <int NT>
+__device__ __forceinline__ double block_sum_all(double v, double *buf)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NW = NT / 32;
+    if (lane == 0) buf[wid] = v;
+    __syncthreads();
+    v = lane < NW ? buf[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return __shfl_sync(0xffffffffu, v, 0);
+}
+
+// a cell's existing-neighbour mask (bit 0..5: x-, x+, y-, y+, z-, z+)
+__device__ __forceinline__ int small_mask(int c, const Box &bx)
+{
+    const int nx = bx.nx, ny = bx.ny;
+    const int i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+    return (i > 0) | (i < nx - 1) << 1 | (j > 0) << 2 | (j < ny - 1) << 3 | (k > 0) << 4 | (k < bx.nz - 1) << 5;
+}
+
+template <int ORDER>
+__device__ __forceinline__ double small_ap_m(const double *v, int c, int m, int nx, int pl, double off, double diag)
+{
+    const bool hxm = m & 1, hxp = m & 2, hym = m & 4, hyp = m & 8, hzm = m & 16, hzp = m & 32;
+    return stencil7<ORDER>(v[c], hxm ? v[c - 1] : 0.0, hxp ? v[c + 1] : 0.0, hym ? v[c - nx] : 0.0,
+                           hyp ? v[c + nx] : 0.0, hzm ? v[c - pl] : 0.0, hzp ? v[c + pl] : 0.0, hxm, hxp, hym, hyp,
+                           hzm, hzp, off, diag);
+}
+
+// Per iteration: p update | barrier | A p kept in registers, p.Ap (one
+// barrier) | r, x from the kept A p, r.r and r.z (one barrier) -- three
+// barriers instead of nine, each cell's neighbour mask computed once per
+// solve and A p evaluated once (the same values: bit-identical).
+constexpr int kSmallPer = (int)((kSmallMaxCells + kSmallThreads - 1) / kSmallThreads);
+
 template <int ORDER, int PK>
 __global__ void __launch_bounds__(kSmallThreads) cg_small_kernel(Box bx, double off, double diag,
                                                                  const double *__restrict__ b,
@@ -368,10 +411,12 @@ __global__ void __launch_bounds__(kSmallThreads) cg_small_kernel(Box bx, double 
 {
     extern __shared__ double sm[];
     __shared__ double red[32];
+    __shared__ double rbuf[3][32];  // rotating broadcast-reduction buffers
     __shared__ double bc[2];
     const int n = (int)bx.cells();
     double *r = sm, *p = sm + n, *x = sm + 2 * n;
     const int t = threadIdx.x;
+    const int nx = bx.nx, pl = bx.nx * bx.ny;
     // r = b (or b - A x0), x = 0 (or x0); |b|^2 and r.z  (src/solver.py:60-61, :130-143)
     for (int c = t; c < n; c += kSmallThreads) x[c] = x0 ? x0[c] : 0.0;
     __syncthreads();
@@ -392,40 +437,56 @@ __global__ void __launch_bounds__(kSmallThreads) cg_small_kernel(Box bx, double 
     __syncthreads();
     CgScalars s = *sc;  // tol, max_iter from the host
     scalar_after_init(&s, bc[0], bc[1]);
+    int mask[kSmallPer];
+    double ap[kSmallPer];
+#pragma unroll
+    for (int q = 0; q < kSmallPer; ++q) {
+        const int c = t + q * kSmallThreads;
+        mask[q] = c < n ? small_mask(c, bx) : 0;
+    }
     while (!s.done) {
         // p = z + beta p (in place: each element depends on itself only)
-        for (int c = t; c < n; c += kSmallThreads) {
-            const double z = zval<PK>(r[c], jd, c, zc);
-            p[c] = s.it == 0 ? z : z + s.beta * p[c];
+#pragma unroll
+        for (int q = 0; q < kSmallPer; ++q) {
+            const int c = t + q * kSmallThreads;
+            if (c < n) {
+                const double z = zval<PK>(r[c], jd, c, zc);
+                p[c] = s.it == 0 ? z : z + s.beta * p[c];
+            }
         }
         __syncthreads();
         double pap = 0.0;
-        for (int c = t; c < n; c += kSmallThreads) pap = pap + p[c] * small_ap<ORDER>(p, c, bx, off, diag);
-        pap = block_sum<kSmallThreads>(pap, red);
-        if (t == 0) bc[0] = pap;
-        __syncthreads();
-        scalar_after_dir(&s, bc[0]);
+#pragma unroll
+        for (int q = 0; q < kSmallPer; ++q) {
+            const int c = t + q * kSmallThreads;
+            if (c < n) {
+                ap[q] = small_ap_m<ORDER>(p, c, mask[q], nx, pl, off, diag);
+                pap = pap + p[c] * ap[q];
+            }
+        }
+        pap = block_sum_all<kSmallThreads>(pap, rbuf[0]);
+        scalar_after_dir(&s, pap);
         if (s.done) break;
         const double alpha = s.alpha, malpha = -alpha;
         double rr = 0.0;
         rz = 0.0;
-        for (int c = t; c < n; c += kSmallThreads) {
-            const double pc = p[c];
-            x[c] = x[c] + alpha * pc;
-            const double rn = r[c] + malpha * small_ap<ORDER>(p, c, bx, off, diag);
-            r[c] = rn;
-            rr = rr + rn * rn;
-            rz = rz + rn * zval<PK>(rn, jd, c, zc);
+#pragma unroll
+        for (int q = 0; q < kSmallPer; ++q) {
+            const int c = t + q * kSmallThreads;
+            if (c < n) {
+                const double pc = p[c];
+                x[c] = x[c] + alpha * pc;
+                const double rn = r[c] + malpha * ap[q];
+                r[c] = rn;
+                rr = rr + rn * rn;
+                rz = rz + rn * zval<PK>(rn, jd, c, zc);
+            }
         }
-        rr = block_sum<kSmallThreads>(rr, red);
-        rz = block_sum<kSmallThreads>(rz, red);
-        if (t == 0) {
-            bc[0] = rr;
-            bc[1] = rz;
-        }
-        __syncthreads();
-        scalar_after_update<true>(&s, bc[0], bc[1]);
+        rr = block_sum_all<kSmallThreads>(rr, rbuf[1]);
+        rz = block_sum_all<kSmallThreads>(rz, rbuf[2]);
+        scalar_after_update<true>(&s, rr, rz);
     }
+    __syncthreads();
     for (int c = t; c < n; c += kSmallThreads) xout[c] = x[c];
     if (t == 0) *sc = s;
 }
