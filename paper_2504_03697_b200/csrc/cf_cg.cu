@@ -1168,6 +1168,13 @@ static void set_grids(cf_cg *ws)
     if (const char *e = getenv("CF_LEAN_ROWS")) ws->lean_rows = atoi(e) == 4 ? 4 : (atoi(e) == 8 ? 8 : 16);
     ws->lg_dir = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows,
                            ws->lean2 && ws->lean_rows == 8 ? 12 : (ws->lean2 && ws->lean_rows == 16 ? 12 : 8));
+    // the direction kernel takes its z chunks top-down: its last wave (the low
+    // chunks, bottom planes last) is where the update kernel's first wave
+    // starts, and the update's last wave (high chunks, top planes last) is
+    // where the next direction kernel starts -- both hand-overs in L2
+    // (measured: +2 % in the sustained bench, 190 -> 186 us per 256^3 iteration)
+    ws->lg_dir.chunk_rev = 1;
+    if (const char *e = getenv("CF_CHUNK_REV")) ws->lg_dir.chunk_rev = atoi(e) != 0;
     ws->lg_upd = lean_geom(ws->bx.nx, ws->bx.ny, ws->bx.nz, ws->lean_rows, 8);
     // persistent solve: the four CG vectors fit in L2 with room to spare
     // (<= 96 MB), above the single-block range; all CTAs co-resident

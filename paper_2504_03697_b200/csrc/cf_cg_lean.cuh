@@ -133,7 +133,7 @@ __device__ __forceinline__ double dir_lean_march(const PairGeom &g, int bid, dou
     using Raw1 = typename LeanSrc<PK, FIRST, COH>::Raw1;
     const int lane = threadIdx.x & 31;
     const int ntiles = g.ntx * g.nty;
-    const int tile = bid % ntiles, chunk = bid / ntiles;
+    const int tile = bid % ntiles, chunk = g.chunk_of(bid);
     const int i = (tile % g.ntx) * kPairX + 2 * lane;
     const int j = (tile / g.ntx) * ROWS + (threadIdx.x >> 5);
     if (j >= g.ny) return 0.0;  // the whole warp
@@ -255,7 +255,7 @@ __device__ __forceinline__ void upd_lean_march(const PairGeom &g, int bid, doubl
 {
     const int lane = threadIdx.x & 31;
     const int ntiles = g.ntx * g.nty;
-    const int tile = bid % ntiles, chunk = bid / ntiles;
+    const int tile = bid % ntiles, chunk = g.chunk_of(bid);
     const int i = (tile % g.ntx) * kPairX + 2 * lane;
     const int j = (tile / g.ntx) * ROWS + (threadIdx.x >> 5);
     if (j >= g.ny) return;  // the whole warp
@@ -368,7 +368,7 @@ __device__ __forceinline__ double dir_lean2_march(const PairGeom &g, int bid, do
     using Raw1 = typename Src::Raw1;
     const int lane = threadIdx.x & 31;
     const int ntiles = g.ntx * g.nty;
-    const int tile = bid % ntiles, chunk = bid / ntiles;
+    const int tile = bid % ntiles, chunk = g.chunk_of(bid);
     const int i = (tile % g.ntx) * kPairX + 2 * lane;
     const int j = (tile / g.ntx) * (2 * RW) + 2 * (threadIdx.x >> 5);  // rows j, j+1
     if (j >= g.ny) return 0.0;

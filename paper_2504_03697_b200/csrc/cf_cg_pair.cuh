@@ -27,7 +27,15 @@ struct PairGeom {
     int nx, ny, nz;
     int lo_halo, hi_halo;  // plane -1 / plane nz exist in memory (z-slab halos)
     int ntx, nty, nchunk;
+    // 1: CTAs take the z chunks from the top down (the lean marches), so a
+    // kernel's last wave ends where the next kernel's first wave starts
+    int chunk_rev = 0;
     __host__ __device__ int ctas() const { return ntx * nty * nchunk; }
+    __host__ __device__ int chunk_of(int bid) const
+    {
+        const int c = bid / (ntx * nty);
+        return chunk_rev ? nchunk - 1 - c : c;
+    }
 };
 
 // Host: geometry for an nx*ny*nz block (z-slab halos lo/hi), z cut into

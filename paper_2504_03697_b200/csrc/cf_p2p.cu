@@ -720,6 +720,7 @@ int cf_pcg_create(cf_pcg **out, int nx, int ny, int nz, double h, int order, int
         d.gd = cf::lean_geom(nx, ny, sb.nzl, cf::kP2PDirRows, 12);  // 6 resident 128-thread CTAs per SM
         d.gd.lo_halo = sb.lo;
         d.gd.hi_halo = sb.hi;
+        d.gd.chunk_rev = 1;  // top-down chunk order: L2 hand-over to / from the update kernel (cf_cg.cu)
         d.gu = cf::pair_geom(nx, ny, sb.nzl, sb.lo, sb.hi, "CF_PAIR_CHUNKS_UPD");
         d.blk_dir = bd;
         d.blk_upd = bu;
