@@ -1337,6 +1337,9 @@ int cf_cg_destroy(cf_cg *ws)
         if (b) cudaFree(b);
     if (ws->per_bar) cudaFree(ws->per_bar);
     if (ws->dic_lptr) cudaFree(ws->dic_lptr);
+    if (ws->dic.wave.prog_f) cudaFree(ws->dic.wave.prog_f);
+    if (ws->dic.wave.ex_f) cudaFree(ws->dic.wave.ex_f);
+    if (ws->dic.wave.ey_f) cudaFree(ws->dic.wave.ey_f);
     if (ws->sc) cudaFree(ws->sc);
     if (ws->tk) cudaFree(ws->tk);
     if (ws->sc_host) cudaFreeHost(ws->sc_host);

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd(DicWave dw, const dou
         // Progress is published every `pub` steps -- a release waits for the
         // stores to land, so it is amortised, not paid per diagonal; the
         // barrier orders every thread's stores before it (cumulativity).
-        if ((s + 1) % dw.pub == 0 || s + 1 == nsteps) {
+        if (((s + 1) & (dw.pub - 1)) == 0 || s + 1 == nsteps) {
             tile_sync<kWTX * kWTY>();
             if (threadIdx.x == 0) st_release_gpu(dw.prog_f + t, s + 1);
         }
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd(DicWave dw, const dou
             zk = zv;
         }
         sm[(s + 1) & 1][tj][ti] = zv;
-        if ((s + 1) % dw.pub == 0 || s + 1 == nsteps) {
+        if (((s + 1) & (dw.pub - 1)) == 0 || s + 1 == nsteps) {
             tile_sync<kWTX * kWTY>();
             if (threadIdx.x == 0) st_release_gpu(dw.prog_b + t, s + 1);
         }
@@ -252,26 +252,69 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd(DicWave dw, const dou
 }
 
 // ---------------------------------------------------------------------------
-// Pipelined form (D-deep): every load a step needs -- this thread's r (or w)
-// and d, and the neighbouring tiles' edge values -- is copied into a shared
-// ring by cp.async D-1 steps ahead, so a diagonal step no longer waits for a
-// memory round trip (the one-step-ahead prefetch above left each step at the
-// ~1.3 us load latency; the DAG depth is only ~1.1x the 3n-2 diagonals).
-// Edges fetched D-1 steps ahead need the neighbour D-1 steps further on: the
-// slack is D-1.  Same arithmetic in the same order: bit-identical results.
+// Pipelined form: this thread's own r (or w) and d -- independent of the
+// sweep -- are copied into a D-deep shared ring by cp.async D-1 steps ahead,
+// so a diagonal step does not wait for a DRAM round trip.  The neighbouring
+// tiles' edge values depend on the sweep: they are loaded into registers one
+// step ahead, after the neighbour has published that step, so the lead
+// between tiles (the slack) stays one step whatever the ring depth.  (Edges
+// in the same ring forced slack D-1 and made every deeper ring slower: 2.43,
+// 2.61, 2.74 ms per 256^3 DIC-PCG iteration at D = 2, 3, 4.)  Same arithmetic
+// in the same order: bit-identical results.
 __device__ __forceinline__ void cp_async8_ca(double *dst, const double *src, int src_bytes)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
                  : "memory");
 }
-__device__ __forceinline__ void cp_async16_cg(void *dst, const double *src, int src_bytes)
-{
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
-                 : "memory");
-}
 __device__ __forceinline__ void cp_async_commit_grp() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait_grp() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Edge mailboxes.  The value itself is the flag: a slot holds kEdgeEmpty (a
+// signalling-NaN pattern no arithmetic result has -- GPU fp64 results carry
+// the canonical quiet NaN) until the producing tile stores the boundary
+// value; the single reader spins on the slot with relaxed gpu-scope loads
+// (8-byte accesses are single-copy atomic) and re-arms it after reading.  No
+// other data travels between tiles during a sweep, so no release / acquire,
+// progress counter or fence is needed: the producer never stalls on a
+// memory barrier and the reader waits for exactly the value it uses.
+constexpr unsigned long long kEdgeEmpty = 0x7FF00000DEADBEEFull;
+
+__device__ __forceinline__ void edge_put(double *p, double v)
+{
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
+}
+
+__device__ __forceinline__ double edge_take(double *p)
+{
+    unsigned long long v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    } while (v == kEdgeEmpty);
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(kEdgeEmpty) : "memory");
+    return __longlong_as_double((long long)v);
+}
+
+// A slot prefetched into shared memory by a 16-byte cp.async.cg (L2, the
+// coherence point) D-1 steps ahead: if it already held the value it is
+// re-armed, else the reader falls back to spinning on the slot.
+__device__ __forceinline__ double edge_use(double *p, const double2 &pre)
+{
+    if ((unsigned long long)__double_as_longlong(pre.x) == kEdgeEmpty) return edge_take(p);
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(kEdgeEmpty) : "memory");
+    return pre.x;
+}
+
+__device__ __forceinline__ void cp_async16_cg(void *dst, const void *src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+__global__ void edge_arm(double *p, long long n)
+{
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x)
+        p[q] = __longlong_as_double((long long)kEdgeEmpty);
+}
 
 // wait (thread 0) until a neighbour's published progress covers `need`
 __device__ __forceinline__ bool wave_wait(const int *nb, int need, int &seen, int &peek)
@@ -291,7 +334,7 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd_p(DicWave dw, const d
     constexpr int NT = kWTX * kWTY;
     __shared__ double sm[2][kWTY][kWTX];
     __shared__ __align__(16) double ring_r[D][NT], ring_d[D][NT];
-    __shared__ __align__(16) double2 ring_x[D][kWTY], ring_y[D][kWTX];  // left / lower edge pairs
+    __shared__ __align__(16) double2 ring_x[D][kWTY], ring_y[D][kWTX];  // prefetched mailbox slots
     if (done && *done) return;
     const int ntx = dw.ntx;
     const int t = blockIdx.x, a = t % ntx, b = t / ntx;
@@ -300,65 +343,56 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd_p(DicWave dw, const d
     const bool col_ok = i < dw.nx && j < dw.ny;
     const long long pl = (long long)dw.nx * dw.ny;
     const long long base = (long long)i + (long long)dw.nx * j;
-    if (tid == 0) dw.prog_b[t] = 0;  // re-arm the backward sweep's counters
-    const int *left = a > 0 ? dw.prog_f + (t - 1) : nullptr;
-    const int *below = b > 0 ? dw.prog_f + (t - ntx) : nullptr;
-    int seen_l = 0, seen_b = 0, peek_l = 0, peek_b = 0;
+    const bool xedge = ti == 0 && i > 0, yedge = tj == 0 && j > 0;               // reads a mailbox
+    const bool xout = ti == kWTX - 1 && a < ntx - 1, yout = tj == kWTY - 1 && b < dw.nty - 1;  // fills one
+    // 16-byte slots (value, pad) so the prefetch can be a cp.async.cg
+    double *const xin_box = dw.ex_f + 2 * (((long long)(t - 1) * dw.nz) * kWTY + tj);
+    double *const yin_box = dw.ey_f + 2 * (((long long)(t - ntx) * dw.nz) * kWTX + ti);
+    double *const xout_box = dw.ex_f + 2 * (((long long)t * dw.nz) * kWTY + tj);
+    double *const yout_box = dw.ey_f + 2 * (((long long)t * dw.nz) * kWTX + ti);
     const int nsteps = dw.nz + kWTX + kWTY - 2;
-    auto issue = [&](int s2) {  // this thread's copies for step s2
+    auto issue = [&](int s2) {  // this thread's own r / d for step s2
         const int k = s2 - ti - tj, q = s2 % D;
         const bool in = col_ok && k >= 0 && k < dw.nz;
         const long long o = base + pl * (in ? k : 0);
         cp_async8_ca(&ring_r[q][tid], r + o, in ? 8 : 0);
         cp_async8_ca(&ring_d[q][tid], d + o, in ? 8 : 0);
-        if (ti == 0 && i > 0) cp_async16_cg(&ring_x[q][tj], w + ((o - 1) & ~1ll), in ? 16 : 0);
-        if (tj == 0 && j > 0) cp_async16_cg(&ring_y[q][ti], w + ((o - dw.nx) & ~1ll), in ? 16 : 0);
-        cp_async_commit_grp();
+        if (in && xedge) cp_async16_cg(&ring_x[q][tj], xin_box + 2ll * k * kWTY);
+        if (in && yedge) cp_async16_cg(&ring_y[q][ti], yin_box + 2ll * k * kWTX);
     };
     double wk = 0.0;  // w at (i, j, k-1)
     for (int s = -(D - 1); s < nsteps; ++s) {
-        const int s2 = s + D - 1;  // the step whose copies are issued now
-        if (tid == 0 && s2 < nsteps) {
-            const bool f1 = wave_wait(left, min(s2 + kWTX, nsteps), seen_l, peek_l);
-            const bool f2 = wave_wait(below, min(s2 + kWTY, nsteps), seen_b, peek_b);
-            if (f1 || f2) fence_acq_rel_gpu();  // an accepted counter value acts as an acquire
-        }
         tile_sync<NT>();
-        if (s2 < nsteps) issue(s2);
-        else cp_async_commit_grp();  // keep one group per step
+        if (s + D - 1 < nsteps) issue(s + D - 1);
+        cp_async_commit_grp();  // one group per step (possibly empty)
         if (s < 0) continue;
         cp_async_wait_grp<D - 1>();  // step s's copies (this thread's) have landed
         const int k = s - ti - tj, q = s % D;
+        double xl = 0.0, yl = 0.0;
+        if (col_ok && k >= 0 && k < dw.nz) {
+            if (xedge) xl = edge_use(xin_box + 2ll * k * kWTY, ring_x[q][tj]);
+            if (yedge) yl = edge_use(yin_box + 2ll * k * kWTX, ring_y[q][ti]);
+        }
         double wv = 0.0;
         if (col_ok && k >= 0 && k < dw.nz) {
             const long long o = base + pl * k;
+            // both in-tile neighbours are read before any arithmetic (clamped
+            // indices, then selects) so the chain after the barrier is
+            // LDS -> DMUL -> DADD -> DADD -> DDIV; same operations, same order
+            const double ys = sm[s & 1][tj > 0 ? tj - 1 : 0][ti], xs = sm[s & 1][tj][ti > 0 ? ti - 1 : 0];
+            const double ym = tj > 0 ? ys : yl, xm = ti > 0 ? xs : xl;
+            const double pz = dw.lval * wk, py = dw.lval * ym, px = dw.lval * xm;
             double acc = ring_r[q][tid];
-            if (k > 0) acc = acc - dw.lval * wk;  // column i - pl
-            if (j > 0) {
-                double yl = 0.0;
-                if (tj == 0) {
-                    const double2 e = ring_y[q][ti];
-                    yl = ((o - dw.nx) & 1) ? e.y : e.x;
-                }
-                acc = acc - dw.lval * (tj > 0 ? sm[s & 1][tj - 1][ti] : yl);  // i - nx
-            }
-            if (i > 0) {
-                double xl = 0.0;
-                if (ti == 0) {
-                    const double2 e = ring_x[q][tj];
-                    xl = ((o - 1) & 1) ? e.y : e.x;
-                }
-                acc = acc - dw.lval * (ti > 0 ? sm[s & 1][tj][ti - 1] : xl);  // i - 1
-            }
+            acc = k > 0 ? acc - pz : acc;  // column i - pl
+            acc = j > 0 ? acc - py : acc;  // i - nx
+            acc = i > 0 ? acc - px : acc;  // i - 1
             wv = acc / ring_d[q][tid];
+            if (xout) edge_put(xout_box + 2ll * k * kWTY, wv);
+            if (yout) edge_put(yout_box + 2ll * k * kWTX, wv);
             w[o] = wv;
             wk = wv;
         }
         sm[(s + 1) & 1][tj][ti] = wv;
-        if ((s + 1) % dw.pub == 0 || s + 1 == nsteps) {
-            tile_sync<NT>();
-            if (tid == 0) st_release_gpu(dw.prog_f + t, s + 1);
-        }
     }
     cp_async_wait_grp<0>();
 }
@@ -371,7 +405,7 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd_p(DicWave dw, const d
     constexpr int NT = kWTX * kWTY;
     __shared__ double sm[2][kWTY][kWTX];
     __shared__ __align__(16) double ring_w[D][NT], ring_d[D][NT];
-    __shared__ __align__(16) double2 ring_x[D][kWTY], ring_y[D][kWTX];  // right / upper edge pairs
+    __shared__ __align__(16) double2 ring_x[D][kWTY], ring_y[D][kWTX];  // prefetched mailbox slots
     if (done && *done) return;
     const int ntx = dw.ntx, nty = dw.nty;
     const int t = ntx * nty - 1 - blockIdx.x, a = t % ntx, b = t / ntx;
@@ -380,10 +414,12 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd_p(DicWave dw, const d
     const bool col_ok = i < dw.nx && j < dw.ny;
     const long long pl = (long long)dw.nx * dw.ny;
     const long long base = (long long)i + (long long)dw.nx * j;
-    if (tid == 0) dw.prog_f[t] = 0;  // re-arm the next forward sweep's counters
-    const int *right = a < ntx - 1 ? dw.prog_b + (t + 1) : nullptr;
-    const int *above = b < nty - 1 ? dw.prog_b + (t + ntx) : nullptr;
-    int seen_r = 0, seen_a = 0, peek_r = 0, peek_a = 0;
+    const bool xedge = ti == kWTX - 1 && i < dw.nx - 1, yedge = tj == kWTY - 1 && j < dw.ny - 1;
+    const bool xout = ti == 0 && a > 0, yout = tj == 0 && b > 0;
+    double *const xin_box = dw.ex_b + 2 * (((long long)(t + 1) * dw.nz) * kWTY + tj);
+    double *const yin_box = dw.ey_b + 2 * (((long long)(t + ntx) * dw.nz) * kWTX + ti);
+    double *const xout_box = dw.ex_b + 2 * (((long long)t * dw.nz) * kWTY + tj);
+    double *const yout_box = dw.ey_b + 2 * (((long long)t * dw.nz) * kWTX + ti);
     const int nsteps = dw.nz + kWTX + kWTY - 2;
     const int ri = kWTX - 1 - ti, rj = kWTY - 1 - tj;
     auto issue = [&](int s2) {
@@ -392,54 +428,40 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd_p(DicWave dw, const d
         const long long o = base + pl * (in ? k : 0);
         cp_async8_ca(&ring_w[q][tid], w + o, in ? 8 : 0);  // written by the forward launch
         cp_async8_ca(&ring_d[q][tid], d + o, in ? 8 : 0);
-        if (ti == kWTX - 1 && i < dw.nx - 1) cp_async16_cg(&ring_x[q][tj], z + ((o + 1) & ~1ll), in ? 16 : 0);
-        if (tj == kWTY - 1 && j < dw.ny - 1) cp_async16_cg(&ring_y[q][ti], z + ((o + dw.nx) & ~1ll), in ? 16 : 0);
-        cp_async_commit_grp();
+        if (in && xedge) cp_async16_cg(&ring_x[q][tj], xin_box + 2ll * k * kWTY);
+        if (in && yedge) cp_async16_cg(&ring_y[q][ti], yin_box + 2ll * k * kWTX);
     };
     double zk = 0.0;  // z at (i, j, k+1)
     for (int s = -(D - 1); s < nsteps; ++s) {
-        const int s2 = s + D - 1;
-        if (tid == 0 && s2 < nsteps) {
-            const bool f1 = wave_wait(right, min(s2 + kWTX, nsteps), seen_r, peek_r);
-            const bool f2 = wave_wait(above, min(s2 + kWTY, nsteps), seen_a, peek_a);
-            if (f1 || f2) fence_acq_rel_gpu();
-        }
         tile_sync<NT>();
-        if (s2 < nsteps) issue(s2);
-        else cp_async_commit_grp();
+        if (s + D - 1 < nsteps) issue(s + D - 1);
+        cp_async_commit_grp();
         if (s < 0) continue;
         cp_async_wait_grp<D - 1>();
         const int k = dw.nz - 1 - (s - ri - rj), q = s % D;
+        double xr = 0.0, yu = 0.0;
+        if (col_ok && k >= 0 && k < dw.nz) {
+            if (xedge) xr = edge_use(xin_box + 2ll * k * kWTY, ring_x[q][tj]);
+            if (yedge) yu = edge_use(yin_box + 2ll * k * kWTX, ring_y[q][ti]);
+        }
         double zv = 0.0;
         if (col_ok && k >= 0 && k < dw.nz) {
             const long long o = base + pl * k;
+            const double xs = sm[s & 1][tj][ti < kWTX - 1 ? ti + 1 : ti];
+            const double ys = sm[s & 1][tj < kWTY - 1 ? tj + 1 : tj][ti];
+            const double xm = ti < kWTX - 1 ? xs : xr, ym = tj < kWTY - 1 ? ys : yu;
+            const double px = dw.uval * xm, py = dw.uval * ym, pz = dw.uval * zk;
             double acc = 0.0;
-            if (i < dw.nx - 1) {
-                double xr = 0.0;
-                if (ti == kWTX - 1) {
-                    const double2 e = ring_x[q][tj];
-                    xr = ((o + 1) & 1) ? e.y : e.x;
-                }
-                acc = acc + dw.uval * (ti < kWTX - 1 ? sm[s & 1][tj][ti + 1] : xr);
-            }
-            if (j < dw.ny - 1) {
-                double yu = 0.0;
-                if (tj == kWTY - 1) {
-                    const double2 e = ring_y[q][ti];
-                    yu = ((o + dw.nx) & 1) ? e.y : e.x;
-                }
-                acc = acc + dw.uval * (tj < kWTY - 1 ? sm[s & 1][tj + 1][ti] : yu);
-            }
-            if (k < dw.nz - 1) acc = acc + dw.uval * zk;
+            acc = i < dw.nx - 1 ? acc + px : acc;
+            acc = j < dw.ny - 1 ? acc + py : acc;
+            acc = k < dw.nz - 1 ? acc + pz : acc;
             zv = ring_w[q][tid] - acc / ring_d[q][tid];
+            if (xout) edge_put(xout_box + 2ll * k * kWTY, zv);
+            if (yout) edge_put(yout_box + 2ll * k * kWTX, zv);
             z[o] = zv;
             zk = zv;
         }
         sm[(s + 1) & 1][tj][ti] = zv;
-        if ((s + 1) % dw.pub == 0 || s + 1 == nsteps) {
-            tile_sync<NT>();
-            if (tid == 0) st_release_gpu(dw.prog_b + t, s + 1);
-        }
     }
     cp_async_wait_grp<0>();
 }
@@ -534,18 +556,36 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
         dw.prog_b = dw.prog_f + ntiles;
     }
     CF_CUDA(cudaMemsetAsync(dw.prog_f, 0, 2 * (size_t)ntiles * sizeof(int), s));
+    if (dw.shape == 0) {  // mailboxes of the pipelined 16 x 8 sweeps: x edges 8, y edges 16 slots per tile plane
+        const long long nbx = 2ll * ntiles * nz * 8, nby = 2ll * ntiles * nz * 16;  // 16-byte slots
+        if (!dw.ex_f) {
+            CF_CUDA(cudaMalloc(&dw.ex_f, 2 * (size_t)nbx * sizeof(double)));
+            CF_CUDA(cudaMalloc(&dw.ey_f, 2 * (size_t)nby * sizeof(double)));
+            dw.ex_b = dw.ex_f + nbx;
+            dw.ey_b = dw.ey_f + nby;
+        }
+        edge_arm<<<num_sms() * 4, 256, 0, s>>>(dw.ex_f, 2 * nbx);
+        edge_arm<<<num_sms() * 4, 256, 0, s>>>(dw.ey_f, 2 * nby);
+        CF_CHECK_LAUNCH("dic mailbox arm");
+    }
     dw.lval = vals[0];
     dw.uval = vals[1];
     dw.slack = 1;
     if (const char *e = std::getenv("CF_DIC_SLACK")) dw.slack = std::max(1, std::atoi(e));  // >= 1: edges are prefetched a step ahead
     dw.pub = 8;
-    if (const char *e = std::getenv("CF_DIC_PUBLISH")) dw.pub = std::max(1, std::atoi(e));
-    // pipelined sweeps, depth 2 (measured at 256^3: one-step prefetch 2.63 ms per
-    // DIC-PCG iteration, depth 2 2.43, 3 2.61, 4 2.74 -- the tiles mostly wait at
-    // the barrier for their neighbours' progress, and deeper rings widen the
-    // slack between tiles)
+    if (const char *e = std::getenv("CF_DIC_PUBLISH")) {  // rounded down to a power of two (a mask, not a modulo)
+        const int v = std::max(1, std::atoi(e));
+        dw.pub = 1;
+        while (dw.pub * 2 <= v && dw.pub < (1 << 29)) dw.pub *= 2;
+    }
+    // pipelined sweeps with mailbox edges, depth 2 (DIC-PCG per iteration,
+    // depth 2 / 3 / 4 / 6: 128^3 0.557 / 0.559 / 0.583 / 0.635 ms, 256^3 1.93 /
+    // 1.97 / 2.02 / 2.33 ms; the progress-counter form before it: 1.01 and 2.62)
     dw.depth = dw.shape == 0 ? 2 : 0;
-    if (const char *e = std::getenv("CF_DIC_DEPTH")) dw.depth = std::max(0, std::atoi(e));
+    if (const char *e = std::getenv("CF_DIC_DEPTH")) {
+        const int v = std::atoi(e);  // 0/1: one-step register prefetch; else a compiled ring depth
+        dw.depth = v <= 1 ? 0 : v >= 12 ? 12 : v >= 8 ? 8 : v >= 6 ? 6 : v;
+    }
     dw.ok = true;
     return CF_OK;
 }
@@ -555,18 +595,20 @@ int dic_wave_apply(const DicData &dd, const double *r, double *w, double *z, con
     const DicWave &dw = dd.wave;
     const int ntiles = dw.ntx * dw.nty;
     if (dw.shape == 0 && dw.depth >= 2) {
-        if (dw.depth == 2) {
-            dic_wave_fwd_p<16, 8, 2><<<ntiles, 128, 0, s>>>(dw, dd.d, r, w, done);
-            dic_wave_bwd_p<16, 8, 2><<<ntiles, 128, 0, s>>>(dw, dd.d, w, z, done);
-        } else if (dw.depth == 3) {
-            dic_wave_fwd_p<16, 8, 3><<<ntiles, 128, 0, s>>>(dw, dd.d, r, w, done);
-            dic_wave_bwd_p<16, 8, 3><<<ntiles, 128, 0, s>>>(dw, dd.d, w, z, done);
-        } else if (dw.depth == 4) {
-            dic_wave_fwd_p<16, 8, 4><<<ntiles, 128, 0, s>>>(dw, dd.d, r, w, done);
-            dic_wave_bwd_p<16, 8, 4><<<ntiles, 128, 0, s>>>(dw, dd.d, w, z, done);
-        } else {
-            dic_wave_fwd_p<16, 8, 6><<<ntiles, 128, 0, s>>>(dw, dd.d, r, w, done);
-            dic_wave_bwd_p<16, 8, 6><<<ntiles, 128, 0, s>>>(dw, dd.d, w, z, done);
+        switch (dw.depth) {
+#define CF_DIC_P(D)                                                                     \
+    case D:                                                                             \
+        dic_wave_fwd_p<16, 8, D><<<ntiles, 128, 0, s>>>(dw, dd.d, r, w, done);          \
+        dic_wave_bwd_p<16, 8, D><<<ntiles, 128, 0, s>>>(dw, dd.d, w, z, done);          \
+        break;
+            CF_DIC_P(2)
+            CF_DIC_P(3)
+            CF_DIC_P(4)
+            CF_DIC_P(6)
+            CF_DIC_P(8)
+            CF_DIC_P(12)
+#undef CF_DIC_P
+        default: return CF_EINVAL;
         }
         CF_CHECK_LAUNCH("dic wavefront sweeps (pipelined)");
         return CF_OK;
