@@ -496,7 +496,11 @@ __global__ void dic_wave_check(const int32_t *lp, const int32_t *lc, const doubl
     }
 }
 
-constexpr int kShapes[5][2] = {{16, 8}, {64, 4}, {128, 4}, {256, 2}, {8, 4}};
+// shapes 5-7 exist only in the pipelined mailbox form (CF_DIC_TILE=5/6/7; DIC-PCG
+// per iteration 128^3 / 256^3: 32x8 0.547 / 1.920 ms, 16x16 0.528 / 1.932, 32x16
+// 0.846 / 2.210, the default 16x8 0.557 / 1.929)
+constexpr int kShapes[8][2] = {{16, 8}, {64, 4}, {128, 4}, {256, 2}, {8, 4}, {32, 8}, {16, 16}, {32, 16}};
+static bool mailbox_shape(int shape) { return shape == 0 || shape >= 5; }
 
 static const void *wave_fwd_kernel(int shape)
 {
@@ -505,6 +509,9 @@ static const void *wave_fwd_kernel(int shape)
     case 1: return (const void *)dic_wave_fwd<64, 4>;
     case 2: return (const void *)dic_wave_fwd<128, 4>;
     case 3: return (const void *)dic_wave_fwd<256, 2>;
+    case 5: return (const void *)dic_wave_fwd_p<32, 8, 2>;
+    case 6: return (const void *)dic_wave_fwd_p<16, 16, 2>;
+    case 7: return (const void *)dic_wave_fwd_p<32, 16, 2>;
     default: return (const void *)dic_wave_fwd<8, 4>;
     }
 }
@@ -522,7 +529,7 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
     // 128x4 1.45, 256x2 2.12, a one-warp 8x4 1.68): wider tiles pay more per
     // block barrier than they save in progress handoffs
     dw.shape = 0;
-    if (const char *e = std::getenv("CF_DIC_TILE")) dw.shape = std::max(0, std::min(4, std::atoi(e)));
+    if (const char *e = std::getenv("CF_DIC_TILE")) dw.shape = std::max(0, std::min(7, std::atoi(e)));
     const int tx = kShapes[dw.shape][0], ty = kShapes[dw.shape][1];
     dw.ntx = (nx + tx - 1) / tx;
     dw.nty = (ny + ty - 1) / ty;
@@ -556,8 +563,8 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
         dw.prog_b = dw.prog_f + ntiles;
     }
     CF_CUDA(cudaMemsetAsync(dw.prog_f, 0, 2 * (size_t)ntiles * sizeof(int), s));
-    if (dw.shape == 0) {  // mailboxes of the pipelined 16 x 8 sweeps: x edges 8, y edges 16 slots per tile plane
-        const long long nbx = 2ll * ntiles * nz * 8, nby = 2ll * ntiles * nz * 16;  // 16-byte slots
+    if (mailbox_shape(dw.shape)) {  // mailboxes of the pipelined sweeps: x edges ty, y edges tx slots per tile plane
+        const long long nbx = 2ll * ntiles * nz * ty, nby = 2ll * ntiles * nz * tx;  // 16-byte slots
         if (!dw.ex_f) {
             CF_CUDA(cudaMalloc(&dw.ex_f, 2 * (size_t)nbx * sizeof(double)));
             CF_CUDA(cudaMalloc(&dw.ey_f, 2 * (size_t)nby * sizeof(double)));
@@ -581,7 +588,7 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
     // pipelined sweeps with mailbox edges, depth 2 (DIC-PCG per iteration,
     // depth 2 / 3 / 4 / 6: 128^3 0.557 / 0.559 / 0.583 / 0.635 ms, 256^3 1.93 /
     // 1.97 / 2.02 / 2.33 ms; the progress-counter form before it: 1.01 and 2.62)
-    dw.depth = dw.shape == 0 ? 2 : 0;
+    dw.depth = mailbox_shape(dw.shape) ? 2 : 0;
     if (const char *e = std::getenv("CF_DIC_DEPTH")) {
         const int v = std::atoi(e);  // 0/1: one-step register prefetch; else a compiled ring depth
         dw.depth = v <= 1 ? 0 : v >= 12 ? 12 : v >= 8 ? 8 : v >= 6 ? 6 : v;
@@ -594,6 +601,16 @@ int dic_wave_apply(const DicData &dd, const double *r, double *w, double *z, con
 {
     const DicWave &dw = dd.wave;
     const int ntiles = dw.ntx * dw.nty;
+    if (dw.shape >= 5) {  // wider / taller tiles, depth 2
+        if (dw.shape == 5) dic_wave_fwd_p<32, 8, 2><<<ntiles, 256, 0, s>>>(dw, dd.d, r, w, done);
+        if (dw.shape == 6) dic_wave_fwd_p<16, 16, 2><<<ntiles, 256, 0, s>>>(dw, dd.d, r, w, done);
+        if (dw.shape == 7) dic_wave_fwd_p<32, 16, 2><<<ntiles, 512, 0, s>>>(dw, dd.d, r, w, done);
+        if (dw.shape == 5) dic_wave_bwd_p<32, 8, 2><<<ntiles, 256, 0, s>>>(dw, dd.d, w, z, done);
+        if (dw.shape == 6) dic_wave_bwd_p<16, 16, 2><<<ntiles, 256, 0, s>>>(dw, dd.d, w, z, done);
+        if (dw.shape == 7) dic_wave_bwd_p<32, 16, 2><<<ntiles, 512, 0, s>>>(dw, dd.d, w, z, done);
+        CF_CHECK_LAUNCH("dic wavefront sweeps (pipelined, wide tiles)");
+        return CF_OK;
+    }
     if (dw.shape == 0 && dw.depth >= 2) {
         switch (dw.depth) {
 #define CF_DIC_P(D)                                                                     \
