@@ -414,6 +414,34 @@ def advect(u, v, w, n: int, h: float, dt: float, threads: int = 1):
     return nu, nv, nw
 
 
+_LATTICE = ((0.0, 0.5, 0.5), (0.5, 0.0, 0.5), (0.5, 0.5, 0.0))
+
+
+def _trilinear(arr, a, b, c):
+    """src/grid.py:102-121 -- clamp to the lattice hull, then lerp x, y, z."""
+    na, nb, nc = arr.shape
+    a = min(max(a, 0.0), na - 1.0)
+    b = min(max(b, 0.0), nb - 1.0)
+    c = min(max(c, 0.0), nc - 1.0)
+    i0, j0, k0 = min(int(a), max(na - 2, 0)), min(int(b), max(nb - 2, 0)), min(int(c), max(nc - 2, 0))
+    i1, j1, k1 = min(i0 + 1, na - 1), min(j0 + 1, nb - 1), min(k0 + 1, nc - 1)
+    fa, fb, fc = a - i0, b - j0, c - k0
+
+    def lx(j, k):
+        return arr[i0, j, k] * (1.0 - fa) + arr[i1, j, k] * fa
+
+    return (lx(j0, k0) * (1.0 - fb) + lx(j1, k0) * fb) * (1.0 - fc) + (lx(j0, k1) * (1.0 - fb) + lx(j1, k1) * fb) * fc
+
+
+def sample_velocity(u, v, w, h: float, point) -> np.ndarray:
+    """src/grid.py:124-142 -- each component on its own face lattice."""
+    p = np.asarray(point, dtype=np.float64)
+    if p.shape != (3,) or not np.all(np.isfinite(p)):
+        raise ValueError(f"bad sample point {p!r}")
+    return np.array([_trilinear(arr, p[0] / h - o[0], p[1] / h - o[1], p[2] / h - o[2])
+                     for arr, o in zip((u, v, w), _LATTICE)])
+
+
 def divergence(u, v, w, h: float, threads: int = 1) -> np.ndarray:
     """src/grid.py:145-154 -- flat, i fastest."""
     nx, ny, nz = u.shape[0] - 1, u.shape[1], u.shape[2]

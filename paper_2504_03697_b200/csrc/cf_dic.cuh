@@ -24,6 +24,8 @@ struct DicWave {
     int shape = 0;                             // tile shape (cf_dic_wave.cu kShapes)
     int depth = 0;                             // cp.async pipeline depth of the 16x8 sweeps (0: one-step prefetch)
     int *prog_f = nullptr, *prog_b = nullptr;  // per-tile progress of the two sweeps
+    int *ticket = nullptr;                     // [2] CTA tickets of the two sweeps (tile order)
+    long long prog_cap = 0, ex_cap = 0, ey_cap = 0;  // allocated ints / doubles (re-sized per setup)
     // edge mailboxes of the pipelined 16x8 sweeps: a tile's boundary values
     // for its neighbour, [tile][k][lane], armed with kEdgeEmpty; the reader
     // spins on the value itself and re-arms it (cf_dic_wave.cu)

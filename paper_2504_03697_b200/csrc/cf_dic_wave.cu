@@ -60,8 +60,23 @@ __device__ __forceinline__ void st_release_gpu(int *p, int v)
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Forward sweep (L + D~) w = r.  blockIdx -> tile in increasing (a, b), so a
-// CTA only ever waits for lower-numbered CTAs.
+// Tile numbers come from an atomic ticket taken at CTA start, not from
+// blockIdx: a CTA only waits on lower tickets, whose owners have already
+// started (are resident), whatever order the hardware dispatches CTAs in.
+// Each sweep re-arms the other sweep's counter (they alternate on one stream).
+__device__ __forceinline__ int wave_ticket(int *mine, int *other)
+{
+    __shared__ int tk;
+    if (threadIdx.x == 0) {
+        tk = atomicAdd(mine, 1);
+        *other = 0;
+    }
+    __syncthreads();
+    return tk;
+}
+
+// Forward sweep (L + D~) w = r.  Tickets -> tiles in increasing (a, b), so a
+// CTA only ever waits for lower-numbered (earlier-started) CTAs.
 template <int kWTX, int kWTY>
 __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd(DicWave dw, const double *__restrict__ d,
                                                           const double *__restrict__ r, double *__restrict__ w,
@@ -70,7 +85,7 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd(DicWave dw, const dou
     __shared__ double sm[2][kWTY][kWTX];
     if (done && *done) return;
     const int ntx = dw.ntx;
-    const int t = blockIdx.x, a = t % ntx, b = t / ntx;
+    const int t = wave_ticket(dw.ticket, dw.ticket + 1), a = t % ntx, b = t / ntx;
     const int ti = threadIdx.x % kWTX, tj = threadIdx.x / kWTX;
     const int i = a * kWTX + ti, j = b * kWTY + tj;
     const bool col_ok = i < dw.nx && j < dw.ny;
@@ -172,7 +187,7 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd(DicWave dw, const dou
     __shared__ double sm[2][kWTY][kWTX];
     if (done && *done) return;
     const int ntx = dw.ntx, nty = dw.nty;
-    const int t = ntx * nty - 1 - blockIdx.x, a = t % ntx, b = t / ntx;
+    const int t = ntx * nty - 1 - wave_ticket(dw.ticket + 1, dw.ticket), a = t % ntx, b = t / ntx;
     const int ti = threadIdx.x % kWTX, tj = threadIdx.x / kWTX;
     const int i = a * kWTX + ti, j = b * kWTY + tj;
     const bool col_ok = i < dw.nx && j < dw.ny;
@@ -337,7 +352,7 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd_p(DicWave dw, const d
     __shared__ __align__(16) double2 ring_x[D][kWTY], ring_y[D][kWTX];  // prefetched mailbox slots
     if (done && *done) return;
     const int ntx = dw.ntx;
-    const int t = blockIdx.x, a = t % ntx, b = t / ntx;
+    const int t = wave_ticket(dw.ticket, dw.ticket + 1), a = t % ntx, b = t / ntx;
     const int tid = threadIdx.x, ti = tid % kWTX, tj = tid / kWTX;
     const int i = a * kWTX + ti, j = b * kWTY + tj;
     const bool col_ok = i < dw.nx && j < dw.ny;
@@ -408,7 +423,7 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd_p(DicWave dw, const d
     __shared__ __align__(16) double2 ring_x[D][kWTY], ring_y[D][kWTX];  // prefetched mailbox slots
     if (done && *done) return;
     const int ntx = dw.ntx, nty = dw.nty;
-    const int t = ntx * nty - 1 - blockIdx.x, a = t % ntx, b = t / ntx;
+    const int t = ntx * nty - 1 - wave_ticket(dw.ticket + 1, dw.ticket), a = t % ntx, b = t / ntx;
     const int tid = threadIdx.x, ti = tid % kWTX, tj = tid / kWTX;
     const int i = a * kWTX + ti, j = b * kWTY + tj;
     const bool col_ok = i < dw.nx && j < dw.ny;
@@ -502,18 +517,59 @@ __global__ void dic_wave_check(const int32_t *lp, const int32_t *lc, const doubl
 constexpr int kShapes[8][2] = {{16, 8}, {64, 4}, {128, 4}, {256, 2}, {8, 4}, {32, 8}, {16, 16}, {32, 16}};
 static bool mailbox_shape(int shape) { return shape == 0 || shape >= 5; }
 
-static const void *wave_fwd_kernel(int shape)
+// The exact (forward, backward) kernels and block size dic_wave_apply launches
+// for a tile shape and ring depth (the residency check must see these).
+struct WaveKernels {
+    const void *fwd, *bwd;
+    int threads;
+};
+
+static WaveKernels wave_kernels(int shape, int depth)
 {
-    switch (shape) {
-    case 0: return (const void *)dic_wave_fwd<16, 8>;
-    case 1: return (const void *)dic_wave_fwd<64, 4>;
-    case 2: return (const void *)dic_wave_fwd<128, 4>;
-    case 3: return (const void *)dic_wave_fwd<256, 2>;
-    case 5: return (const void *)dic_wave_fwd_p<32, 8, 2>;
-    case 6: return (const void *)dic_wave_fwd_p<16, 16, 2>;
-    case 7: return (const void *)dic_wave_fwd_p<32, 16, 2>;
-    default: return (const void *)dic_wave_fwd<8, 4>;
+    if (shape == 0 && depth >= 2) {
+        switch (depth) {
+        case 2: return {(const void *)dic_wave_fwd_p<16, 8, 2>, (const void *)dic_wave_bwd_p<16, 8, 2>, 128};
+        case 3: return {(const void *)dic_wave_fwd_p<16, 8, 3>, (const void *)dic_wave_bwd_p<16, 8, 3>, 128};
+        case 4: return {(const void *)dic_wave_fwd_p<16, 8, 4>, (const void *)dic_wave_bwd_p<16, 8, 4>, 128};
+        case 6: return {(const void *)dic_wave_fwd_p<16, 8, 6>, (const void *)dic_wave_bwd_p<16, 8, 6>, 128};
+        case 8: return {(const void *)dic_wave_fwd_p<16, 8, 8>, (const void *)dic_wave_bwd_p<16, 8, 8>, 128};
+        default: return {(const void *)dic_wave_fwd_p<16, 8, 12>, (const void *)dic_wave_bwd_p<16, 8, 12>, 128};
+        }
     }
+    switch (shape) {
+    case 0: return {(const void *)dic_wave_fwd<16, 8>, (const void *)dic_wave_bwd<16, 8>, 128};
+    case 1: return {(const void *)dic_wave_fwd<64, 4>, (const void *)dic_wave_bwd<64, 4>, 256};
+    case 2: return {(const void *)dic_wave_fwd<128, 4>, (const void *)dic_wave_bwd<128, 4>, 512};
+    case 3: return {(const void *)dic_wave_fwd<256, 2>, (const void *)dic_wave_bwd<256, 2>, 512};
+    case 5: return {(const void *)dic_wave_fwd_p<32, 8, 2>, (const void *)dic_wave_bwd_p<32, 8, 2>, 256};
+    case 6: return {(const void *)dic_wave_fwd_p<16, 16, 2>, (const void *)dic_wave_bwd_p<16, 16, 2>, 256};
+    case 7: return {(const void *)dic_wave_fwd_p<32, 16, 2>, (const void *)dic_wave_bwd_p<32, 16, 2>, 512};
+    default: return {(const void *)dic_wave_fwd<8, 4>, (const void *)dic_wave_bwd<8, 4>, 32};
+    }
+}
+
+// a compiled ring depth of the 16x8 pipelined sweeps: 0/1 -> the one-step
+// register prefetch, otherwise the largest compiled depth <= v
+static int clamp_depth(int v)
+{
+    if (v <= 1) return 0;
+    static const int kDepths[] = {12, 8, 6, 4, 3, 2};
+    for (int d : kDepths)
+        if (v >= d) return d;
+    return 2;
+}
+
+// (re)allocate a device buffer to hold at least `need` elements
+template <typename T>
+static int ensure_buf(T *&p, long long &cap, long long need)
+{
+    if (p && cap >= need) return CF_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    CF_CUDA(cudaMalloc(&p, (size_t)need * sizeof(T)));
+    cap = need;
+    return CF_OK;
 }
 
 int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
@@ -534,10 +590,19 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
     dw.ntx = (nx + tx - 1) / tx;
     dw.nty = (ny + ty - 1) / ty;
     const int ntiles = dw.ntx * dw.nty;
-    // every CTA of a sweep must be resident (CTAs wait for lower-numbered ones)
-    int bpsm = 0;
-    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, wave_fwd_kernel(dw.shape), tx * ty, 0));
-    if ((long long)bpsm * num_sms() < ntiles) return CF_OK;
+    // ring depth of the pipelined sweeps, depth 2 (DIC-PCG per iteration,
+    // depth 2 / 3 / 4 / 6: 128^3 0.557 / 0.559 / 0.583 / 0.635 ms, 256^3 1.93 /
+    // 1.97 / 2.02 / 2.33 ms; the progress-counter form before it: 1.01 and 2.62)
+    dw.depth = mailbox_shape(dw.shape) ? 2 : 0;
+    if (dw.shape == 0)
+        if (const char *e = std::getenv("CF_DIC_DEPTH")) dw.depth = clamp_depth(std::atoi(e));
+    // every CTA of a sweep must be resident (a CTA waits on CTAs with lower
+    // tickets): check the exact forward and backward kernels apply launches
+    const WaveKernels wk = wave_kernels(dw.shape, dw.depth);
+    int bpf = 0, bpb = 0;
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpf, wk.fwd, wk.threads, 0));
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpb, wk.bwd, wk.threads, 0));
+    if ((long long)std::min(bpf, bpb) * num_sms() < ntiles) return CF_OK;
     // the off-diagonal values (the first lower / upper entry of the first row that has one)
     double vals[2] = {0.0, 0.0};
     int32_t p[2];
@@ -558,19 +623,22 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
     CF_CUDA(cudaStreamSynchronize(s));
     cudaFree(ok);
     if (!good) return CF_OK;
-    if (!dw.prog_f) {
-        CF_CUDA(cudaMalloc(&dw.prog_f, 2 * (size_t)ntiles * sizeof(int)));
-        dw.prog_b = dw.prog_f + ntiles;
+    // progress counters of both sweeps + the two ticket counters; sized per
+    // setup (a later attach with another tile shape or grid re-sizes them)
+    {
+        const int rc = ensure_buf(dw.prog_f, dw.prog_cap, 2ll * ntiles + 2);
+        if (rc != CF_OK) return rc;
     }
-    CF_CUDA(cudaMemsetAsync(dw.prog_f, 0, 2 * (size_t)ntiles * sizeof(int), s));
+    dw.prog_b = dw.prog_f + ntiles;
+    dw.ticket = dw.prog_f + 2 * ntiles;
+    CF_CUDA(cudaMemsetAsync(dw.prog_f, 0, (2 * (size_t)ntiles + 2) * sizeof(int), s));
     if (mailbox_shape(dw.shape)) {  // mailboxes of the pipelined sweeps: x edges ty, y edges tx slots per tile plane
         const long long nbx = 2ll * ntiles * nz * ty, nby = 2ll * ntiles * nz * tx;  // 16-byte slots
-        if (!dw.ex_f) {
-            CF_CUDA(cudaMalloc(&dw.ex_f, 2 * (size_t)nbx * sizeof(double)));
-            CF_CUDA(cudaMalloc(&dw.ey_f, 2 * (size_t)nby * sizeof(double)));
-            dw.ex_b = dw.ex_f + nbx;
-            dw.ey_b = dw.ey_f + nby;
-        }
+        int rc = ensure_buf(dw.ex_f, dw.ex_cap, 2 * nbx);
+        if (rc == CF_OK) rc = ensure_buf(dw.ey_f, dw.ey_cap, 2 * nby);
+        if (rc != CF_OK) return rc;
+        dw.ex_b = dw.ex_f + nbx;
+        dw.ey_b = dw.ey_f + nby;
         edge_arm<<<num_sms() * 4, 256, 0, s>>>(dw.ex_f, 2 * nbx);
         edge_arm<<<num_sms() * 4, 256, 0, s>>>(dw.ey_f, 2 * nby);
         CF_CHECK_LAUNCH("dic mailbox arm");
@@ -585,14 +653,9 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
         dw.pub = 1;
         while (dw.pub * 2 <= v && dw.pub < (1 << 29)) dw.pub *= 2;
     }
-    // pipelined sweeps with mailbox edges, depth 2 (DIC-PCG per iteration,
-    // depth 2 / 3 / 4 / 6: 128^3 0.557 / 0.559 / 0.583 / 0.635 ms, 256^3 1.93 /
-    // 1.97 / 2.02 / 2.33 ms; the progress-counter form before it: 1.01 and 2.62)
-    dw.depth = mailbox_shape(dw.shape) ? 2 : 0;
-    if (const char *e = std::getenv("CF_DIC_DEPTH")) {
-        const int v = std::atoi(e);  // 0/1: one-step register prefetch; else a compiled ring depth
-        dw.depth = v <= 1 ? 0 : v >= 12 ? 12 : v >= 8 ? 8 : v >= 6 ? 6 : v;
-    }
+    // the counters and armed mailboxes must be in place before any sweep
+    // runs, on whatever stream the solve later uses
+    CF_CUDA(cudaStreamSynchronize(s));
     dw.ok = true;
     return CF_OK;
 }
@@ -625,7 +688,7 @@ int dic_wave_apply(const DicData &dd, const double *r, double *w, double *z, con
             CF_DIC_P(8)
             CF_DIC_P(12)
 #undef CF_DIC_P
-        default: return CF_EINVAL;
+        default: CF_REQUIRE(false, "dic wavefront: ring depth not compiled");
         }
         CF_CHECK_LAUNCH("dic wavefront sweeps (pipelined)");
         return CF_OK;

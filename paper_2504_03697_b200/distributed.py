@@ -35,6 +35,17 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+
+def _slab_precond(precond) -> int:
+    """The z-slab CG runs Jacobi or no preconditioner; DIC does not shard
+    (SURVEY.md §8(e)), so it is rejected instead of silently dropped."""
+    if precond == "jacobi":
+        return _lib.PRECOND_JACOBI
+    if precond is None or precond == "none":
+        return _lib.PRECOND_NONE
+    raise ValueError(f"the z-slab CG supports precond 'jacobi' or None, got {precond!r}")
+
+
 class SlabCG:
     """CG over the z-slabs [bounds[k], bounds[k+1]) owned by this process."""
 
@@ -70,7 +81,7 @@ class SlabCG:
         xs = [torch.empty_like(b) for b in bs]
         bp = (ctypes.c_void_p * ns)(*(b.data_ptr() for b in bs))
         xp = (ctypes.c_void_p * ns)(*(x.data_ptr() for x in xs))
-        pk = _lib.PRECOND_JACOBI if precond == "jacobi" else _lib.PRECOND_NONE
+        pk = _slab_precond(precond)
         its = ctypes.c_int64()
         res = ctypes.c_double()
         rc = lib.cf_dcg_solve(self._h, bp, xp, float(tol), int(max_iter), pk, ctypes.byref(its), ctypes.byref(res),
@@ -160,7 +171,7 @@ class PeerSlabCG:
         xs = [torch.empty_like(b) for b in bs]
         bp = (ctypes.c_void_p * ns)(*(b.data_ptr() for b in bs))
         xp = (ctypes.c_void_p * ns)(*(x.data_ptr() for x in xs))
-        pk = _lib.PRECOND_JACOBI if precond == "jacobi" else _lib.PRECOND_NONE
+        pk = _slab_precond(precond)
         its = ctypes.c_int64()
         res = ctypes.c_double()
         rc = lib.cf_pcg_solve(self._h, bp, xp, float(tol), int(max_iter), pk, ctypes.byref(its), ctypes.byref(res),

@@ -147,7 +147,6 @@ class DicPreconditioner:
             raise ValueError(f"DIC breakdown at row {int(bad[0])}: modified diagonal {d!r} <= 0 "
                              "(matrix not SPD or pattern pathological)")
         _lib.check(rc, "dic factor")
-        self._ws_bound = set()
 
     def _args(self):
         return (*(t.data_ptr() for t in self._lower), *(t.data_ptr() for t in self._upper),
@@ -176,9 +175,12 @@ class DicPreconditioner:
         import ctypes
 
         lib = _lib.load_library()
-        if id(ws) not in self._ws_bound:
+        # the workspace holds raw pointers to the bound factor: rebind whenever
+        # another preconditioner was bound last, and keep this one alive while
+        # the workspace points at it
+        if getattr(ws, "_dic_owner", None) is not self:
             _lib.check(lib.cf_cg_set_dic(ws._h, *self._args()), "cf_cg_set_dic")
-            self._ws_bound.add(id(ws))
+            ws._dic_owner = self
         return lib.cf_cg_solve(ws._h, b.data_ptr(), x.data_ptr(), _lib.ptr(x0), float(tol), int(max_iter),
                                _lib.PRECOND_DIC, None, ctypes.byref(its), ctypes.byref(res), _lib.stream())
 

@@ -46,3 +46,37 @@ def cuda():
 
     cf.load_library()
     return cf
+
+
+_ACHIEVED = []
+
+
+@pytest.fixture
+def achieved(request):
+    """Record an achieved parity error (printed in the terminal summary and
+    written to gpurun_out/parity_achieved.json, so a drift inside a tolerance
+    band is visible run to run)."""
+
+    def rec(what: str, **vals):
+        _ACHIEVED.append({"test": request.node.nodeid, "what": what, **vals})
+
+    return rec
+
+
+def pytest_terminal_summary(terminalreporter):
+    if not _ACHIEVED:
+        return
+    import json
+
+    terminalreporter.write_sep("-", "achieved parity (GPU vs oracle / reference fixtures)")
+    for r in _ACHIEVED:
+        vals = " ".join(f"{k}={v:.2e}" if isinstance(v, float) else f"{k}={v}" for k, v in r.items()
+                        if k not in ("test", "what"))
+        terminalreporter.write_line(f"{r['what']}: {vals}")
+    out = os.path.join(ROOT, "gpurun_out")
+    try:
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, "parity_achieved.json"), "w") as f:
+            json.dump(_ACHIEVED, f, indent=1)
+    except OSError:
+        pass

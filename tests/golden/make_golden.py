@@ -272,10 +272,42 @@ def profiling_fixtures():
     print("wrote", path)
 
 
+def grid_fixtures():
+    """sample_velocity (src/grid.py:124-142) on seeded random fields: points
+    inside the domain, on lattice nodes, on the walls and far outside (the
+    clamp), at a cube with h != 1 and one with h = 1."""
+    from cavityflow import grid
+
+    out = {}
+    for tag, n, h, seed in (("a", 5, 0.4, 11), ("b", 8, 1.0, 12), ("c", 3, 0.7, 13)):
+        spec = grid.GridSpec(n, h)
+        f = grid.VelocityField(spec)
+        rng = np.random.default_rng(seed)
+        f.u[:] = rng.standard_normal(f.u.shape)
+        f.v[:] = rng.standard_normal(f.v.shape)
+        f.w[:] = rng.standard_normal(f.w.shape)
+        L = spec.side_length
+        pts = [rng.random(3) * L for _ in range(40)]
+        pts += [rng.uniform(-0.5 * L, 1.5 * L, 3) for _ in range(20)]  # partly outside: clamped
+        pts += [np.array([i * h, (j + 0.5) * h, (k + 0.5) * h]) for i, j, k in ((0, 0, 0), (n, n - 1, n - 1), (2, 1, 0))]
+        pts += [np.array([0.0, 0.0, 0.0]), np.array([L, L, L]), np.array([1e6, -1e6, 0.5 * L])]
+        pts = np.array(pts)
+        out[f"{tag}_n"], out[f"{tag}_h"] = np.int64(n), np.float64(h)
+        out[f"{tag}_u"], out[f"{tag}_v"], out[f"{tag}_w"] = f.u.copy(), f.v.copy(), f.w.copy()
+        out[f"{tag}_pts"] = pts
+        out[f"{tag}_samples"] = np.array([grid.sample_velocity(f, p) for p in pts])
+    save("grid.npz", **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[f"{name}_fixtures"]()
+        sys.exit(0)
     profiling_fixtures()
     snapshot_fixtures()
     sparse_fixtures()
     advection_fixtures()
     cavity_fixtures()
     pcg_fixtures()
+    grid_fixtures()

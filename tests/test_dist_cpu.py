@@ -172,3 +172,17 @@ def test_gloo_slab_cg_matches_single_domain(world):
                      max_iter=5000)
     assert abs(its.pop() - so.iterations) <= 2
     assert np.linalg.norm(x - xo) / np.linalg.norm(xo) <= 1e-10
+
+
+def test_slab_precond_validation():
+    """The z-slab CG accepts only Jacobi or no preconditioner (DIC does not
+    shard); anything else is a ValueError, not a silent
+    unpreconditioned solve."""
+    from paper_2504_03697_b200 import _lib, distributed
+
+    assert distributed._slab_precond("jacobi") == _lib.PRECOND_JACOBI
+    assert distributed._slab_precond(None) == _lib.PRECOND_NONE
+    assert distributed._slab_precond("none") == _lib.PRECOND_NONE
+    for bad in ("dic", "Jacobi", 3):
+        with pytest.raises(ValueError, match="z-slab CG"):
+            distributed._slab_precond(bad)

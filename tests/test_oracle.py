@@ -227,3 +227,13 @@ def test_box_restatement_consistency(golden):
     assert st.u.shape == (10, 5, 7) and st.p.shape == (9 * 5 * 7,)
     for res in results:
         assert res.solve.converged and res.div_post <= 1e-3 * res.div_pre
+
+
+def test_sample_velocity_matches_reference(golden):
+    """src/grid.py:124-142 on reference-sampled random fields (inside, lattice
+    nodes, walls, far outside): bit for bit."""
+    g = golden("grid")
+    for tag in "abc":
+        u, v, w, h = g[f"{tag}_u"], g[f"{tag}_v"], g[f"{tag}_w"], float(g[f"{tag}_h"])
+        got = np.array([orc.sample_velocity(u, v, w, h, p) for p in g[f"{tag}_pts"]])
+        assert np.array_equal(got, g[f"{tag}_samples"]), tag
