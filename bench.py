@@ -22,10 +22,19 @@ cpu_baseline: the oracle port (oracle/, the reference's algorithm in C with
           the reference's WorkerPool chunking) on a bounded sample: 256^3
           Jacobi PCG iterations with the symmetric SpMV, all host threads.
 --impl reference: that CPU path alone, as the driver's reference arm.
---gpus N > 1 (torchrun): z-slab decomposition, one slab per GPU, max over
-          ranks.  Default --scaling weak: the cavity extruded to 256x256x(256*N),
-          one 256^3 slab per GPU (value in 256^3-equivalent CG iterations/s);
-          --scaling strong: the 256^3 cube split over the GPUs.
+--gpus N > 1: z-slab decomposition, one slab per GPU, max over ranks.  Run
+          outside torchrun, bench.py re-executes itself under
+          torch.distributed.run (N ranks, 127.0.0.1).  Default --scaling weak:
+          the cavity extruded to 256x256x(256*N), one 256^3 slab per GPU (value
+          in 256^3-equivalent CG iterations/s); --scaling strong: the 256^3
+          cube split over the GPUs.
+sub-records (each its own CUDA-event timed region after the main one):
+          config5 (512^3, BASELINE config 5; at N > 1 the cube split over the
+          ranks -> strong-scaling points), dic (the reference's default
+          baseline/DIC solver at 256^3), config4_as_written (nu=0.001, lid
+          velocity 1, no-slip); --no-extra skips them.
+roofline.traffic: DRAM bytes per CG iteration from the newest committed ncu
+          summary (profiles/ncu_cg_r*.json, named in traffic_source).
 """
 
 from __future__ import annotations
@@ -173,15 +182,16 @@ def run_reference(args, rank):
 
 
 def load_traffic():
-    """Per-iteration DRAM bytes of the fused CG kernels from the committed ncu summary."""
+    """Per-iteration DRAM bytes of the fused CG kernels from the newest committed
+    ncu summary (ncu cannot run inside the timed bench): (bytes, source path)."""
     import glob
     found = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_cg_r*.json")))
     path = found[-1] if found else os.path.join(ROOT, "profiles", "ncu_cg_r01.json")
     try:
         with open(path) as f:
-            return json.load(f).get("dram_bytes_per_iteration")
+            return json.load(f).get("dram_bytes_per_iteration"), os.path.relpath(path, ROOT)
     except Exception:
-        return None
+        return None, None
 
 
 def run_ours(args, rank, world, local_rank):
@@ -271,7 +281,7 @@ def run_ours(args, rank, world, local_rank):
     alg_bytes = 88 * cells
     iter_s = (loop_ms / 1e3) / max(sum(its), 1)
     achieved = alg_bytes / iter_s / 1e9
-    traffic = load_traffic()
+    traffic, traffic_src = load_traffic()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -287,7 +297,7 @@ def run_ours(args, rank, world, local_rank):
         "fused_iter_gbs": achieved,
         "fused_iter_frac": achieved / peak,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": "fused CG iteration (cg_dir_lean2 + cg_update_tma; x updated every 2nd iteration)",
                      "algorithmic_bytes_per_iteration": alg_bytes, "design_bytes_per_iteration": 60 * cells,
                      # the same iteration time against the bytes this design moves (60 N) and
@@ -300,6 +310,10 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
+    if not args.no_extra:
+        del state, cache, pinned, phys
+        torch.cuda.empty_cache()
+        line.update(extra_records(args))
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         v, dt, k = cpu_baseline(n, args.cpu_iters, threads)
@@ -307,6 +321,82 @@ def run_ours(args, rank, world, local_rank):
                                 "sample": f"{n}^3 Jacobi-PCG, {k} iterations ({dt:.1f} s), oracle port"}
     print(json.dumps(line))
     return 0
+
+
+# ---------------------------------------------------------------- sub-records
+
+
+def _timed_steps(step, steps, warmup):
+    """Device time (CUDA events, synchronised both sides) of `steps` calls
+    after `warmup` untimed ones; returns (ms, [StepStats])."""
+    import torch
+
+    for _ in range(warmup):
+        step()
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    out = [step() for _ in range(steps)]
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b), out
+
+
+def _cavity_record(cfg, steps, warmup, note):
+    import torch
+
+    import paper_2504_03697_b200 as cf
+
+    st = cf.initial_state(cfg)
+    cache = cf.PoissonCache()
+    loop = []
+
+    def step():
+        s = cf.step(st, cfg, cache)
+        loop.append(cache.operator(cfg)._cg_ws.last_loop_ms)
+        return s
+
+    ms, out = _timed_steps(step, steps, warmup)
+    its = [s.solve.iterations for s in out]
+    loop_ms = sum(loop[-steps:])
+    rec = {"workload": note, "n": cfg.n, "dt": cfg.dt, "tol": cfg.tol, "preconditioner": cfg.preconditioner,
+           "variant": cfg.variant, "steps_timed": steps, "warmup": warmup, "ms_per_step": ms / steps,
+           "sim_steps_per_s": steps / (ms / 1e3), "cg_iterations": its,
+           "cg_iterations_per_s": sum(its) / (ms / 1e3),
+           "cg_ms_per_iteration": loop_ms / max(sum(its), 1), "converged": all(s.solve.converged for s in out)}
+    del st, cache
+    torch.cuda.empty_cache()
+    return rec
+
+
+def extra_records(args):
+    """Sub-records of the N=1 line (each its own timed region, CUDA events):
+    config5 -- BASELINE config 5's 512^3 cavity (h=1/512, dt=0.001, tol 1e-8),
+        reference physics, Jacobi: the single-GPU t_1 of the strong-scaling
+        curve (N > 1 lines carry the same cube split over the ranks);
+    dic -- the reference's DEFAULT solver (baseline variant, DIC preconditioner,
+        src/sim.py:65) on the config-4 cavity at 256^3;
+    config4_as_written -- config 4's physics as BASELINE states it
+        (nu = 0.001, lid velocity 1, no-slip, explicit diffusion)."""
+    import paper_2504_03697_b200 as cf
+
+    out = {}
+    n = args.grid
+    if args.config5_steps > 0:
+        cfg5 = cf.SimConfig(n=512, h=1.0 / 512, dt=0.001, t_end=1.0, tol=1e-8, max_iter=50000,
+                            variant="optimized", preconditioner="jacobi")
+        out["config5"] = _cavity_record(cfg5, args.config5_steps, 1,
+                                        "BASELINE config 5: 512^3 cavity, reference physics, 1 GPU")
+    base = dict(n=n, h=1.0 / n, dt=args.dt, t_end=1.0, tol=1e-8, max_iter=50000)
+    out["dic"] = _cavity_record(cf.SimConfig(variant="baseline", preconditioner="dic", **base), 2, 1,
+                                f"{n}^3 cavity (config 4 grid) with the reference's default solver: "
+                                "baseline variant, DIC preconditioner")
+    out["config4_as_written"] = _cavity_record(
+        cf.SimConfig(variant="optimized", preconditioner="jacobi", lid_accel=0.0, viscosity=0.001,
+                     lid_velocity=1.0, no_slip=True, initial_pressure=0.0, **base), 2, 1,
+        f"BASELINE config 4 as written: {n}^3, nu=0.001, lid velocity 1, no-slip, explicit diffusion")
+    return out
 
 
 def run_slabs(args, cfg, rank, world, local_rank, barrier):
@@ -387,6 +477,12 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
     e2e_value = norm * e2e_its / (float(t2[0]) / 1e3)
     bytes_in = sum(x.numel() * x.element_size() for x in phys[:3])
     bytes_out = sum(x.numel() * x.element_size() for x in phys)
+    clock_summary = clocks.summary()
+    c5 = None
+    if not args.no_extra and args.config5_steps > 0:
+        del sim, sl, phys, pinned
+        torch.cuda.empty_cache()
+        c5 = config5_slabs(args, rank, world, barrier)
     if rank != 0:
         return 0
     peak, peak_kind = peaks()
@@ -413,8 +509,80 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_in * world,
                 "d2h_bytes_per_step": bytes_out * world},
         "gpu_launches": sum(6 * i + 10 for i in its),
-        "clocks": clocks.summary(),
+        "clocks": clock_summary,
+        **({"config5": c5} if c5 else {}),
     }))
+    return 0
+
+
+def config5_slabs(args, rank, world, barrier):
+    """BASELINE config 5 (512^3, h=1/512, dt=0.001, tol 1e-8, reference
+    physics, Jacobi) as a strong-scaling point: the 512^3 cube split into
+    `world` z-slabs.  Against the N=1 line's config5 record (t_1) the driver's
+    SCALE runs give E(N) = t_1 / (N t_N).  Device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_03697_b200 as cf
+    from paper_2504_03697_b200.distributed import SlabSim
+    from paper_2504_03697_b200.parallel import SlabDecomposition
+
+    cfg = cf.SimConfig(n=512, h=1.0 / 512, dt=0.001, t_end=1.0, tol=1e-8, max_iter=50000,
+                       variant="optimized", preconditioner="jacobi")
+    dec = SlabDecomposition(512, 512, 512, world, rank)
+    sim = SlabSim(cfg, [dec.z0, dec.z1], distributed=True, collective=args.collective)
+    sim.step()
+    barrier()
+    stream = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    its, loop = [], 0.0
+    for _ in range(args.config5_steps):
+        its.append(sim.step().solve.iterations)
+        loop += sim.cg.last_loop_ms
+    b.record(stream)
+    barrier()
+    t = torch.tensor([a.elapsed_time(b), loop], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, loop_ms = float(t[0]), float(t[1])
+    del sim
+    torch.cuda.empty_cache()
+    return {"workload": f"BASELINE config 5: 512^3 cavity, reference physics, z-slab over {world} GPUs (strong)",
+            "n": 512, "dt": 0.001, "tol": 1e-8, "preconditioner": "jacobi", "steps_timed": args.config5_steps,
+            "warmup": 1, "ms_per_step": ms / args.config5_steps, "sim_steps_per_s": args.config5_steps / (ms / 1e3),
+            "cg_iterations": its, "cg_iterations_per_s": sum(its) / (ms / 1e3),
+            "cg_ms_per_iteration": loop_ms / max(sum(its), 1), "collective": args.collective}
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 outside torchrun: re-exec this script under
+    torch.distributed.run, one rank per GPU on this node (127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dry_run(args, rank, world) -> int:
+    """Plumbing check without a GPU: the rank layout bench.py would use, over
+    gloo, with one all-reduce (the timing reduction) across the ranks."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "world": world, "n_gpus": args.gpus, "max_rank_plus_1": float(t[0]),
+                          "impl": args.impl}))
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
@@ -429,16 +597,25 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=40)
     ap.add_argument("--ref-iters", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config5 / dic / config4_as_written sub-records")
+    ap.add_argument("--config5-steps", type=int, default=2, help="timed 512^3 steps of the config5 sub-record")
     ap.add_argument("--collective", choices=("p2p", "nccl"), default="p2p",
                     help="z-slab CG collectives (N > 1): fused peer-memory kernels, or NCCL calls")
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
                     help="N > 1: one n^3 slab per GPU (weak, default) or the n^3 cube split over the GPUs (strong)")
     ap.add_argument("--force-slabs", action="store_true",
                     help="run the z-slab/NCCL path even on one rank (plumbing check)")
+    ap.add_argument("--dry-run", action="store_true", help="rank plumbing only (gloo, no GPU work)")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        return dry_run(args, rank, world)
     if args.impl == "reference":
         return run_reference(args, rank)
     use_pg = world > 1 or args.force_slabs
