@@ -21,6 +21,7 @@
 // The iteration loop is a CUDA graph with a conditional WHILE node whose
 // condition is cleared on the device when the solve stops.
 #include <algorithm>
+#include <type_traits>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -264,6 +265,7 @@ __global__ void __launch_bounds__(kMarchThreads) cg_x_fixup(long long n, double 
 #include "cf_cg_pass.cuh"
 #include "cf_cg_lean.cuh"
 #include "cf_cg_lpass.cuh"
+#include "cf_cg_spass.cuh"
 #include "cf_cg_persist.cuh"
 
 // Host: single-reduction pass geometry (32 x 16 tiles; chunks of ~32 planes,
@@ -658,6 +660,12 @@ struct cf_cg {
     int pass_form = 1;  // 0 cg_pass_kernel, 1 / 2 cg_lpass_kernel with 8 / 16-row tiles (CF_PASS_FORM=old|lean|lean16)
     cf::PairGeom lpass_g{};
     double *r2 = nullptr;
+    // TMA-fed single-reduction pass (cf_cg_spass.cuh): one kernel per
+    // iteration, 40 N; r ping-pongs with r2, x updated every second pass
+    bool spass = false;
+    cf::SpGeom sp_g{};
+    int sp_ctas = 0;
+    CUtensorMap m_spr[2]{}, m_spp[2]{}, m_spx{};
     cudaGraphExec_t exec_pass[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaGraph_t graph_pass[4] = {nullptr, nullptr, nullptr, nullptr};
     double zc_pass[4] = {0, 0, 0, 0};
@@ -1008,6 +1016,109 @@ static int pass_solve(cf_cg *ws, const double *b, double zc, cudaStream_t s)
     return CF_OK;
 }
 
+// ---------------------------------------------------------------- TMA-fed single pass
+constexpr int kSpTY = 16, kSpS = 6;
+using SpCfg = Sp<kSpTY, kSpS>;
+
+template <int PK>
+static int spass_body_launch(cf_cg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond, int use_cond)
+{
+    for (int half = 0; half < 2; ++half) {
+        // half 0: r, p[0] -> r2, p[1], x skipped; half 1: r2, p[1] -> r, p[0], x for both passes
+        double *r_out = half ? ws->r : ws->r2;
+        if (half == 0)
+            cg_spass_kernel<PK, kSpTY, kSpS, false><<<ws->sp_ctas, SpCfg::Threads, SpCfg::Smem, s>>>(
+                ws->m_spr[0], ws->m_spp[0], ws->m_spx, ws->sp_g, ws->off, ws->diag, zc, r_out, ws->p[1], ws->x,
+                ws->sc, ws->partials, ws->tk, use_cond, cond);
+        else
+            cg_spass_kernel<PK, kSpTY, kSpS, true><<<ws->sp_ctas, SpCfg::Threads, SpCfg::Smem, s>>>(
+                ws->m_spr[1], ws->m_spp[1], ws->m_spx, ws->sp_g, ws->off, ws->diag, zc, r_out, ws->p[0], ws->x,
+                ws->sc, ws->partials, ws->tk, use_cond, cond);
+        CF_CHECK_LAUNCH("cg_spass_kernel");
+    }
+    return CF_OK;
+}
+
+template <int ORDER, int PK>
+static int spass_build_graph(cf_cg *ws, double zc)
+{
+    cudaGraph_t g;
+    CF_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle cond;
+    CF_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CF_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+    cudaStream_t cs;
+    CF_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CF_CUDA(cudaStreamBeginCaptureToGraph(cs, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeRelaxed));
+    int rc = spass_body_launch<PK>(ws, cs, zc, cond, 1);
+    cudaGraph_t captured;
+    cudaError_t e = cudaStreamEndCapture(cs, &captured);
+    cudaStreamDestroy(cs);
+    if (rc != CF_OK) return rc;
+    CF_CUDA(e);
+    {  // x += alpha p_k owed by a final skipping pass (odd iteration count), p_k in p[1]
+        cudaKernelNodeParams kp = {};
+        void *args[] = {&ws->n, &ws->x, &ws->p[1], &ws->sc};
+        kp.func = (void *)cg_x_fixup;
+        kp.gridDim = dim3(ws->grid_init);
+        kp.blockDim = dim3(kMarchThreads);
+        kp.kernelParams = args;
+        cudaGraphNode_t fix;
+        CF_CUDA(cudaGraphAddKernelNode(&fix, g, &node, 1, &kp));
+    }
+    cudaGraphExec_t exec;
+    CF_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    ws->graph_pass[PK] = g;
+    ws->exec_pass[PK] = exec;
+    ws->zc_pass[PK] = zc;
+    return CF_OK;
+}
+
+template <int ORDER, int PK>
+static int spass_solve(cf_cg *ws, const double *b, double zc, cudaStream_t s)
+{
+    // r = b, x = 0, |b|^2, gamma_0 = r.z, delta_0 = z.A z -> alpha_0 (cf_cg_pass.cuh)
+    cg_pass_init<ORDER, PK><<<ws->pg_upd.ctas(), kPairThreads, 0, s>>>(ws->pg_upd, ws->off, ws->diag, zc, b, ws->r,
+                                                                       ws->x, ws->sc, ws->partials, ws->tk);
+    CF_CHECK_LAUNCH("cg_pass_init");
+    if (ws->direct) {
+        CF_CUDA(cudaEventRecord(ws->ev0, s));
+        for (;;) {
+            for (int b2 = 0; b2 < ws->direct_batch; ++b2) {
+                int rc = spass_body_launch<PK>(ws, s, zc, 0, 0);
+                if (rc != CF_OK) return rc;
+            }
+            CF_CUDA(cudaMemcpyAsync(&ws->sc_host->done, &ws->sc->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CF_CUDA(cudaStreamSynchronize(s));
+            if (ws->sc_host->done) break;
+        }
+        cg_x_fixup<<<ws->grid_init, kMarchThreads, 0, s>>>(ws->n, ws->x, ws->p[1], ws->sc);
+        CF_CHECK_LAUNCH("cg_x_fixup");
+        CF_CUDA(cudaEventRecord(ws->ev1, s));
+        return CF_OK;
+    }
+    if (!ws->exec_pass[PK] || ws->zc_pass[PK] != zc) {
+        if (ws->exec_pass[PK]) {
+            cudaGraphExecDestroy(ws->exec_pass[PK]);
+            cudaGraphDestroy(ws->graph_pass[PK]);
+            ws->exec_pass[PK] = nullptr;
+        }
+        int rc = spass_build_graph<ORDER, PK>(ws, zc);
+        if (rc != CF_OK) return rc;
+    }
+    CF_CUDA(cudaEventRecord(ws->ev0, s));
+    CF_CUDA(cudaGraphLaunch(ws->exec_pass[PK], s));
+    CF_CUDA(cudaEventRecord(ws->ev1, s));
+    return CF_OK;
+}
+
 template <int ORDER, int PK>
 static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, cudaStream_t s)
 {
@@ -1035,6 +1146,9 @@ static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, c
         CF_CHECK_LAUNCH("cg_small_kernel");
         CF_CUDA(cudaEventRecord(ws->ev1, s));
         return CF_OK;
+    }
+    if ((PK == PK_NONE || PK == PK_JCONST) && ws->spass && !x0) {
+        if constexpr (PK == PK_NONE || PK == PK_JCONST) return spass_solve<ORDER, PK>(ws, b, zc, s);
     }
     if ((PK == PK_NONE || PK == PK_JCONST) && ws->pass && !x0) {
         if constexpr (PK == PK_NONE || PK == PK_JCONST) return pass_solve<ORDER, PK>(ws, b, zc, s);
@@ -1232,6 +1346,26 @@ static void set_grids(cf_cg *ws)
         }
         ws->lpass_g = lg;
     }
+    // TMA-fed single-reduction pass (cf_cg_spass.cuh): CF_CG_ALGO=spass
+    ws->spass = ws->tma && ws->bx.nx % 2 == 0 && algo && !strcmp(algo, "spass");
+    if (ws->spass) {
+        cudaFuncSetAttribute(cg_spass_kernel<PK_NONE, kSpTY, kSpS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpCfg::Smem);
+        cudaFuncSetAttribute(cg_spass_kernel<PK_NONE, kSpTY, kSpS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpCfg::Smem);
+        cudaFuncSetAttribute(cg_spass_kernel<PK_JCONST, kSpTY, kSpS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpCfg::Smem);
+        cudaFuncSetAttribute(cg_spass_kernel<PK_JCONST, kSpTY, kSpS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpCfg::Smem);
+        SpGeom g{ws->bx.nx, ws->bx.ny, ws->bx.nz, (ws->bx.nx + kSpTX - 1) / kSpTX, (ws->bx.ny + kSpTY - 1) / kSpTY, 1};
+        const int bps = blocks_per_sm((const void *)cg_spass_kernel<PK_JCONST, kSpTY, kSpS, true>, SpCfg::Threads,
+                                      SpCfg::Smem);
+        const long long slots = (long long)num_sms() * (bps > 0 ? bps : 1), tiles = (long long)g.ntx * g.nty;
+        // z-chunks: as many as fill the resident slots in one round, each >= 8 planes
+        long long c = std::max(1LL, std::min(slots / std::max(1LL, tiles), (long long)g.nz / 8));
+        if (const char *e = getenv("CF_SPASS_CHUNKS")) c = std::max(1, std::min(atoi(e), g.nz));
+        g.nchunk = (int)c;
+        const long long items = tiles * c, rounds = (items + slots - 1) / slots;
+        ws->sp_ctas = (int)((items + rounds - 1) / rounds);  // equal rounds for every CTA
+        ws->sp_g = g;
+        ws->spass = bps >= 1;
+    }
     if (const char *e = getenv("CF_CG_UPD_SKIP")) ws->kind_upd_skip = kern_kind("CF_CG_UPD_SKIP", ws->kind_upd, ws->tma, pair_ok);
     const char *dx = getenv("CF_CG_DEFER_X");
     ws->defer_x = ws->kind_upd != KK_LDG && !(dx && atoi(dx) == 0);
@@ -1285,6 +1419,7 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
     maxg = std::max(maxg, std::max(ws->pg_dir.ctas(), ws->pg_upd.ctas()));
     maxg = std::max(maxg, std::max(ws->lg_dir.ctas(), ws->lg_upd.ctas()));
     if (ws->pass) maxg = std::max(maxg, std::max(ws->pass_g.ctas(), ws->lpass_g.ctas()));
+    if (ws->spass) maxg = std::max(maxg, ws->sp_ctas);
     size_t vec = (size_t)ws->n * sizeof(double);
     cudaError_t e = cudaSuccess;
     // every CG vector carries kLeanPad zeroed doubles after its n cells (the
@@ -1295,8 +1430,8 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
         if (e == cudaSuccess) e = cudaMemsetAsync(reinterpret_cast<char *>(*b) + vec, 0, pad, cf::as_stream(stream));
     }
     if (e == cudaSuccess) e = cudaMalloc(&ws->partials, sizeof(double) * 3 * (size_t)maxg);
-    if (e == cudaSuccess && ws->pass) e = cudaMalloc(&ws->r2, vec + pad);
-    if (e == cudaSuccess && ws->pass)
+    if (e == cudaSuccess && (ws->pass || ws->spass)) e = cudaMalloc(&ws->r2, vec + pad);
+    if (e == cudaSuccess && (ws->pass || ws->spass))
         e = cudaMemsetAsync(reinterpret_cast<char *>(ws->r2) + vec, 0, pad, cf::as_stream(stream));
     if (e == cudaSuccess) e = cudaMalloc(&ws->sc, sizeof(cf::CgScalars));
     if (e == cudaSuccess) e = cudaMalloc(&ws->tk, sizeof(cf::CgTickets));
@@ -1311,6 +1446,18 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
         int rc = cf::cuda_fail(e, "cf_cg_create");
         cf_cg_destroy(ws);
         return rc;
+    }
+    if (ws->spass) {  // boxes of the single pass: 68 x (TY+4) halo boxes of r / p, 64 x TY interior box of x
+        const int nx = ws->bx.nx, ny = ws->bx.ny, nz = ws->bx.nz;
+        const int hy = cf::kSpTY + 4;
+        int pr = 256;
+        if (const char *e = getenv("CF_SPASS_PROMO")) pr = atoi(e);
+        auto mk = [&](CUtensorMap *m, const double *b, int bx, int by) {
+            return cf::make_map_promo(m, b, nx, ny, nz, bx, by, pr);
+        };
+        ws->spass = mk(&ws->m_spr[0], ws->r, cf::kSpBX, hy) && mk(&ws->m_spr[1], ws->r2, cf::kSpBX, hy) &&
+                    mk(&ws->m_spp[0], ws->p[0], cf::kSpBX, hy) && mk(&ws->m_spp[1], ws->p[1], cf::kSpBX, hy) &&
+                    mk(&ws->m_spx, ws->x, cf::kSpTX, cf::kSpTY);
     }
     if (ws->tma && !cf::build_maps(ws)) {  // TMA cannot describe the arrays: pair / LDG forms
         ws->tma = false;

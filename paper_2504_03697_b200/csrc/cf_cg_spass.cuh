@@ -1,0 +1,360 @@
+// cf_cg_spass.cuh -- the single-reduction CG iteration as ONE streaming pass
+// fed by TMA (included by cf_cg.cu inside namespace cf, after cf_cg_pass.cuh
+// for scalar_after_pass / cg_pass_init and cf_tma.cuh for the TMA helpers).
+//
+// Same recurrence as cg_pass_kernel (Chronopoulos-Gear, src/solver.py:128-171
+// rearranged so one grid reduction per iteration suffices):
+//   p_k     = z_k + beta_k p_{k-1}          (halo 2)
+//   q       = A p_k                          (halo 1)
+//   r_{k+1} = r_k - alpha_k q,  z' = M^-1 r_{k+1}   (halo 1)
+//   w       = A z'                           (tile)  -> r.r, gamma = r.z', delta = z'.w
+// with x updated every second pass, x_{k+1} = x_{k-1} + alpha_{k-1} p_{k-1} +
+// alpha_k p_k (p_{k-1} is read anyway).  HBM per iteration: read r_k,
+// p_{k-1}; write r_{k+1}, p_k; + x read/write every second pass = 40 N
+// (the two-kernel form moves 60 N, the reference's op sequence 88 N).
+//
+// Layout for few instructions and one block barrier per plane:
+//   * a CTA owns a 64 x TY tile and marches z; every plane of r_k and p_{k-1}
+//     arrives as ONE 68 x (TY+4) box per vector (x0-2 .. x0+65, y0-2 ..
+//     y0+TY+1) by TMA into an S-deep ring (a producer warp, full/empty
+//     mbarriers); ghosts outside the domain are zero-filled by the TMA unit
+//     (negative box origins work when the x origin is a 16-byte multiple:
+//     tools/tma_selftest.cu variants 6-10), so p = 0 there with no mask;
+//   * the stage is handed back to the producer as soon as the raw values are
+//     in registers; p_k and z' go to two double-buffered plane buffers (the
+//     ring sees TMA writes and generic reads only: no proxy fence per step);
+//   * warp w owns box row w (TY+4 row warps), lane l the cell pair
+//     x0+2l, x0+2l+1; the 2(TY+4) halo pairs at x0-2 and x0+64 belong to
+//     edge warps, which form p there and carry q / z' for the halo cell;
+//   * the stencils are split along z: A p at plane t collects its z-1 and
+//     in-plane terms when plane t is formed and its z+1 term one step later,
+//     so each thread keeps 5 pair registers (accumulators for q and w, the
+//     previous p and z', the raw r) instead of 3-plane windows;
+//   * step t: take stage t+2 (raw r, p_old, x) and release it; form p(t+2);
+//     finish q(t+1) -> r', z'(t+1); finish w(t) -> dots; barrier; in-plane
+//     terms of q(t+2) and of w(t+1).  A tile row's steady state (every plane
+//     condition true) is a separate instantiation of the step.
+//   * one CTA per SM walks (tile, z-chunk) items in lockstep with its
+//     neighbours (SpGeom); each item's march has 4 planes of fill.
+// The stencil sums follow the reference CSR column order (k-1, j-1, i-1, i,
+// i+1, j+1, k+1; src/sparse.py:194-201) with fused multiply-adds: the
+// single-reduction recurrence rounds differently from the reference anyway
+// (parity: iterations within +-2, solution within 1e-8; tests/test_gpu_parity.py).
+
+constexpr int kSpTX = 64;            // tile width (32 pairs)
+constexpr int kSpBX = kSpTX + 4;     // box width: x0-2 .. x0+65
+
+template <int TY, int S>
+struct Sp {
+    static_assert(TY % 4 == 0, "box bytes must stay 128-byte multiples");
+    static constexpr int Rows = TY + 4;                       // box rows y0-2 .. y0+TY+1
+    static constexpr int EdgeWarps = (2 * Rows + 31) / 32;    // halo pairs at x0-2 / x0+64
+    static constexpr int CWarps = Rows + EdgeWarps;           // consumer warps
+    static constexpr int Threads = 32 * (CWarps + 1);         // + the producer warp
+    static constexpr int BoxD = Rows * kSpBX;                 // doubles per box
+    static constexpr int XD = TY * kSpTX;                     // doubles per x box
+    static constexpr uint32_t BoxBytes = BoxD * 8, XBytes = XD * 8;
+    static constexpr int StageD = 2 * BoxD + XD;              // R | P | X (TMA writes only)
+    // + two p planes and two z' planes (double-buffered, generic writes only)
+    static constexpr size_t Smem = ((size_t)S * StageD + 4 * BoxD) * sizeof(double) + 128;
+};
+
+// Work items (tile, z-chunk), chunk-major: item j = chunk j / T, tile j % T
+// (T = ntx * nty).  CTA b takes items b, b + G, b + 2G, ... so the items in
+// flight at any time are neighbouring tiles on the same chunk, marching in
+// lockstep: the halo rows / columns a tile reads were fetched by its
+// neighbours moments earlier and come from L2 (measured at 256^3: 128
+// lockstep CTAs 157 us per iteration against 169 for 148 CTAs on equal
+// contiguous (tile, plane) ranges, whose neighbours ran tens of planes apart).
+struct SpGeom {
+    int nx, ny, nz, ntx, nty, nchunk;
+    __host__ __device__ int items() const { return ntx * nty * nchunk; }
+};
+
+__device__ __forceinline__ double2 sp_lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+__device__ __forceinline__ void sp_sts2(double *p, double2 v) { *reinterpret_cast<double2 *>(p) = v; }
+__device__ __forceinline__ void sp_stg2(double *p, double2 v) { *reinterpret_cast<double2 *>(p) = v; }
+__device__ __forceinline__ void sp_bar(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
+
+template <int PK>
+__device__ __forceinline__ double sp_z(double r, double zc) { return PK == PK_JCONST ? r * zc : r; }
+
+// p = M^-1 r + beta p_old (src/precond.py:94, src/solver.py:169; p = z first, :142)
+template <int PK, bool FIRST>
+__device__ __forceinline__ double sp_form(double r, double po, double zc, double beta)
+{
+    const double z = sp_z<PK>(r, zc);
+    return FIRST ? z : __fma_rn(beta, po, z);
+}
+
+// The march of one CTA.  Consumers return their partial rr / gamma / delta.
+template <int PK, int TY, int S, bool FIRST, bool XDBL>
+__device__ __forceinline__ void spass_body(const CUtensorMap *mr, const CUtensorMap *mp, const CUtensorMap *mx,
+                                           const SpGeom &g, double off, double diag, double zc,
+                                           double *__restrict__ r_out, double *__restrict__ p_new,
+                                           double *__restrict__ x, double alpha, double alpha_prev, double beta,
+                                           double *ring, uint64_t *full, uint64_t *empty, double &rr, double &gam,
+                                           double &dlt)
+{
+    using G = Sp<TY, S>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long plane = (long long)g.nx * g.ny;
+    const double malpha = -alpha;
+
+    if (warp == G::CWarps) {  // ---------------- producer: one lane drives the ring
+        if (lane != 0) return;
+        prefetch_map(mr);
+        if (!FIRST) prefetch_map(mp);
+        if (XDBL) prefetch_map(mx);
+        int slot = 0;
+        uint32_t phase = 0;
+        bool wrapped = false;  // the ring has been filled once: wait for releases
+        for (int j = blockIdx.x; j < g.items(); j += gridDim.x) {
+            const int tile = j % (g.ntx * g.nty), chunk = j / (g.ntx * g.nty);
+            const int za = g.nz * chunk / g.nchunk, zb = g.nz * (chunk + 1) / g.nchunk;
+            const int x0 = (tile % g.ntx) * kSpTX, y0 = (tile / g.ntx) * TY;
+            for (int s = 0; s < zb - za + 4; ++s) {
+                if (wrapped) mbar_wait(&empty[slot], phase ^ 1u);
+                const int zp = za - 2 + s;
+                const bool xo = XDBL && zp >= za && zp < zb;
+                double *st = ring + slot * G::StageD;
+                mbar_expect_tx(&full[slot], (FIRST ? 1 : 2) * G::BoxBytes + (xo ? G::XBytes : 0));
+                tma_load_3d(st, mr, x0 - 2, y0 - 2, zp, &full[slot]);
+                if (!FIRST) tma_load_3d(st + G::BoxD, mp, x0 - 2, y0 - 2, zp, &full[slot]);
+                if (xo) tma_load_3d(st + 2 * G::BoxD, mx, x0, y0, zp, &full[slot]);
+                if (++slot == S) {
+                    slot = 0;
+                    phase ^= 1u;
+                    wrapped = true;
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers
+    double *const PB = ring + S * G::StageD;  // p planes [2], then z' planes [2]
+    double *const ZB = PB + 2 * G::BoxD;
+    const bool edge = warp >= G::Rows;
+    const int e = (warp - G::Rows) * 32 + lane;          // edge item
+    const bool eact = edge && e < 2 * G::Rows;
+    const int row = edge ? (eact ? e >> 1 : 0) : warp;
+    const int side = e & 1;                               // edge: 0 = x0-2 pair, 1 = x0+64 pair
+    const int col = edge ? (side ? kSpBX - 2 : 0) : 2 + 2 * lane;  // pair start column in the box
+    const int o = row * kSpBX + col;
+    const int oi = row * kSpBX + (side ? kSpBX - 2 : 1);  // edge: the halo cell next to the tile
+    const int ox = 2 * G::BoxD + (row - 2) * kSpTX + 2 * lane;  // row warps: the pair in the x box
+    const bool qrow = row >= 1 && row <= TY + 2;          // q / r' / z' rows (halo 1)
+    const int nthr = 32 * G::CWarps;
+    const unsigned pl = (unsigned)plane;
+    // ring position, carried across segments (no 64-bit division in the loop)
+    int slot = 0;
+    uint32_t phase = 0;
+    // take the staged raw values of this step, then hand the stage back to the
+    // producer at once: p and z' live in their own plane buffers, so the ring
+    // sees generic-proxy READS only (no proxy fence needed before the refill)
+    auto take = [&](double2 &r2, double2 &po, double2 &xo, bool want_x) {
+        mbar_wait(&full[slot], phase);
+        const double *st = ring + slot * G::StageD;
+        r2 = sp_lds2(st + o);
+        po = make_double2(0.0, 0.0);
+        if (!FIRST) po = sp_lds2(st + G::BoxD + o);
+        xo = make_double2(0.0, 0.0);
+        if (XDBL && want_x) xo = sp_lds2(st + ox);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (++slot == S) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    };
+    for (int j = blockIdx.x; j < g.items(); j += gridDim.x) {
+        const int tile = j % (g.ntx * g.nty), chunk = j / (g.ntx * g.nty);
+        const int za = g.nz * chunk / g.nchunk, zb = g.nz * (chunk + 1) / g.nchunk;
+        const int x0 = (tile % g.ntx) * kSpTX, y0 = (tile / g.ntx) * TY;
+        const int gy = y0 - 2 + row;
+        const int gx = edge ? (side ? x0 + kSpTX : x0 - 1) : x0 + 2 * lane;  // edge: the halo cell
+        const bool xyin = gy >= 0 && gy < g.ny && gx >= 0 && gx < g.nx;    // z' may be nonzero
+        const bool irow = !edge && row >= 2 && row < TY + 2 && gy < g.ny;  // tile rows
+        const bool own = irow && gx < g.nx;                                 // tile pairs
+        const int L = zb - za, last = L + 3;
+        // 32-bit flat offset of this pair on plane zp = za - 2 + s (wraps for
+        // ghost rows / planes; used only when the cell is owned)
+        unsigned gz = (unsigned)gx + (unsigned)g.nx * (unsigned)gy + pl * (unsigned)(za - 2);
+        // per-pair state (edge warps use .x only): accumulators of q (plane
+        // zp) and w (plane zq), previous p and z', raw r of the newest plane
+        double2 aq = make_double2(0.0, 0.0), aw = aq, pc = aq, zl = aq, rw = aq;
+        if (!edge) {
+            // step s: p(zp), zp = za-2+s; q, r', z' of zq = zp-1; w of zq-1.
+            // ST: the steady state of a tile row (every plane condition true)
+            auto step = [&](auto steady, int s) {
+                constexpr bool ST = decltype(steady)::value;
+                const int zq = za - 3 + s;
+                double2 r2, po, xo;
+                take(r2, po, xo, own && s >= 2 && s <= L + 1);
+                const double2 p2 = make_double2(sp_form<PK, FIRST>(r2.x, po.x, zc, beta),
+                                                sp_form<PK, FIRST>(r2.y, po.y, zc, beta));
+                double *const Pb = PB + (s & 1) * G::BoxD + o;
+                double *const Zb = ZB + (s & 1) * G::BoxD + o;
+                sp_sts2(Pb, p2);
+                if (ST ? own : (own && s >= 2 && s <= L + 1)) {
+                    sp_stg2(p_new + gz, p2);
+                    if (XDBL)  // x = (x + alpha_prev p_{k-1}) + alpha p_k (src/solver.py:155, twice)
+                        sp_stg2(x + gz, make_double2(__fma_rn(alpha, p2.x, __fma_rn(alpha_prev, po.x, xo.x)),
+                                                     __fma_rn(alpha, p2.y, __fma_rn(alpha_prev, po.y, xo.y))));
+                }
+                // ---- q(zq) complete (its z+1 term), r_{k+1} and z' of plane zq
+                if (ST || (qrow && s >= 1)) {
+                    const double q0 = __fma_rn(off, p2.x, aq.x), q1 = __fma_rn(off, p2.y, aq.y);
+                    const double r0 = __fma_rn(malpha, q0, rw.x), r1 = __fma_rn(malpha, q1, rw.y);  // :157
+                    const bool zin = ST || (unsigned)zq < (unsigned)g.nz;
+                    const double2 zn = xyin && zin ? make_double2(sp_z<PK>(r0, zc), sp_z<PK>(r1, zc))
+                                                   : make_double2(0.0, 0.0);
+                    sp_sts2(Zb, zn);
+                    if (ST ? own : (own && s >= 3 && s <= L + 2)) {
+                        sp_stg2(r_out + (gz - pl), make_double2(r0, r1));
+                        rr = __fma_rn(r0, r0, rr);  // :158
+                        rr = __fma_rn(r1, r1, rr);
+                        gam = __fma_rn(r0, zn.x, gam);  // :163-164
+                        gam = __fma_rn(r1, zn.y, gam);
+                    }
+                    // ---- w(zq-1) complete (its z+1 term): delta += z'.w
+                    if (ST ? own : (own && s >= 4)) {
+                        dlt = __fma_rn(zl.x, __fma_rn(off, zn.x, aw.x), dlt);
+                        dlt = __fma_rn(zl.y, __fma_rn(off, zn.y, aw.y), dlt);
+                    }
+                    aw = zn;  // parked: z'(zq) for w's in-plane terms after the barrier
+                }
+                rw = r2;
+                gz += pl;
+                sp_bar(nthr);
+                if (ST || qrow) {  // in-plane terms of q(zp) = A p(zp): k-1, j-1, i-1, i, i+1, j+1
+                    const double2 ym = sp_lds2(Pb - kSpBX), yp = sp_lds2(Pb + kSpBX);
+                    const double xl = Pb[-1], xr = Pb[2];
+                    double a0 = off * pc.x, a1 = off * pc.y;
+                    a0 = __fma_rn(off, ym.x, a0);
+                    a1 = __fma_rn(off, ym.y, a1);
+                    a0 = __fma_rn(off, xl, a0);
+                    a1 = __fma_rn(off, p2.x, a1);
+                    a0 = __fma_rn(diag, p2.x, a0);
+                    a1 = __fma_rn(diag, p2.y, a1);
+                    a0 = __fma_rn(off, p2.y, a0);
+                    a1 = __fma_rn(off, xr, a1);
+                    a0 = __fma_rn(off, yp.x, a0);
+                    a1 = __fma_rn(off, yp.y, a1);
+                    aq = make_double2(a0, a1);
+                    pc = p2;
+                }
+                if (ST || (irow && s >= 1)) {  // in-plane terms of w(zq) = A z'(zq)
+                    const double2 zc2 = aw;
+                    const double2 ym = sp_lds2(Zb - kSpBX), yp = sp_lds2(Zb + kSpBX);
+                    const double xl = Zb[-1], xr = Zb[2];
+                    double a0 = off * zl.x, a1 = off * zl.y;
+                    a0 = __fma_rn(off, ym.x, a0);
+                    a1 = __fma_rn(off, ym.y, a1);
+                    a0 = __fma_rn(off, xl, a0);
+                    a1 = __fma_rn(off, zc2.x, a1);
+                    a0 = __fma_rn(diag, zc2.x, a0);
+                    a1 = __fma_rn(diag, zc2.y, a1);
+                    a0 = __fma_rn(off, zc2.y, a0);
+                    a1 = __fma_rn(off, xr, a1);
+                    a0 = __fma_rn(off, yp.x, a0);
+                    a1 = __fma_rn(off, yp.y, a1);
+                    zl = zc2;
+                    aw = make_double2(a0, a1);
+                }
+            };
+            int s = 0;
+            if (irow) {
+                for (; s < 4 && s <= last; ++s) step(std::false_type{}, s);
+                for (; s <= L + 1; ++s) step(std::true_type{}, s);
+            }
+            for (; s <= last; ++s) step(std::false_type{}, s);
+        } else {
+            // ---- edge warps: the halo pairs' p, and q / z' of the halo cell
+            for (int s = 0; s <= last; ++s) {
+                const int zq = za - 3 + s;
+                double2 r2, po, xo;
+                take(r2, po, xo, false);
+                double *const Pb = PB + (s & 1) * G::BoxD;
+                double *const Zb = ZB + (s & 1) * G::BoxD;
+                double pin = 0.0;
+                if (eact) {
+                    const double2 p2 = make_double2(sp_form<PK, FIRST>(r2.x, po.x, zc, beta),
+                                                    sp_form<PK, FIRST>(r2.y, po.y, zc, beta));
+                    sp_sts2(Pb + o, p2);
+                    pin = side ? p2.x : p2.y;
+                    if (qrow && s >= 1) {
+                        const double q0 = __fma_rn(off, pin, aq.x);
+                        const double r0 = __fma_rn(malpha, q0, rw.x);
+                        Zb[oi] = xyin && (unsigned)zq < (unsigned)g.nz ? sp_z<PK>(r0, zc) : 0.0;
+                    }
+                    rw.x = side ? r2.x : r2.y;
+                }
+                sp_bar(nthr);
+                if (eact && qrow) {
+                    double a0 = off * pc.x;
+                    a0 = __fma_rn(off, Pb[oi - kSpBX], a0);
+                    a0 = __fma_rn(off, Pb[oi - 1], a0);
+                    a0 = __fma_rn(diag, pin, a0);
+                    a0 = __fma_rn(off, Pb[oi + 1], a0);
+                    a0 = __fma_rn(off, Pb[oi + kSpBX], a0);
+                    aq.x = a0;
+                    pc.x = pin;
+                }
+            }
+        }
+    }
+}
+
+template <int PK, int TY, int S, bool XDBL>
+__global__ void __launch_bounds__(Sp<TY, S>::Threads, 1)
+    cg_spass_kernel(const __grid_constant__ CUtensorMap mr, const __grid_constant__ CUtensorMap mp,
+                    const __grid_constant__ CUtensorMap mx, SpGeom g, double off, double diag, double zc,
+                    double *__restrict__ r_out, double *__restrict__ p_new, double *__restrict__ x, CgScalars *sc,
+                    double *partials, CgTickets *tk, int use_cond, cudaGraphConditionalHandle cond)
+{
+    using G = Sp<TY, S>;
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[S], empty[S];
+    __shared__ double red[32];
+    __shared__ int is_last;
+    if (sc->done) {
+        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    double *const ring = aligned_smem(smem_raw);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], G::CWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    double rr = 0.0, gam = 0.0, dlt = 0.0;
+    const double alpha = sc->alpha, alpha_prev = sc->alpha_prev, beta = sc->beta;
+    if (!XDBL && sc->it == 0)
+        spass_body<PK, TY, S, true, false>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev, 0.0,
+                                           ring, full, empty, rr, gam, dlt);
+    else
+        spass_body<PK, TY, S, false, XDBL>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev, beta,
+                                           ring, full, empty, rr, gam, dlt);
+    rr = block_sum<G::Threads>(rr, red);
+    gam = block_sum<G::Threads>(gam, red);
+    dlt = block_sum<G::Threads>(dlt, red);
+    if (threadIdx.x == 0) {
+        partials[3 * blockIdx.x] = rr;
+        partials[3 * blockIdx.x + 1] = gam;
+        partials[3 * blockIdx.x + 2] = dlt;
+    }
+    if (last_block(&tk->upd, &is_last)) {
+        rr = reduce_partials<G::Threads>(partials, gridDim.x, 3, red);
+        gam = reduce_partials<G::Threads>(partials + 1, gridDim.x, 3, red);
+        dlt = reduce_partials<G::Threads>(partials + 2, gridDim.x, 3, red);
+        if (threadIdx.x == 0) {
+            scalar_after_pass(sc, rr, gam, dlt);
+            if (sc->done && use_cond) cudaGraphSetConditional(cond, 0);
+        }
+    }
+}

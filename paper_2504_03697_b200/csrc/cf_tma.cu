@@ -25,6 +25,11 @@ static EncodeTiledFn encode_fn()
 
 bool make_map(CUtensorMap *map, const double *base, int nx, int ny, int planes, int bx, int by)
 {
+    return make_map_promo(map, base, nx, ny, planes, bx, by, 256);
+}
+
+bool make_map_promo(CUtensorMap *map, const double *base, int nx, int ny, int planes, int bx, int by, int promo)
+{
     EncodeTiledFn enc = encode_fn();
     if (!enc || !base) return false;
     const cuuint64_t row = (cuuint64_t)nx * sizeof(double);
@@ -35,7 +40,11 @@ bool make_map(CUtensorMap *map, const double *base, int nx, int ny, int planes, 
     cuuint32_t estr[3] = {1, 1, 1};
     // OOB_FILL_NONE: out-of-bounds elements of a box read as zero
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     promo >= 256   ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                     : promo >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                     : promo >= 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }

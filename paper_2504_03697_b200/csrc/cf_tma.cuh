@@ -24,8 +24,10 @@ constexpr int kTTY = 16;               // tile y (16 warps)
 constexpr int kTThreads = kTTX * kTTY;  // 512
 // Halo box: x from x0-2 (the TMA unit faults unless a box's x origin is a
 // 16-byte multiple -- measured: any odd fp64 x origin traps -- so the box
-// starts two cells early and is 36 wide), y from y0-1, 18 tall.  Box origins
-// are clamped at 0: negative coordinates trap as well.
+// starts two cells early and is 36 wide), y from y0-1, 18 tall.  (Negative
+// origins with a 16-byte-multiple x zero-fill correctly -- tools/tma_selftest.cu
+// variants 6-10; round 1 read the odd-x trap at (-1, -1) as a negative-origin
+// one -- these kernels still clamp at 0 and mask.)
 constexpr int kHX = kTTX + 4, kHY = kTTY + 2;
 constexpr int kStages = 3;  // measured 3/4/6: depth is not the limiter; 3 frees smem
 
@@ -102,6 +104,8 @@ struct TmaGeom {
 // planes starting at `base`, box (bx, by, 1).  Returns false when TMA cannot
 // describe the array (row pitch not a multiple of 16 bytes, ...).
 bool make_map(CUtensorMap *map, const double *base, int nx, int ny, int planes, int bx, int by);
+// the same with an explicit L2 promotion (0 / 64 / 128 / 256 bytes; make_map uses 256)
+bool make_map_promo(CUtensorMap *map, const double *base, int nx, int ny, int planes, int bx, int by, int promo);
 
 // Host: chunk count and grid for a kernel with `blocks_per_sm` residency.
 TmaGeom tma_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, int blocks_per_sm);
