@@ -15,9 +15,11 @@ value   = CG iterations / second over the K timed steps (whole steps, so
 e2e     = the same metric through the public API with the state in pinned
           HOST memory: H2D of the step's inputs (u, v, w; p too with
           warm_start) + step() + D2H of u, v, w, p every step.
-roofline: the fused CG iteration (dir + update kernels), algorithmic bytes
-          88*N per iteration / measured loop time per
-          iteration, against MEASURED_PEAKS.json hbm_gbs.
+roofline: the fused CG iteration (the single TMA-fed pass by default; the
+          two-kernel loop with CF_CG_ALGO=two), algorithmic bytes 88*N per
+          iteration / measured loop time per iteration,
+          against MEASURED_PEAKS.json hbm_gbs; design_frac / dram_frac on the
+          bytes the kernels move (40 N single pass) / ncu measured.
 cpu_baseline: the oracle port (oracle/, the reference's algorithm in C with
           the reference's WorkerPool chunking) on a bounded sample: 256^3
           Jacobi PCG iterations with the symmetric SpMV, all host threads.
@@ -34,7 +36,8 @@ sub-records (each its own CUDA-event timed region after the main one):
           baseline/DIC solver at 256^3), config4_as_written (nu=0.001, lid
           velocity 1, no-slip); --no-extra skips them.
 roofline.traffic: DRAM bytes per CG iteration from the newest committed ncu
-          summary (profiles/ncu_cg_r*.json, named in traffic_source).
+          summary of the same CG form (profiles/ncu_cg_r*.json, "form"; named
+          in traffic_source).
 """
 
 from __future__ import annotations
@@ -181,17 +184,28 @@ def run_reference(args, rank):
 # ---------------------------------------------------------------- our arm
 
 
-def load_traffic():
+# the CG form a solve ran (solver.FORMS) -> roofline description / bytes per cell it moves
+KERNELS = {"single-pass": "fused CG iteration: ONE TMA-fed single-reduction pass (cg_spass_kernel; "
+                          "x updated every 2nd pass)",
+           "two-kernel": "fused CG iteration (cg_dir_lean2 + cg_update_tma; x updated every 2nd iteration)"}
+DESIGN_BYTES = {"single-pass": 40, "two-kernel": 60}
+
+
+def load_traffic(form=None):
     """Per-iteration DRAM bytes of the fused CG kernels from the newest committed
-    ncu summary (ncu cannot run inside the timed bench): (bytes, source path)."""
+    ncu summary for this CG form (ncu cannot run inside the timed bench):
+    (bytes, source path)."""
     import glob
     found = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_cg_r*.json")))
-    path = found[-1] if found else os.path.join(ROOT, "profiles", "ncu_cg_r01.json")
-    try:
-        with open(path) as f:
-            return json.load(f).get("dram_bytes_per_iteration"), os.path.relpath(path, ROOT)
-    except Exception:
-        return None, None
+    for path in reversed(found):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+        except Exception:
+            continue
+        if d.get("form", "two-kernel") == (form or "two-kernel"):
+            return d.get("dram_bytes_per_iteration"), os.path.relpath(path, ROOT)
+    return None, None
 
 
 def run_ours(args, rank, world, local_rank):
@@ -223,16 +237,18 @@ def run_ours(args, rank, world, local_rank):
     # ---- device-resident timed region
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    its, loop_ms, launches = [], 0.0, 0
+    its, loop_ms, launches, form = [], 0.0, 0, None
     with ClockSampler(local_rank) as clocks:
         e0.record(stream)
         for _ in range(args.steps):
             s = cf.step(state, cfg, cache)
             its.append(s.solve.iterations)
-            loop_ms += cache.operator(cfg)._cg_ws.last_loop_ms
-            # forces, advect, divergence, cg-init, correct + 2 kernels per iteration,
-            # the while body is unrolled by two (an odd count adds 2 early-exit launches)
-            launches += 5 + 4 * ((s.solve.iterations + 1) // 2)
+            ws = cache.operator(cfg)._cg_ws
+            loop_ms += ws.last_loop_ms
+            # forces, advect, divergence, correct + the solve's own count (init,
+            # the while body of two iterations, the x fix-up: cf_cg_last_form)
+            launches += 4 + ws.last_launches
+            form = ws.last_form
         e1.record(stream)
         barrier()
     ms = e0.elapsed_time(e1)
@@ -281,7 +297,8 @@ def run_ours(args, rank, world, local_rank):
     alg_bytes = 88 * cells
     iter_s = (loop_ms / 1e3) / max(sum(its), 1)
     achieved = alg_bytes / iter_s / 1e9
-    traffic, traffic_src = load_traffic()
+    design = DESIGN_BYTES.get(form, 60)
+    traffic, traffic_src = load_traffic(form)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -298,12 +315,13 @@ def run_ours(args, rank, world, local_rank):
         "fused_iter_frac": achieved / peak,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                     "kernel": "fused CG iteration (cg_dir_lean2 + cg_update_tma; x updated every 2nd iteration)",
-                     "algorithmic_bytes_per_iteration": alg_bytes, "design_bytes_per_iteration": 60 * cells,
-                     # the same iteration time against the bytes this design moves (60 N) and
-                     # against the DRAM traffic ncu measured per iteration (frac above uses the
-                     # reference op sequence's 88 N, hence > 1)
-                     "design_frac": 60 * cells / iter_s / 1e9 / peak,
+                     "kernel": KERNELS.get(form, form),
+                     "algorithmic_bytes_per_iteration": alg_bytes, "design_bytes_per_iteration": design * cells,
+                     # the same iteration time against the bytes this design moves (40 N for the
+                     # single pass, 60 N for the two-kernel loop) and against the DRAM traffic ncu
+                     # measured per iteration (frac above uses the reference op sequence's 88 N,
+                     # SURVEY.md 8(d), hence > 1)
+                     "design_frac": design * cells / iter_s / 1e9 / peak,
                      "dram_frac": (traffic / iter_s / 1e9 / peak) if traffic else None,
                      "peak_kind": peak_kind},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

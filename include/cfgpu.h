@@ -122,6 +122,17 @@ int cf_cg_solve(cf_cg *ws, const double *b, double *x, const double *x0, double 
                 double *res_host, void *stream);
 /* Device time (ms) of the last solve's iteration loop, CUDA-event timed. */
 int cf_cg_last_loop_ms(cf_cg *ws, float *ms_host);
+/* The kernel form the last solve ran and how many kernels it launched
+ * (no reference counterpart: measurement support for bench.py). */
+enum {
+    CF_CG_FORM_SMALL = 0,    /* n^3 <= 5120: the whole solve in one block */
+    CF_CG_FORM_TWO = 1,      /* two fused kernels per iteration (the reference recurrence) */
+    CF_CG_FORM_SPASS = 2,    /* one TMA-fed single-reduction pass per iteration (default) */
+    CF_CG_FORM_PASS = 3,     /* opt-in single-reduction pass kernels (CF_CG_ALGO=pass) */
+    CF_CG_FORM_PERSIST = 4,  /* opt-in persistent single launch (CF_PERSIST=1) */
+    CF_CG_FORM_TWO_DIC = 5   /* two-kernel loop with the DIC sweeps */
+};
+int cf_cg_last_form(cf_cg *ws, int *form_host, int64_t *launches_host);
 /* Attach a DIC factor (arguments as cf_dic_apply; device arrays must stay
  * alive) so cf_cg_solve accepts CF_PRECOND_DIC: each iteration then runs the
  * level sweeps inside the same device loop. */

@@ -62,6 +62,7 @@ _SIGNATURES = {
     "cf_cg_destroy": ([_vp], _int),
     "cf_cg_solve": ([_vp, _vp, _vp, _vp, _dbl, _i64, _int, _vp, _pi64, _pd, _vp], _int),
     "cf_cg_last_loop_ms": ([_vp, _pf], _int),
+    "cf_cg_last_form": ([_vp, ctypes.POINTER(_int), _pi64], _int),
     "cf_nccl_unique_id": ([_vp], _int),
     "cf_dcg_create": ([ctypes.POINTER(_vp), _int, _int, _int, _dbl, _int, _int, _int, _vp, _int, _vp, _int, _int,
                        _vp], _int),

@@ -671,6 +671,10 @@ struct cf_cg {
     double zc_pass[4] = {0, 0, 0, 0};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float last_loop_ms = 0.f;
+    // the form the last solve ran (CF_CG_FORM_*) and its kernel launches
+    int last_form = 0;
+    long long last_launches = 0;
+    bool last_x0 = false;
     // one instantiated while-graph per (preconditioner kind)
     cudaGraphExec_t exec[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaGraph_t graph[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -1130,6 +1134,7 @@ static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, c
                                      (int)smem));
         CF_CUDA(cudaEventRecord(ws->ev0, s));
         const int nlev = (int)ws->dic.level_ptr.size() - 1;
+        ws->last_form = CF_CG_FORM_SMALL;
         cg_small_dic_kernel<ORDER><<<1, kSmallThreads, smem, s>>>(ws->bx, ws->off, ws->diag, b, ws->x, ws->dic.d,
                                                                   ws->dic.rows, ws->dic_lptr, nlev,
                                                                   ws->dic.wave.lval, ws->dic.wave.uval, ws->sc);
@@ -1141,6 +1146,7 @@ static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, c
         const size_t smem = 3 * (size_t)ws->n * sizeof(double);
         CF_CUDA(cudaFuncSetAttribute(cg_small_kernel<ORDER, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CF_CUDA(cudaEventRecord(ws->ev0, s));
+        ws->last_form = CF_CG_FORM_SMALL;
         cg_small_kernel<ORDER, PK><<<1, kSmallThreads, smem, s>>>(ws->bx, ws->off, ws->diag, b, x0, ws->x, ws->jd, zc,
                                                                   ws->sc);
         CF_CHECK_LAUNCH("cg_small_kernel");
@@ -1148,13 +1154,16 @@ static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, c
         return CF_OK;
     }
     if ((PK == PK_NONE || PK == PK_JCONST) && ws->spass && !x0) {
+        ws->last_form = CF_CG_FORM_SPASS;
         if constexpr (PK == PK_NONE || PK == PK_JCONST) return spass_solve<ORDER, PK>(ws, b, zc, s);
     }
     if ((PK == PK_NONE || PK == PK_JCONST) && ws->pass && !x0) {
+        ws->last_form = CF_CG_FORM_PASS;
         if constexpr (PK == PK_NONE || PK == PK_JCONST) return pass_solve<ORDER, PK>(ws, b, zc, s);
     }
     if ((PK == PK_NONE || PK == PK_JCONST) && ws->persist && !x0 && !ws->direct) {
         if constexpr (PK == PK_NONE || PK == PK_JCONST) {
+            ws->last_form = CF_CG_FORM_PERSIST;
             int rc0 = launch_init<ORDER, PK>(ws, b, x0, zc, s);
             if (rc0 != CF_OK) return rc0;
             CF_CUDA(cudaEventRecord(ws->ev0, s));
@@ -1166,6 +1175,7 @@ static int solve_impl(cf_cg *ws, const double *b, const double *x0, double zc, c
             return CF_OK;
         }
     }
+    ws->last_form = PK == PK_ZVEC ? CF_CG_FORM_TWO_DIC : CF_CG_FORM_TWO;
     int rc = launch_init<ORDER, PK>(ws, b, x0, zc, s);
     if (rc != CF_OK) return rc;
     if (ws->direct) {
@@ -1346,8 +1356,11 @@ static void set_grids(cf_cg *ws)
         }
         ws->lpass_g = lg;
     }
-    // TMA-fed single-reduction pass (cf_cg_spass.cuh): CF_CG_ALGO=spass
-    ws->spass = ws->tma && ws->bx.nx % 2 == 0 && algo && !strcmp(algo, "spass");
+    // TMA-fed single-reduction pass (cf_cg_spass.cuh): the default for Jacobi /
+    // no preconditioner without a start vector (measured 256^3: 125 us per
+    // iteration against 181 for the two-kernel loop); CF_CG_ALGO=two (or pass)
+    // selects the two-kernel form, which is the reference's own recurrence
+    ws->spass = ws->tma && ws->bx.nx % 2 == 0 && ws->n + kLeanPad < (1LL << 32) && !(algo && strcmp(algo, "spass"));
     if (ws->spass) {
         cudaFuncSetAttribute(cg_spass_kernel<PK_NONE, kSpTY, kSpS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpCfg::Smem);
         cudaFuncSetAttribute(cg_spass_kernel<PK_NONE, kSpTY, kSpS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpCfg::Smem);
@@ -1543,6 +1556,21 @@ int cf_cg_solve(cf_cg *ws, const double *b, double *x, const double *x0, double 
     }
     if (iters_host) *iters_host = h->it;
     if (res_host) *res_host = h->res;
+    {  // kernel launches of this solve (the while body holds two iterations)
+        const long long batch = ws->direct ? ws->direct_batch : 1;
+        long long bodies = std::max(1LL, (h->it + 1) / 2);
+        bodies = (bodies + batch - 1) / batch * batch;
+        switch (ws->last_form) {
+        case CF_CG_FORM_SMALL: ws->last_launches = 1; break;
+        case CF_CG_FORM_SPASS: ws->last_launches = 1 + 2 * bodies + 1; break;  // init, passes, x fix-up
+        case CF_CG_FORM_PASS: ws->last_launches = 1 + 2 * bodies; break;
+        case CF_CG_FORM_PERSIST: ws->last_launches = 2; break;
+        case CF_CG_FORM_TWO_DIC:  // init, z = M^-1 r (2 sweeps), r.z; per iteration dir, update, 2 sweeps
+            ws->last_launches = (x0 ? 2 : 1) + 3 + 8 * bodies + (ws->defer_x ? 1 : 0);
+            break;
+        default: ws->last_launches = (x0 ? 2 : 1) + 4 * bodies + (ws->defer_x ? 1 : 0);
+        }
+    }
     if (h->status == cf::ST_BREAKDOWN) {
         cf::set_error("p^T A p = " + std::to_string(h->pap) + " at iteration " +
                       std::to_string(h->it + 1));
@@ -1590,6 +1618,14 @@ int cf_cg_set_dic(cf_cg *ws, const int32_t *lp, const int32_t *lc, const double 
         ws->exec[cf::PK_ZVEC] = nullptr;
         ws->graph[cf::PK_ZVEC] = nullptr;
     }
+    return CF_OK;
+}
+
+int cf_cg_last_form(cf_cg *ws, int *form_host, int64_t *launches_host)
+{
+    CF_REQUIRE(ws && form_host, "cf_cg_last_form: null argument");
+    *form_host = ws->last_form;
+    if (launches_host) *launches_host = ws->last_launches;
     return CF_OK;
 }
 

@@ -57,6 +57,10 @@ class _NullProfiler:
 NULL_PROFILER = _NullProfiler()
 
 
+# cf_cg_last_form codes (include/cfgpu.h CF_CG_FORM_*)
+FORMS = {0: "small", 1: "two-kernel", 2: "single-pass", 3: "pass", 4: "persistent", 5: "two-kernel+dic"}
+
+
 class CgWorkspace:
     """Device workspace of the fused solver (one per operator grid; like
     PoissonCache it is built once and reused every step)."""
@@ -69,6 +73,8 @@ class CgWorkspace:
         self._h = h
         self.op = op
         self.last_loop_ms = 0.0
+        self.last_form = None  # the CG kernel form of the last solve (FORMS) and its kernel launches
+        self.last_launches = 0
 
     def solve(self, b: torch.Tensor, x0, precond, tol: float, max_iter: int):
         lib = _lib.load_library()
@@ -96,6 +102,9 @@ class CgWorkspace:
         ms = ctypes.c_float()
         lib.cf_cg_last_loop_ms(self._h, ctypes.byref(ms))
         self.last_loop_ms = float(ms.value)
+        form, launches = ctypes.c_int(), ctypes.c_int64()
+        lib.cf_cg_last_form(self._h, ctypes.byref(form), ctypes.byref(launches))
+        self.last_form, self.last_launches = FORMS.get(form.value, str(form.value)), int(launches.value)
         if rc == _lib.CF_BREAKDOWN:
             raise BreakdownError(_lib.last_error())
         _lib.check(rc, "cf_cg_solve")

@@ -50,16 +50,22 @@ def main():
         kernels[name] = {"launches": k["launches"], "share_pct": round(100 * k["us"] / total, 2),
                          "avg_us": round(k["us"] / k["launches"], 2),
                          "dram_mb_per_launch": round(k["bytes"] / k["launches"] / 1e6, 1)}
-    cg = {n: k for n, k in agg.items() if n.startswith(("cg_dir", "cg_update"))}
-    dirs = sum(k["launches"] for n, k in cg.items() if n.startswith("cg_dir"))
+    spass = {n: k for n, k in agg.items() if n.startswith("cg_spass")}
+    if spass:  # the single-pass form: one launch per iteration
+        cg, form, design = spass, "single-pass", 40
+        dirs = sum(k["launches"] for k in spass.values())
+    else:
+        cg = {n: k for n, k in agg.items() if n.startswith(("cg_dir", "cg_update"))}
+        form, design = "two-kernel", 60
+        dirs = sum(k["launches"] for n, k in cg.items() if n.startswith("cg_dir"))
     cg_bytes = sum(k["bytes"] for k in cg.values())
     n3 = a.grid ** 3
-    out = {"round": a.round, "source": a.label, "grid": f"{a.grid}^3", "kernels": kernels,
+    out = {"round": a.round, "source": a.label, "grid": f"{a.grid}^3", "form": form, "kernels": kernels,
            "cg_iterations_profiled": dirs,
            "dram_bytes_per_iteration": cg_bytes / dirs if dirs else None,
            "cg_us_per_iteration_cold": sum(k["us"] for k in cg.values()) / dirs if dirs else None,
            "algorithmic_bytes_per_iteration_88N": 88 * n3,
-           "design_bytes_per_iteration_60N": 60 * n3}
+           f"design_bytes_per_iteration_{design}N": design * n3}
     with open(a.out, "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "kernels"}))
