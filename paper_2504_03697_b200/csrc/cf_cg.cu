@@ -663,6 +663,8 @@ struct cf_cg {
     // TMA-fed single-reduction pass (cf_cg_spass.cuh): one kernel per
     // iteration, 40 N; r ping-pongs with r2, x updated every second pass
     bool spass = false;
+    int sp_ty = 16;  // tile height: 16 (one CTA per SM) or 8 (two; form 1 only)
+    int sp_form = 2;  // 2: two rows per warp, SoA planes; 1: one row per warp (CF_SPASS_FORM=1)
     cf::SpGeom sp_g{};
     int sp_ctas = 0;
     CUtensorMap m_spr[2]{}, m_spp[2]{}, m_spx{};
@@ -1021,26 +1023,56 @@ static int pass_solve(cf_cg *ws, const double *b, double zc, cudaStream_t s)
 }
 
 // ---------------------------------------------------------------- TMA-fed single pass
-constexpr int kSpTY = 16, kSpS = 6;
-using SpCfg = Sp<kSpTY, kSpS>;
-
-template <int PK>
-static int spass_body_launch(cf_cg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond, int use_cond)
+// tile height / ring depth variants: 16-row tiles, one CTA per SM (default);
+// 8-row tiles, two CTAs per SM (CF_SPASS_TY=8)
+template <int PK, int TY, int S, int FORM>
+static void spass_launch(cf_cg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond, int use_cond)
 {
+    using G = Sp<TY, S, FORM>;
     for (int half = 0; half < 2; ++half) {
         // half 0: r, p[0] -> r2, p[1], x skipped; half 1: r2, p[1] -> r, p[0], x for both passes
         double *r_out = half ? ws->r : ws->r2;
         if (half == 0)
-            cg_spass_kernel<PK, kSpTY, kSpS, false><<<ws->sp_ctas, SpCfg::Threads, SpCfg::Smem, s>>>(
+            cg_spass_kernel<PK, TY, S, false, FORM><<<ws->sp_ctas, G::Threads, G::Smem, s>>>(
                 ws->m_spr[0], ws->m_spp[0], ws->m_spx, ws->sp_g, ws->off, ws->diag, zc, r_out, ws->p[1], ws->x,
                 ws->sc, ws->partials, ws->tk, use_cond, cond);
         else
-            cg_spass_kernel<PK, kSpTY, kSpS, true><<<ws->sp_ctas, SpCfg::Threads, SpCfg::Smem, s>>>(
+            cg_spass_kernel<PK, TY, S, true, FORM><<<ws->sp_ctas, G::Threads, G::Smem, s>>>(
                 ws->m_spr[1], ws->m_spp[1], ws->m_spx, ws->sp_g, ws->off, ws->diag, zc, r_out, ws->p[0], ws->x,
                 ws->sc, ws->partials, ws->tk, use_cond, cond);
-        CF_CHECK_LAUNCH("cg_spass_kernel");
     }
+}
+
+template <int PK>
+static int spass_body_launch(cf_cg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond, int use_cond)
+{
+    if (ws->sp_form == 1 && ws->sp_ty == 8) spass_launch<PK, 8, 5, 1>(ws, s, zc, cond, use_cond);
+    else if (ws->sp_form == 1) spass_launch<PK, 16, 6, 1>(ws, s, zc, cond, use_cond);
+    else spass_launch<PK, 16, 6, 2>(ws, s, zc, cond, use_cond);
+    CF_CHECK_LAUNCH("cg_spass_kernel");
     return CF_OK;
+}
+
+// host setup of one variant: smem opt-in, (tile, chunk) geometry, resident CTAs
+template <int TY, int S, int FORM>
+static void spass_setup(cf_cg *ws)
+{
+    using G = Sp<TY, S, FORM>;
+    cudaFuncSetAttribute(cg_spass_kernel<PK_NONE, TY, S, false, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::Smem);
+    cudaFuncSetAttribute(cg_spass_kernel<PK_NONE, TY, S, true, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::Smem);
+    cudaFuncSetAttribute(cg_spass_kernel<PK_JCONST, TY, S, false, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::Smem);
+    cudaFuncSetAttribute(cg_spass_kernel<PK_JCONST, TY, S, true, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::Smem);
+    SpGeom g{ws->bx.nx, ws->bx.ny, ws->bx.nz, (ws->bx.nx + kSpTX - 1) / kSpTX, (ws->bx.ny + TY - 1) / TY, 1};
+    const int bps = blocks_per_sm((const void *)cg_spass_kernel<PK_JCONST, TY, S, true, FORM>, G::Threads, G::Smem);
+    const long long slots = (long long)num_sms() * (bps > 0 ? bps : 1), tiles = (long long)g.ntx * g.nty;
+    // z-chunks: as many as fill the resident slots in one round, each >= 8 planes
+    long long c = std::max(1LL, std::min(slots / std::max(1LL, tiles), (long long)g.nz / 8));
+    if (const char *e = getenv("CF_SPASS_CHUNKS")) c = std::max(1, std::min(atoi(e), g.nz));
+    g.nchunk = (int)c;
+    const long long items = tiles * c, rounds = (items + slots - 1) / slots;
+    ws->sp_ctas = (int)((items + rounds - 1) / rounds);  // equal rounds for every CTA
+    ws->sp_g = g;
+    ws->spass = bps >= 1;
 }
 
 template <int ORDER, int PK>
@@ -1362,22 +1394,11 @@ static void set_grids(cf_cg *ws)
     // selects the two-kernel form, which is the reference's own recurrence
     ws->spass = ws->tma && ws->bx.nx % 2 == 0 && ws->n + kLeanPad < (1LL << 32) && !(algo && strcmp(algo, "spass"));
     if (ws->spass) {
-        cudaFuncSetAttribute(cg_spass_kernel<PK_NONE, kSpTY, kSpS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpCfg::Smem);
-        cudaFuncSetAttribute(cg_spass_kernel<PK_NONE, kSpTY, kSpS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpCfg::Smem);
-        cudaFuncSetAttribute(cg_spass_kernel<PK_JCONST, kSpTY, kSpS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpCfg::Smem);
-        cudaFuncSetAttribute(cg_spass_kernel<PK_JCONST, kSpTY, kSpS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SpCfg::Smem);
-        SpGeom g{ws->bx.nx, ws->bx.ny, ws->bx.nz, (ws->bx.nx + kSpTX - 1) / kSpTX, (ws->bx.ny + kSpTY - 1) / kSpTY, 1};
-        const int bps = blocks_per_sm((const void *)cg_spass_kernel<PK_JCONST, kSpTY, kSpS, true>, SpCfg::Threads,
-                                      SpCfg::Smem);
-        const long long slots = (long long)num_sms() * (bps > 0 ? bps : 1), tiles = (long long)g.ntx * g.nty;
-        // z-chunks: as many as fill the resident slots in one round, each >= 8 planes
-        long long c = std::max(1LL, std::min(slots / std::max(1LL, tiles), (long long)g.nz / 8));
-        if (const char *e = getenv("CF_SPASS_CHUNKS")) c = std::max(1, std::min(atoi(e), g.nz));
-        g.nchunk = (int)c;
-        const long long items = tiles * c, rounds = (items + slots - 1) / slots;
-        ws->sp_ctas = (int)((items + rounds - 1) / rounds);  // equal rounds for every CTA
-        ws->sp_g = g;
-        ws->spass = bps >= 1;
+        if (const char *e = getenv("CF_SPASS_FORM")) ws->sp_form = atoi(e) == 1 ? 1 : 2;
+        if (const char *e = getenv("CF_SPASS_TY")) ws->sp_ty = atoi(e) == 8 && ws->sp_form == 1 ? 8 : 16;
+        if (ws->sp_form == 1 && ws->sp_ty == 8) spass_setup<8, 5, 1>(ws);
+        else if (ws->sp_form == 1) spass_setup<16, 6, 1>(ws);
+        else spass_setup<16, 6, 2>(ws);
     }
     if (const char *e = getenv("CF_CG_UPD_SKIP")) ws->kind_upd_skip = kern_kind("CF_CG_UPD_SKIP", ws->kind_upd, ws->tma, pair_ok);
     const char *dx = getenv("CF_CG_DEFER_X");
@@ -1462,7 +1483,7 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
     }
     if (ws->spass) {  // boxes of the single pass: 68 x (TY+4) halo boxes of r / p, 64 x TY interior box of x
         const int nx = ws->bx.nx, ny = ws->bx.ny, nz = ws->bx.nz;
-        const int hy = cf::kSpTY + 4;
+        const int hy = ws->sp_ty + 4;
         int pr = 256;
         if (const char *e = getenv("CF_SPASS_PROMO")) pr = atoi(e);
         auto mk = [&](CUtensorMap *m, const double *b, int bx, int by) {
@@ -1470,7 +1491,7 @@ int cf_cg_create(cf_cg **out, int nx, int ny, int nz, double h, int order, void 
         };
         ws->spass = mk(&ws->m_spr[0], ws->r, cf::kSpBX, hy) && mk(&ws->m_spr[1], ws->r2, cf::kSpBX, hy) &&
                     mk(&ws->m_spp[0], ws->p[0], cf::kSpBX, hy) && mk(&ws->m_spp[1], ws->p[1], cf::kSpBX, hy) &&
-                    mk(&ws->m_spx, ws->x, cf::kSpTX, cf::kSpTY);
+                    mk(&ws->m_spx, ws->x, cf::kSpTX, ws->sp_ty);
     }
     if (ws->tma && !cf::build_maps(ws)) {  // TMA cannot describe the arrays: pair / LDG forms
         ws->tma = false;

@@ -44,12 +44,17 @@
 constexpr int kSpTX = 64;            // tile width (32 pairs)
 constexpr int kSpBX = kSpTX + 4;     // box width: x0-2 .. x0+65
 
-template <int TY, int S>
+// FORM 1: one box row per warp, AoS plane buffers (the first form, kept for
+// A/B); FORM 2: two box rows per warp (their shared y-neighbours stay in
+// registers) and even / odd (SoA) plane buffers, so every x- and y-neighbour
+// read is a conflict-free 8-byte LDS: 32 % fewer shared-memory wavefronts.
+template <int TY, int S, int FORM = 2>
 struct Sp {
     static_assert(TY % 4 == 0, "box bytes must stay 128-byte multiples");
     static constexpr int Rows = TY + 4;                       // box rows y0-2 .. y0+TY+1
-    static constexpr int EdgeWarps = (2 * Rows + 31) / 32;    // halo pairs at x0-2 / x0+64
-    static constexpr int CWarps = Rows + EdgeWarps;           // consumer warps
+    static constexpr int RowWarps = FORM == 2 ? Rows / 2 : Rows;
+    static constexpr int EdgeWarps = FORM == 2 ? (Rows + 31) / 32 : (2 * Rows + 31) / 32;  // halo pairs
+    static constexpr int CWarps = RowWarps + EdgeWarps;       // consumer warps
     static constexpr int Threads = 32 * (CWarps + 1);         // + the producer warp
     static constexpr int BoxD = Rows * kSpBX;                 // doubles per box
     static constexpr int XD = TY * kSpTX;                     // doubles per x box
@@ -57,6 +62,8 @@ struct Sp {
     static constexpr int StageD = 2 * BoxD + XD;              // R | P | X (TMA writes only)
     // + two p planes and two z' planes (double-buffered, generic writes only)
     static constexpr size_t Smem = ((size_t)S * StageD + 4 * BoxD) * sizeof(double) + 128;
+    // small tiles run two CTAs per SM (two independent lockstep groups)
+    static constexpr int MinBlocks = Threads <= 512 && FORM == 1 ? 2 : 1;
 };
 
 // Work items (tile, z-chunk), chunk-major: item j = chunk j / T, tile j % T
@@ -87,7 +94,41 @@ __device__ __forceinline__ double sp_form(double r, double po, double zc, double
     return FIRST ? z : __fma_rn(beta, po, z);
 }
 
-// The march of one CTA.  Consumers return their partial rr / gamma / delta.
+// The producer: one lane streams the boxes of every step of this CTA's items
+// through the ring (the consumers release a stage as soon as they have read it).
+template <class G, int TY, int S, bool FIRST, bool XDBL>
+__device__ __forceinline__ void sp_produce(const CUtensorMap *mr, const CUtensorMap *mp, const CUtensorMap *mx,
+                                           const SpGeom &g, double *ring, uint64_t *full, uint64_t *empty)
+{
+    prefetch_map(mr);
+    if (!FIRST) prefetch_map(mp);
+    if (XDBL) prefetch_map(mx);
+    int slot = 0;
+    uint32_t phase = 0;
+    bool wrapped = false;  // the ring has been filled once: wait for releases
+    for (int j = blockIdx.x; j < g.items(); j += gridDim.x) {
+        const int tile = j % (g.ntx * g.nty), chunk = j / (g.ntx * g.nty);
+        const int za = g.nz * chunk / g.nchunk, zb = g.nz * (chunk + 1) / g.nchunk;
+        const int x0 = (tile % g.ntx) * kSpTX, y0 = (tile / g.ntx) * TY;
+        for (int s = 0; s < zb - za + 4; ++s) {
+            if (wrapped) mbar_wait(&empty[slot], phase ^ 1u);
+            const int zp = za - 2 + s;
+            const bool xo = XDBL && zp >= za && zp < zb;
+            double *st = ring + slot * G::StageD;
+            mbar_expect_tx(&full[slot], (FIRST ? 1 : 2) * G::BoxBytes + (xo ? G::XBytes : 0));
+            tma_load_3d(st, mr, x0 - 2, y0 - 2, zp, &full[slot]);
+            if (!FIRST) tma_load_3d(st + G::BoxD, mp, x0 - 2, y0 - 2, zp, &full[slot]);
+            if (xo) tma_load_3d(st + 2 * G::BoxD, mx, x0, y0, zp, &full[slot]);
+            if (++slot == S) {
+                slot = 0;
+                phase ^= 1u;
+                wrapped = true;
+            }
+        }
+    }
+}
+
+// The march of one CTA (FORM 1).  Consumers return their partial rr / gamma / delta.
 template <int PK, int TY, int S, bool FIRST, bool XDBL>
 __device__ __forceinline__ void spass_body(const CUtensorMap *mr, const CUtensorMap *mp, const CUtensorMap *mx,
                                            const SpGeom &g, double off, double diag, double zc,
@@ -96,39 +137,13 @@ __device__ __forceinline__ void spass_body(const CUtensorMap *mr, const CUtensor
                                            double *ring, uint64_t *full, uint64_t *empty, double &rr, double &gam,
                                            double &dlt)
 {
-    using G = Sp<TY, S>;
+    using G = Sp<TY, S, 1>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long plane = (long long)g.nx * g.ny;
     const double malpha = -alpha;
 
     if (warp == G::CWarps) {  // ---------------- producer: one lane drives the ring
-        if (lane != 0) return;
-        prefetch_map(mr);
-        if (!FIRST) prefetch_map(mp);
-        if (XDBL) prefetch_map(mx);
-        int slot = 0;
-        uint32_t phase = 0;
-        bool wrapped = false;  // the ring has been filled once: wait for releases
-        for (int j = blockIdx.x; j < g.items(); j += gridDim.x) {
-            const int tile = j % (g.ntx * g.nty), chunk = j / (g.ntx * g.nty);
-            const int za = g.nz * chunk / g.nchunk, zb = g.nz * (chunk + 1) / g.nchunk;
-            const int x0 = (tile % g.ntx) * kSpTX, y0 = (tile / g.ntx) * TY;
-            for (int s = 0; s < zb - za + 4; ++s) {
-                if (wrapped) mbar_wait(&empty[slot], phase ^ 1u);
-                const int zp = za - 2 + s;
-                const bool xo = XDBL && zp >= za && zp < zb;
-                double *st = ring + slot * G::StageD;
-                mbar_expect_tx(&full[slot], (FIRST ? 1 : 2) * G::BoxBytes + (xo ? G::XBytes : 0));
-                tma_load_3d(st, mr, x0 - 2, y0 - 2, zp, &full[slot]);
-                if (!FIRST) tma_load_3d(st + G::BoxD, mp, x0 - 2, y0 - 2, zp, &full[slot]);
-                if (xo) tma_load_3d(st + 2 * G::BoxD, mx, x0, y0, zp, &full[slot]);
-                if (++slot == S) {
-                    slot = 0;
-                    phase ^= 1u;
-                    wrapped = true;
-                }
-            }
-        }
+        if (lane == 0) sp_produce<G, TY, S, FIRST, XDBL>(mr, mp, mx, g, ring, full, empty);
         return;
     }
 
@@ -307,14 +322,275 @@ __device__ __forceinline__ void spass_body(const CUtensorMap *mr, const CUtensor
     }
 }
 
-template <int PK, int TY, int S, bool XDBL>
-__global__ void __launch_bounds__(Sp<TY, S>::Threads, 1)
+// ---------------------------------------------------------------- FORM 2
+constexpr int kSpPX = kSpBX / 2;  // 34 pairs per box row
+__device__ __forceinline__ double sp_lds(const double *p) { return *p; }
+
+// The march of one CTA (FORM 2: two box rows per row warp, SoA plane buffers).
+template <int PK, int TY, int S, bool FIRST, bool XDBL>
+__device__ __forceinline__ void spass2_body(const CUtensorMap *mr, const CUtensorMap *mp, const CUtensorMap *mx,
+                                            const SpGeom &g, double off, double diag, double zc,
+                                            double *__restrict__ r_out, double *__restrict__ p_new,
+                                            double *__restrict__ x, double alpha, double alpha_prev, double beta,
+                                            double *ring, uint64_t *full, uint64_t *empty, double &rr, double &gam,
+                                            double &dlt)
+{
+    using G = Sp<TY, S, 2>;
+    constexpr int R = G::Rows, PL = R * kSpPX;  // one SoA plane: R rows x 34 pairs
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned pl = (unsigned)g.nx * (unsigned)g.ny;
+    const double malpha = -alpha;
+    if (warp == G::CWarps) {  // ---------------- producer
+        if (lane == 0) sp_produce<G, TY, S, FIRST, XDBL>(mr, mp, mx, g, ring, full, empty);
+        return;
+    }
+    // plane buffers [2 steps]: p even / odd cells, z' even / odd cells
+    double *const pe = ring + S * G::StageD, *const po = pe + 2 * PL;
+    double *const ze = po + 2 * PL, *const zo = ze + 2 * PL;
+    const int nthr = 32 * G::CWarps;
+    int slot = 0;
+    uint32_t phase = 0;
+    auto wait_stage = [&]() -> const double * {
+        mbar_wait(&full[slot], phase);
+        return ring + slot * G::StageD;
+    };
+    auto release_stage = [&]() {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (++slot == S) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    };
+    const bool edge = warp >= G::RowWarps;
+    for (int j = blockIdx.x; j < g.items(); j += gridDim.x) {
+        const int tile = j % (g.ntx * g.nty), chunk = j / (g.ntx * g.nty);
+        const int za = g.nz * chunk / g.nchunk, zb = g.nz * (chunk + 1) / g.nchunk;
+        const int x0 = (tile % g.ntx) * kSpTX, y0 = (tile / g.ntx) * TY;
+        const int L = zb - za, last = L + 3;
+        if (!edge) {
+            // ---- row warp: box rows a = 2w, b = 2w + 1; lane l owns the pair x0+2l
+            const int a = 2 * warp, b = a + 1;
+            const int jp = lane + 1;                       // pair index in the box row
+            const int ga = y0 - 2 + a, gx = x0 + 2 * lane;  // row b is ga + 1
+            const bool xin = gx < g.nx;
+            const bool qa = a >= 1 && a <= TY + 2, qb = b <= TY + 2;  // q / z' rows (b >= 1 always)
+            const bool ia = a >= 2 && a < TY + 2 && ga < g.ny, ib = b >= 2 && b < TY + 2 && ga + 1 < g.ny;
+            const bool inner = a >= 2 && b < TY + 2;      // both rows are tile rows (warp-uniform)
+            const bool oa = ia && xin, ob = ib && xin;     // owned pairs
+            const bool za_ok = ga >= 0 && ga < g.ny && xin, zb_ok = ga + 1 >= 0 && ga + 1 < g.ny && xin;
+            const int sa = a * kSpBX + 2 + 2 * lane;      // stage offset of row a's pair (row b: + kSpBX)
+            const int xa = 2 * G::BoxD + (a - 2) * kSpTX + 2 * lane;  // x box offset (row b: + kSpTX)
+            const int ea = a * kSpPX + jp, eb = ea + kSpPX;  // SoA plane index of the pair
+            unsigned gz = (unsigned)gx + (unsigned)g.nx * (unsigned)ga + pl * (unsigned)(za - 2);
+            double2 aqa = make_double2(0.0, 0.0), aqb = aqa, awa = aqa, awb = aqa, pca = aqa, pcb = aqa;
+            double2 zla = aqa, zlb = aqa, rwa = aqa, rwb = aqa;
+            // raw r_k / p_{k-1} (/ x) of the NEXT plane: taken right after the barrier,
+            // so the stage wait and its loads overlap the in-plane arithmetic
+            double2 nra, nrb, npoa = aqa, npob = aqa, nxoa = aqa, nxob = aqa;
+            auto take2 = [&](int s) {
+                const double *st = wait_stage();
+                nra = sp_lds2(st + sa);
+                nrb = sp_lds2(st + sa + kSpBX);
+                if (!FIRST) {
+                    npoa = sp_lds2(st + G::BoxD + sa);
+                    npob = sp_lds2(st + G::BoxD + sa + kSpBX);
+                }
+                if (XDBL && inner && s >= 2 && s <= L + 1) {
+                    nxoa = sp_lds2(st + xa);
+                    nxob = sp_lds2(st + xa + kSpTX);
+                }
+                release_stage();
+            };
+            auto step = [&](auto steady, int s) {
+                constexpr bool ST = decltype(steady)::value;
+                const int zq = za - 3 + s;
+                // this plane's raw values were taken at the end of the previous step
+                const double2 ra = nra, rb = nrb, poa = npoa, pob = npob, xoa = nxoa, xob = nxob;
+                const bool stp = ST || (s >= 2 && s <= L + 1);  // p / x of this plane are stored
+                const double2 pa = make_double2(sp_form<PK, FIRST>(ra.x, poa.x, zc, beta),
+                                                sp_form<PK, FIRST>(ra.y, poa.y, zc, beta));
+                const double2 pb = make_double2(sp_form<PK, FIRST>(rb.x, pob.x, zc, beta),
+                                                sp_form<PK, FIRST>(rb.y, pob.y, zc, beta));
+                const int bo = (s & 1) * PL;
+                pe[bo + ea] = pa.x;
+                po[bo + ea] = pa.y;
+                pe[bo + eb] = pb.x;
+                po[bo + eb] = pb.y;
+                if (stp) {
+                    if (oa) sp_stg2(p_new + gz, pa);
+                    if (ob) sp_stg2(p_new + gz + g.nx, pb);
+                    if (XDBL) {  // x = (x + alpha_prev p_{k-1}) + alpha p_k (src/solver.py:155, twice)
+                        if (oa)
+                            sp_stg2(x + gz, make_double2(__fma_rn(alpha, pa.x, __fma_rn(alpha_prev, poa.x, xoa.x)),
+                                                         __fma_rn(alpha, pa.y, __fma_rn(alpha_prev, poa.y, xoa.y))));
+                        if (ob)
+                            sp_stg2(x + gz + g.nx,
+                                    make_double2(__fma_rn(alpha, pb.x, __fma_rn(alpha_prev, pob.x, xob.x)),
+                                                 __fma_rn(alpha, pb.y, __fma_rn(alpha_prev, pob.y, xob.y))));
+                    }
+                }
+                // ---- q(zq) complete, r_{k+1}, z' (+ r.r, gamma); w(zq-1) complete (+ delta)
+                const bool zin = ST || (unsigned)zq < (unsigned)g.nz;
+                const bool str = ST || (s >= 3 && s <= L + 2), std_ = ST || s >= 4;
+                auto finish = [&](const double2 &p2, const double2 &aq, const double2 &rw, const double2 &aw,
+                                  const double2 &zl, bool zok, bool own, unsigned o, int e, double2 &zpark) {
+                    const double q0 = __fma_rn(off, p2.x, aq.x), q1 = __fma_rn(off, p2.y, aq.y);
+                    const double r0 = __fma_rn(malpha, q0, rw.x), r1 = __fma_rn(malpha, q1, rw.y);  // :157
+                    const double2 zn = zok && zin ? make_double2(sp_z<PK>(r0, zc), sp_z<PK>(r1, zc))
+                                                  : make_double2(0.0, 0.0);
+                    ze[bo + e] = zn.x;
+                    zo[bo + e] = zn.y;
+                    if (own && str) {
+                        sp_stg2(r_out + o, make_double2(r0, r1));
+                        rr = __fma_rn(r0, r0, rr);  // :158
+                        rr = __fma_rn(r1, r1, rr);
+                        gam = __fma_rn(r0, zn.x, gam);  // :163-164
+                        gam = __fma_rn(r1, zn.y, gam);
+                    }
+                    if (own && std_) {
+                        dlt = __fma_rn(zl.x, __fma_rn(off, zn.x, aw.x), dlt);
+                        dlt = __fma_rn(zl.y, __fma_rn(off, zn.y, aw.y), dlt);
+                    }
+                    zpark = zn;
+                };
+                double2 zna = make_double2(0.0, 0.0), znb = zna;
+                if (ST || s >= 1) {
+                    if (ST || qa) finish(pa, aqa, rwa, awa, zla, za_ok, oa, gz - pl, ea, zna);
+                    if (ST || qb) finish(pb, aqb, rwb, awb, zlb, zb_ok, ob, gz - pl + g.nx, eb, znb);
+                }
+                rwa = ra;
+                rwb = rb;
+                gz += pl;
+                sp_bar(nthr);
+                if (s < last) take2(s + 1);
+                // ---- in-plane terms (k-1, j-1, i-1, i, i+1, j+1) of q(zp) and w(zq)
+                const double *Pe = pe + bo, *Po = po + bo, *Ze = ze + bo, *Zo = zo + bo;
+                auto inplane = [&](const double2 &c, const double2 &zm, const double2 &ym, const double2 &yp,
+                                   double xl, double xr) {
+                    double a0 = off * zm.x, a1 = off * zm.y;
+                    a0 = __fma_rn(off, ym.x, a0);
+                    a1 = __fma_rn(off, ym.y, a1);
+                    a0 = __fma_rn(off, xl, a0);
+                    a1 = __fma_rn(off, c.x, a1);
+                    a0 = __fma_rn(diag, c.x, a0);
+                    a1 = __fma_rn(diag, c.y, a1);
+                    a0 = __fma_rn(off, c.y, a0);
+                    a1 = __fma_rn(off, xr, a1);
+                    a0 = __fma_rn(off, yp.x, a0);
+                    a1 = __fma_rn(off, yp.y, a1);
+                    return make_double2(a0, a1);
+                };
+                if (ST || qa) {
+                    const double2 ym = make_double2(sp_lds(Pe + ea - kSpPX), sp_lds(Po + ea - kSpPX));
+                    aqa = inplane(pa, pca, ym, pb, sp_lds(Po + ea - 1), sp_lds(Pe + ea + 1));
+                }
+                if (ST || qb) {
+                    const double2 yp = make_double2(sp_lds(Pe + eb + kSpPX), sp_lds(Po + eb + kSpPX));
+                    aqb = inplane(pb, pcb, pa, yp, sp_lds(Po + eb - 1), sp_lds(Pe + eb + 1));
+                }
+                pca = pa;
+                pcb = pb;
+                if (ST || (inner && s >= 1)) {
+                    const double2 ym = make_double2(sp_lds(Ze + ea - kSpPX), sp_lds(Zo + ea - kSpPX));
+                    const double2 yp = make_double2(sp_lds(Ze + eb + kSpPX), sp_lds(Zo + eb + kSpPX));
+                    awa = inplane(zna, zla, ym, znb, sp_lds(Zo + ea - 1), sp_lds(Ze + ea + 1));
+                    awb = inplane(znb, zlb, zna, yp, sp_lds(Zo + eb - 1), sp_lds(Ze + eb + 1));
+                    zla = zna;
+                    zlb = znb;
+                }
+            };
+            take2(0);
+            int s = 0;
+            if (inner) {
+                for (; s < 4 && s <= last; ++s) step(std::false_type{}, s);
+                for (; s <= L + 1; ++s) step(std::true_type{}, s);
+            }
+            for (; s <= last; ++s) step(std::false_type{}, s);
+        } else {
+            // ---- edge warp: lane = box row; the halo pairs x0-2 (left) and x0+64
+            // (right), q / z' of their inner cells x0-1 and x0+64
+            const int e = (warp - G::RowWarps) * 32 + lane;
+            const bool act = e < R;
+            const int row = act ? e : 0;
+            const int gy = y0 - 2 + row;
+            const bool yin = gy >= 0 && gy < g.ny;
+            const bool zl_ok = yin && x0 - 1 >= 0, zr_ok = yin && x0 + kSpTX < g.nx;
+            const bool q = act && row >= 1 && row <= TY + 2;
+            const int so = row * kSpBX, ei = row * kSpPX;  // stage / SoA offsets of the row
+            double aqL = 0.0, aqR = 0.0, pcL = 0.0, pcR = 0.0, rwL = 0.0, rwR = 0.0;
+            double2 nrL = make_double2(0.0, 0.0), nrR = nrL, noL = nrL, noR = nrL;
+            auto take_e = [&]() {  // the next plane's raw halo pairs (see take2)
+                const double *st = wait_stage();
+                if (act) {
+                    nrL = sp_lds2(st + so);
+                    nrR = sp_lds2(st + so + kSpBX - 2);
+                    if (!FIRST) {
+                        noL = sp_lds2(st + G::BoxD + so);
+                        noR = sp_lds2(st + G::BoxD + so + kSpBX - 2);
+                    }
+                }
+                release_stage();
+            };
+            take_e();
+            for (int s = 0; s <= last; ++s) {
+                const int zq = za - 3 + s;
+                const double2 rL = nrL, rR = nrR, oL = noL, oR = noR;
+                const int bo = (s & 1) * PL;
+                const double2 pL = make_double2(sp_form<PK, FIRST>(rL.x, oL.x, zc, beta),
+                                                sp_form<PK, FIRST>(rL.y, oL.y, zc, beta));
+                const double2 pR = make_double2(sp_form<PK, FIRST>(rR.x, oR.x, zc, beta),
+                                                sp_form<PK, FIRST>(rR.y, oR.y, zc, beta));
+                if (act) {
+                    pe[bo + ei] = pL.x;
+                    po[bo + ei] = pL.y;
+                    pe[bo + ei + kSpPX - 1] = pR.x;
+                    po[bo + ei + kSpPX - 1] = pR.y;
+                }
+                if (q && s >= 1) {
+                    const bool zin = (unsigned)zq < (unsigned)g.nz;
+                    const double rl = __fma_rn(malpha, __fma_rn(off, pL.y, aqL), rwL);
+                    const double rr_ = __fma_rn(malpha, __fma_rn(off, pR.x, aqR), rwR);
+                    zo[bo + ei] = zl_ok && zin ? sp_z<PK>(rl, zc) : 0.0;
+                    ze[bo + ei + kSpPX - 1] = zr_ok && zin ? sp_z<PK>(rr_, zc) : 0.0;
+                }
+                rwL = rL.y;
+                rwR = rR.x;
+                sp_bar(nthr);
+                if (s < last) take_e();
+                if (q) {
+                    const double *Pe = pe + bo, *Po = po + bo;
+                    double a0 = off * pcL;  // x0-1: k-1, j-1, i-1 (own), i, i+1 (row warp), j+1
+                    a0 = __fma_rn(off, sp_lds(Po + ei - kSpPX), a0);
+                    a0 = __fma_rn(off, pL.x, a0);
+                    a0 = __fma_rn(diag, pL.y, a0);
+                    a0 = __fma_rn(off, sp_lds(Pe + ei + 1), a0);
+                    a0 = __fma_rn(off, sp_lds(Po + ei + kSpPX), a0);
+                    aqL = a0;
+                    const int er = ei + kSpPX - 1;
+                    double a1 = off * pcR;  // x0+64: i-1 (row warp), i, i+1 (own)
+                    a1 = __fma_rn(off, sp_lds(Pe + er - kSpPX), a1);
+                    a1 = __fma_rn(off, sp_lds(Po + er - 1), a1);
+                    a1 = __fma_rn(diag, pR.x, a1);
+                    a1 = __fma_rn(off, pR.y, a1);
+                    a1 = __fma_rn(off, sp_lds(Pe + er + kSpPX), a1);
+                    aqR = a1;
+                }
+                pcL = pL.y;
+                pcR = pR.x;
+            }
+        }
+    }
+}
+
+template <int PK, int TY, int S, bool XDBL, int FORM = 2>
+__global__ void __launch_bounds__(Sp<TY, S, FORM>::Threads, Sp<TY, S, FORM>::MinBlocks)
     cg_spass_kernel(const __grid_constant__ CUtensorMap mr, const __grid_constant__ CUtensorMap mp,
                     const __grid_constant__ CUtensorMap mx, SpGeom g, double off, double diag, double zc,
                     double *__restrict__ r_out, double *__restrict__ p_new, double *__restrict__ x, CgScalars *sc,
                     double *partials, CgTickets *tk, int use_cond, cudaGraphConditionalHandle cond)
 {
-    using G = Sp<TY, S>;
+    using G = Sp<TY, S, FORM>;
     extern __shared__ unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full[S], empty[S];
     __shared__ double red[32];
@@ -334,12 +610,21 @@ __global__ void __launch_bounds__(Sp<TY, S>::Threads, 1)
     __syncthreads();
     double rr = 0.0, gam = 0.0, dlt = 0.0;
     const double alpha = sc->alpha, alpha_prev = sc->alpha_prev, beta = sc->beta;
-    if (!XDBL && sc->it == 0)
-        spass_body<PK, TY, S, true, false>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev, 0.0,
-                                           ring, full, empty, rr, gam, dlt);
-    else
-        spass_body<PK, TY, S, false, XDBL>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev, beta,
-                                           ring, full, empty, rr, gam, dlt);
+    if (FORM == 1) {
+        if (!XDBL && sc->it == 0)
+            spass_body<PK, TY, S, true, false>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev,
+                                               0.0, ring, full, empty, rr, gam, dlt);
+        else
+            spass_body<PK, TY, S, false, XDBL>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev,
+                                               beta, ring, full, empty, rr, gam, dlt);
+    } else {
+        if (!XDBL && sc->it == 0)
+            spass2_body<PK, TY, S, true, false>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev,
+                                                0.0, ring, full, empty, rr, gam, dlt);
+        else
+            spass2_body<PK, TY, S, false, XDBL>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev,
+                                                beta, ring, full, empty, rr, gam, dlt);
+    }
     rr = block_sum<G::Threads>(rr, red);
     gam = block_sum<G::Threads>(gam, red);
     dlt = block_sum<G::Threads>(dlt, red);
