@@ -14,8 +14,10 @@
 #include <algorithm>
 
 #include <cmath>
+#include <cstring>
 
 #include "cf_common.cuh"
+#include "cf_tma.cuh"
 
 namespace cf {
 
@@ -158,6 +160,8 @@ __global__ void __launch_bounds__(kFaceThreads, 4) advect_kernel(Vel3 in, double
         if (f < total[2]) advect_face<POW2>(in, in.c[2], nw, sz, 2, f, h, inv_h, dt, lx, ly, lz);
     }
 }
+
+#include "cf_advect.cuh"
 
 static bool is_pow2(double h)
 {
@@ -504,6 +508,33 @@ static int advect(const double *u, const double *v, const double *w, double *nu,
     CF_REQUIRE(slab_ok(sz) && h > 0 && pitches_ok(sz, ldu, ldv, ldw), "advect: bad slab/pitch");
     CF_REQUIRE(nu != u && nv != v && nw != w, "advect: output aliases input");
     Vel3 in = make_vel(u, v, w, sz, ldu, ldv, ldw);
+    // TMA-fed z-march (cf_advect.cuh) for the single domain; CF_ADVECT=global
+    // selects the global-gather kernel (also the z-slab form)
+    const char *ae = getenv("CF_ADVECT");
+    const bool single = sz.H == 0 && sz.z0 == 0 && sz.z1 == sz.nz;
+    if (single && is_pow2(h) && sz.nx >= 2 && sz.ny >= 2 && sz.nz >= 2 && !(ae && !strcmp(ae, "global"))) {
+        CUtensorMap mu, mv, mw;
+        const bool ok = make_map_pitched(&mu, u, sz.nx + 1, sz.ny, sz.nz, ldu, kAdvBX, kAdvBY) &&
+                        make_map_pitched(&mv, v, sz.nx, sz.ny + 1, sz.nz, ldv, kAdvBX, kAdvBY) &&
+                        make_map_pitched(&mw, w, sz.nx, sz.ny, sz.nz + 1, ldw, kAdvBX, kAdvBY);
+        if (ok) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(advect_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kAdvSmem);
+                attr = true;
+            }
+            AdvGeom ag{(sz.nx + kAdvTX - 1) / kAdvTX, (sz.ny + kAdvTY - 1) / kAdvTY, 1};
+            const int bps = blocks_per_sm((const void *)advect_tma_kernel<true>, kAdvThreads, kAdvSmem);
+            ag.nchunk = wave_chunks((long long)ag.ntx * ag.nty, sz.nz + 1, (long long)num_sms() * (bps > 0 ? bps : 1),
+                                    8);
+            const int ctas = ag.ntx * ag.nty * ag.nchunk;
+            advect_tma_kernel<true><<<ctas, kAdvThreads, kAdvSmem, as_stream(stream)>>>(mu, mv, mw, in, nu, nv, nw, sz,
+                                                                                      ag, h, 1.0 / h, dt);
+            CF_CHECK_LAUNCH("advect_tma_kernel");
+            return CF_OK;
+        }
+    }
     long long faces = (long long)(sz.nx + 1) * (sz.ny + 1) * (sz.z1 - sz.z0 + 1);
     const int grid = grid_for(faces, kFaceThreads, 8);
     if (is_pow2(h))

@@ -49,6 +49,22 @@ bool make_map_promo(CUtensorMap *map, const double *base, int nx, int ny, int pl
     return r == CUDA_SUCCESS;
 }
 
+bool make_map_pitched(CUtensorMap *map, const double *base, int nx, int ny, int planes, int pitch, int bx, int by)
+{
+    EncodeTiledFn enc = encode_fn();
+    if (!enc || !base || pitch < nx) return false;
+    const cuuint64_t row = (cuuint64_t)pitch * sizeof(double);
+    if (row % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {row, row * (cuuint64_t)ny};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 TmaGeom tma_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, int blocks_per_sm)
 {
     TmaGeom g;

@@ -107,6 +107,9 @@ bool make_map(CUtensorMap *map, const double *base, int nx, int ny, int planes, 
 // the same with an explicit L2 promotion (0 / 64 / 128 / 256 bytes; make_map uses 256)
 bool make_map_promo(CUtensorMap *map, const double *base, int nx, int ny, int planes, int bx, int by, int promo);
 
+// the same over rows of `pitch` elements (padded rows: the velocity components)
+bool make_map_pitched(CUtensorMap *map, const double *base, int nx, int ny, int planes, int pitch, int bx, int by);
+
 // Host: chunk count and grid for a kernel with `blocks_per_sm` residency.
 TmaGeom tma_geom(int nx, int ny, int nz, int lo_halo, int hi_halo, int blocks_per_sm);
 

@@ -32,6 +32,7 @@ def alg_bytes(name, n):
         (r"cg_init_flat", 32 * N, "b read; r, x, (z) written"),
         (r"cg_x_fixup", 24 * N, "x, p read; x written (only after an odd count)"),
         (r"advect_kernel", 48 * F, "3 components read (gathers) and written"),
+        (r"advect_tma_kernel", 48 * F, "3 components read (TMA boxes) and written"),
         (r"diffuse_kernel", 48 * F, "3 components read and written"),
         (r"divergence_kernel", 24 * F + 8 * N, "3 components read; b written"),
         (r"correct_kernel", 48 * F + 8 * N, "3 components + p read; 3 components written"),
