@@ -90,4 +90,51 @@ __device__ __forceinline__ void scalar_after_init(CgScalars *sc, double bb, doub
     }
 }
 
+// The single-reduction (Chronopoulos-Gear) scalars of the pass forms
+// (cf_cg_pass.cuh, cf_cg_lpass.cuh, cf_cg_spass.cuh; z-slab: cf_p2p.cu).
+// After the pass's reduction: stop test on r_{k+1} (src/solver.py:158-162),
+// then the next pass's beta and alpha by the single-reduction identity.
+__device__ __forceinline__ void scalar_after_pass(CgScalars *sc, double rr, double gam, double dlt)
+{
+    sc->rr = rr;
+    sc->it += 1;
+    sc->res = sqrt(rr) / sc->norm_b;
+    if (sc->res <= sc->tol) {
+        sc->status = ST_CONVERGED;
+        sc->done = 1;
+        return;
+    }
+    if (sc->it >= sc->max_iter) {
+        sc->status = ST_MAXITER;
+        sc->done = 1;
+        return;
+    }
+    const double beta = gam / sc->rz;                 // src/solver.py:165
+    const double pap = dlt - beta * gam / sc->alpha;  // p_{k+1}.A p_{k+1}
+    sc->pap = pap;
+    if (pap <= 0.0) {  // src/solver.py:151-152
+        sc->status = ST_BREAKDOWN;
+        sc->done = 1;
+        return;
+    }
+    sc->alpha_prev = sc->alpha;
+    sc->alpha = gam / pap;  // :153
+    sc->beta = beta;
+    sc->rz = gam;
+}
+
+// After the init pass: |b|, gamma_0, delta_0 -> alpha_0 = gamma_0 / delta_0.
+__device__ __forceinline__ void scalar_after_pass_init(CgScalars *sc, double bb, double gam, double dlt)
+{
+    scalar_after_init(sc, bb, gam);
+    if (sc->done) return;
+    sc->pap = dlt;
+    if (dlt <= 0.0) {
+        sc->status = ST_BREAKDOWN;
+        sc->done = 1;
+        return;
+    }
+    sc->alpha = gam / dlt;
+}
+
 }  // namespace cf

@@ -78,6 +78,17 @@ struct SpGeom {
     __host__ __device__ int items() const { return ntx * nty * nchunk; }
 };
 
+// z-slab form (cf_p2p.cu): the slab's arrays hold 2 halo planes below and
+// above its nz owned planes; a missing neighbour's halo stays zero (the
+// Dirichlet ghost).  Boundary planes 0, 1 and nz-2, nz-1 of r_{k+1} and p_k
+// are also stored straight into the neighbours' halo planes (peer memory).
+struct SpSlabIO {
+    int zoff;                // TMA plane coordinate of local plane 0 (2 in a slab array)
+    int lo_ghost, hi_ghost;  // planes < 0 / >= nz are ghosts (no neighbour there)
+    double *lo_r, *lo_p;     // the lower neighbour's planes matching our planes 0, 1 (null: none)
+    double *hi_r, *hi_p;     // the upper neighbour's planes matching our planes nz-2, nz-1
+};
+
 __device__ __forceinline__ double2 sp_lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
 __device__ __forceinline__ void sp_sts2(double *p, double2 v) { *reinterpret_cast<double2 *>(p) = v; }
 __device__ __forceinline__ void sp_stg2(double *p, double2 v) { *reinterpret_cast<double2 *>(p) = v; }
@@ -98,7 +109,8 @@ __device__ __forceinline__ double sp_form(double r, double po, double zc, double
 // through the ring (the consumers release a stage as soon as they have read it).
 template <class G, int TY, int S, bool FIRST, bool XDBL>
 __device__ __forceinline__ void sp_produce(const CUtensorMap *mr, const CUtensorMap *mp, const CUtensorMap *mx,
-                                           const SpGeom &g, double *ring, uint64_t *full, uint64_t *empty)
+                                           const SpGeom &g, double *ring, uint64_t *full, uint64_t *empty,
+                                           int bid, int nblk, int zoff)
 {
     prefetch_map(mr);
     if (!FIRST) prefetch_map(mp);
@@ -106,14 +118,14 @@ __device__ __forceinline__ void sp_produce(const CUtensorMap *mr, const CUtensor
     int slot = 0;
     uint32_t phase = 0;
     bool wrapped = false;  // the ring has been filled once: wait for releases
-    for (int j = blockIdx.x; j < g.items(); j += gridDim.x) {
+    for (int j = bid; j < g.items(); j += nblk) {
         const int tile = j % (g.ntx * g.nty), chunk = j / (g.ntx * g.nty);
         const int za = g.nz * chunk / g.nchunk, zb = g.nz * (chunk + 1) / g.nchunk;
         const int x0 = (tile % g.ntx) * kSpTX, y0 = (tile / g.ntx) * TY;
         for (int s = 0; s < zb - za + 4; ++s) {
             if (wrapped) mbar_wait(&empty[slot], phase ^ 1u);
-            const int zp = za - 2 + s;
-            const bool xo = XDBL && zp >= za && zp < zb;
+            const int zp = za - 2 + s + zoff;
+            const bool xo = XDBL && zp - zoff >= za && zp - zoff < zb;
             double *st = ring + slot * G::StageD;
             mbar_expect_tx(&full[slot], (FIRST ? 1 : 2) * G::BoxBytes + (xo ? G::XBytes : 0));
             tma_load_3d(st, mr, x0 - 2, y0 - 2, zp, &full[slot]);
@@ -143,7 +155,7 @@ __device__ __forceinline__ void spass_body(const CUtensorMap *mr, const CUtensor
     const double malpha = -alpha;
 
     if (warp == G::CWarps) {  // ---------------- producer: one lane drives the ring
-        if (lane == 0) sp_produce<G, TY, S, FIRST, XDBL>(mr, mp, mx, g, ring, full, empty);
+        if (lane == 0) sp_produce<G, TY, S, FIRST, XDBL>(mr, mp, mx, g, ring, full, empty, blockIdx.x, gridDim.x, 0);
         return;
     }
 
@@ -327,13 +339,16 @@ constexpr int kSpPX = kSpBX / 2;  // 34 pairs per box row
 __device__ __forceinline__ double sp_lds(const double *p) { return *p; }
 
 // The march of one CTA (FORM 2: two box rows per row warp, SoA plane buffers).
-template <int PK, int TY, int S, bool FIRST, bool XDBL>
+// SLAB: the z-slab form (bid / nblk: this slab's block range, io: halo
+// offsets, ghosts and the neighbours' planes); the single domain passes
+// blockIdx.x / gridDim.x and {0, 1, 1, null...}.
+template <int PK, int TY, int S, bool FIRST, bool XDBL, bool SLAB = false>
 __device__ __forceinline__ void spass2_body(const CUtensorMap *mr, const CUtensorMap *mp, const CUtensorMap *mx,
                                             const SpGeom &g, double off, double diag, double zc,
                                             double *__restrict__ r_out, double *__restrict__ p_new,
                                             double *__restrict__ x, double alpha, double alpha_prev, double beta,
                                             double *ring, uint64_t *full, uint64_t *empty, double &rr, double &gam,
-                                            double &dlt)
+                                            double &dlt, int bid, int nblk, const SpSlabIO &io)
 {
     using G = Sp<TY, S, 2>;
     constexpr int R = G::Rows, PL = R * kSpPX;  // one SoA plane: R rows x 34 pairs
@@ -341,9 +356,19 @@ __device__ __forceinline__ void spass2_body(const CUtensorMap *mr, const CUtenso
     const unsigned pl = (unsigned)g.nx * (unsigned)g.ny;
     const double malpha = -alpha;
     if (warp == G::CWarps) {  // ---------------- producer
-        if (lane == 0) sp_produce<G, TY, S, FIRST, XDBL>(mr, mp, mx, g, ring, full, empty);
+        if (lane == 0) sp_produce<G, TY, S, FIRST, XDBL>(mr, mp, mx, g, ring, full, empty, bid, nblk, io.zoff);
         return;
     }
+    // z' vanishes on ghost planes only (a neighbour's halo plane is real data)
+    auto zreal = [&](int zq) { return (zq >= 0 || !io.lo_ghost) && (zq < g.nz || !io.hi_ghost); };
+    // boundary planes also into the neighbours' halo planes (SLAB)
+    const unsigned top = (unsigned)g.nx * (unsigned)g.ny * (unsigned)(g.nz - 2);
+    auto peer2 = [&](double *lo, double *hi, int z, unsigned o, double2 v) {
+        if (!SLAB) return;
+        if (lo && z < 2) sp_stg2(lo + o, v);
+        if (hi && z >= g.nz - 2) sp_stg2(hi + (o - top), v);
+    };
+
     // plane buffers [2 steps]: p even / odd cells, z' even / odd cells
     double *const pe = ring + S * G::StageD, *const po = pe + 2 * PL;
     double *const ze = po + 2 * PL, *const zo = ze + 2 * PL;
@@ -363,7 +388,7 @@ __device__ __forceinline__ void spass2_body(const CUtensorMap *mr, const CUtenso
         }
     };
     const bool edge = warp >= G::RowWarps;
-    for (int j = blockIdx.x; j < g.items(); j += gridDim.x) {
+    for (int j = bid; j < g.items(); j += nblk) {
         const int tile = j % (g.ntx * g.nty), chunk = j / (g.ntx * g.nty);
         const int za = g.nz * chunk / g.nchunk, zb = g.nz * (chunk + 1) / g.nchunk;
         const int x0 = (tile % g.ntx) * kSpTX, y0 = (tile / g.ntx) * TY;
@@ -418,8 +443,15 @@ __device__ __forceinline__ void spass2_body(const CUtensorMap *mr, const CUtenso
                 pe[bo + eb] = pb.x;
                 po[bo + eb] = pb.y;
                 if (stp) {
-                    if (oa) sp_stg2(p_new + gz, pa);
-                    if (ob) sp_stg2(p_new + gz + g.nx, pb);
+                    const int zp = za - 2 + s;
+                    if (oa) {
+                        sp_stg2(p_new + gz, pa);
+                        peer2(io.lo_p, io.hi_p, zp, gz, pa);
+                    }
+                    if (ob) {
+                        sp_stg2(p_new + gz + g.nx, pb);
+                        peer2(io.lo_p, io.hi_p, zp, gz + g.nx, pb);
+                    }
                     if (XDBL) {  // x = (x + alpha_prev p_{k-1}) + alpha p_k (src/solver.py:155, twice)
                         if (oa)
                             sp_stg2(x + gz, make_double2(__fma_rn(alpha, pa.x, __fma_rn(alpha_prev, poa.x, xoa.x)),
@@ -431,7 +463,7 @@ __device__ __forceinline__ void spass2_body(const CUtensorMap *mr, const CUtenso
                     }
                 }
                 // ---- q(zq) complete, r_{k+1}, z' (+ r.r, gamma); w(zq-1) complete (+ delta)
-                const bool zin = ST || (unsigned)zq < (unsigned)g.nz;
+                const bool zin = ST || zreal(zq);
                 const bool str = ST || (s >= 3 && s <= L + 2), std_ = ST || s >= 4;
                 auto finish = [&](const double2 &p2, const double2 &aq, const double2 &rw, const double2 &aw,
                                   const double2 &zl, bool zok, bool own, unsigned o, int e, double2 &zpark) {
@@ -443,6 +475,7 @@ __device__ __forceinline__ void spass2_body(const CUtensorMap *mr, const CUtenso
                     zo[bo + e] = zn.y;
                     if (own && str) {
                         sp_stg2(r_out + o, make_double2(r0, r1));
+                        peer2(io.lo_r, io.hi_r, zq, o, make_double2(r0, r1));
                         rr = __fma_rn(r0, r0, rr);  // :158
                         rr = __fma_rn(r1, r1, rr);
                         gam = __fma_rn(r0, zn.x, gam);  // :163-164
@@ -548,7 +581,7 @@ __device__ __forceinline__ void spass2_body(const CUtensorMap *mr, const CUtenso
                     po[bo + ei + kSpPX - 1] = pR.y;
                 }
                 if (q && s >= 1) {
-                    const bool zin = (unsigned)zq < (unsigned)g.nz;
+                    const bool zin = zreal(zq);
                     const double rl = __fma_rn(malpha, __fma_rn(off, pL.y, aqL), rwL);
                     const double rr_ = __fma_rn(malpha, __fma_rn(off, pR.x, aqR), rwR);
                     zo[bo + ei] = zl_ok && zin ? sp_z<PK>(rl, zc) : 0.0;
@@ -618,12 +651,13 @@ __global__ void __launch_bounds__(Sp<TY, S, FORM>::Threads, Sp<TY, S, FORM>::Min
             spass_body<PK, TY, S, false, XDBL>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev,
                                                beta, ring, full, empty, rr, gam, dlt);
     } else {
+        const SpSlabIO io{0, 1, 1, nullptr, nullptr, nullptr, nullptr};
         if (!XDBL && sc->it == 0)
             spass2_body<PK, TY, S, true, false>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev,
-                                                0.0, ring, full, empty, rr, gam, dlt);
+                                                0.0, ring, full, empty, rr, gam, dlt, blockIdx.x, gridDim.x, io);
         else
             spass2_body<PK, TY, S, false, XDBL>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev,
-                                                beta, ring, full, empty, rr, gam, dlt);
+                                                beta, ring, full, empty, rr, gam, dlt, blockIdx.x, gridDim.x, io);
     }
     rr = block_sum<G::Threads>(rr, red);
     gam = block_sum<G::Threads>(gam, red);

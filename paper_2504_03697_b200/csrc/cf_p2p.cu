@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "cf_cg_common.cuh"
@@ -50,11 +51,12 @@ namespace cf {
 #include "cf_cg_tma.cuh"
 #include "cf_cg_pair.cuh"
 #include "cf_cg_lean.cuh"
+#include "cf_cg_spass.cuh"
 
 constexpr int kMaxRanks = 8;
 
 struct Mailbox {
-    double val[2][kMaxRanks][2];           // [phase parity][sender][component]
+    double val[2][kMaxRanks][3];           // [phase parity][sender][component] (3: the single pass)
     unsigned long long seq[2][kMaxRanks];  // phase number posted by each sender
 };
 
@@ -159,26 +161,26 @@ constexpr int ST_PEER_TIMEOUT = 4;
 
 // Thread 0 of a slab's last block: post `v` (ncomp values) to every rank,
 // wait for every rank's post of this phase, return the rank-ordered sums.
-__device__ __forceinline__ void p2p_allreduce(const P2PSet &ps, const P2PSlab &sl, int ncomp, const double *v,
-                                              double *out)
+__device__ __forceinline__ void allreduce_core(int nranks, Mailbox *const *mail, CgScalars *sc, int me, int ncomp,
+                                               const double *v, double *out)
 {
-    if (ps.nranks == 1) {  // one rank (single-slab run): nothing to exchange
+    if (nranks == 1) {  // one rank (single-slab run): nothing to exchange
         for (int c = 0; c < ncomp; ++c) out[c] = 0.0 + v[c];
         return;
     }
-    const unsigned long long ph = ++sl.sc->phase;
-    const int par = (int)(ph & 1ull), me = sl.rank;
-    for (int q = 0; q < ps.nranks; ++q)
-        for (int c = 0; c < ncomp; ++c) st_relaxed_sys(&ps.mail[q]->val[par][me][c], v[c]);
-    for (int q = 0; q < ps.nranks; ++q) st_release_sys(&ps.mail[q]->seq[par][me], ph);
-    Mailbox *mine = ps.mail[me];
+    const unsigned long long ph = ++sc->phase;
+    const int par = (int)(ph & 1ull);
+    for (int q = 0; q < nranks; ++q)
+        for (int c = 0; c < ncomp; ++c) st_relaxed_sys(&mail[q]->val[par][me][c], v[c]);
+    for (int q = 0; q < nranks; ++q) st_release_sys(&mail[q]->seq[par][me], ph);
+    Mailbox *mine = mail[me];
     const unsigned long long t0 = globaltimer_ns();
-    for (int q = 0; q < ps.nranks; ++q) {
+    for (int q = 0; q < nranks; ++q) {
         while (ld_acquire_sys(&mine->seq[par][q]) < ph) {
             __nanosleep(64);
             if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
-                sl.sc->status = ST_PEER_TIMEOUT;
-                sl.sc->done = 1;
+                sc->status = ST_PEER_TIMEOUT;
+                sc->done = 1;
                 for (int c = 0; c < ncomp; ++c) out[c] = __longlong_as_double(0x7ff8000000000000ll);
                 return;
             }
@@ -186,9 +188,15 @@ __device__ __forceinline__ void p2p_allreduce(const P2PSet &ps, const P2PSlab &s
     }
     for (int c = 0; c < ncomp; ++c) {
         double sum = 0.0;
-        for (int q = 0; q < ps.nranks; ++q) sum = sum + ld_relaxed_sys(&mine->val[par][q][c]);
+        for (int q = 0; q < nranks; ++q) sum = sum + ld_relaxed_sys(&mine->val[par][q][c]);
         out[c] = sum;
     }
+}
+
+__device__ __forceinline__ void p2p_allreduce(const P2PSet &ps, const P2PSlab &sl, int ncomp, const double *v,
+                                              double *out)
+{
+    allreduce_core(ps.nranks, ps.mail, sl.sc, sl.rank, ncomp, v, out);
 }
 
 // ---------------------------------------------------------------- init
@@ -430,6 +438,213 @@ __global__ void __launch_bounds__(256) p2p_x_fixup(const P2PSet *__restrict__ ps
         sl.x[i] = sl.x[i] + alpha * sl.p1[i];  // src/solver.py:155
 }
 
+
+// ================================================================ single pass over z-slabs
+// The default single-domain CG form (cf_cg_spass.cuh: one TMA-fed
+// Chronopoulos-Gear pass per iteration, 40 N) on z-slabs.  Each slab array
+// carries TWO halo planes below and above its owned planes (the pass reads
+// r_k and p_{k-1} on planes z0-2 .. z1+1); the pass stores its boundary planes
+// 0, 1 / nz-2, nz-1 of r_{k+1} and p_k also into the neighbours' halo planes
+// (peer stores as they are produced), and the slab's last block all-reduces
+// (r.r, gamma, delta) over the mailboxes -- one collective per iteration
+// instead of two.  A missing neighbour's halo planes stay zero (the Dirichlet
+// ghost), exactly as the single domain's out-of-range TMA boxes.
+constexpr int kSpSlabTY = 16, kSpSlabS = 6;
+using SpSlabCfg = Sp<kSpSlabTY, kSpSlabS, 2>;
+
+struct SpSlab {
+    CUtensorMap m_r[2], m_p[2], m_x;  // maps over the slab arrays (nz + 4 planes, the lowest halo plane first)
+    SpGeom g;                         // nz = owned planes
+    int blk, blk_init;                // first block of this slab in the pass / init launches
+    double *r[2], *p[2], *x;          // owned plane 0 (two halo planes below it in memory)
+    const double *b;
+    double *lo[2][2], *hi[2][2];      // [r | p][buffer]: the neighbours' planes matching ours (null: none)
+    int lo_ghost, hi_ghost;
+    double *partials;
+    CgTickets *tk;
+    CgScalars *sc;
+    int rank;
+};
+
+struct SpSet {
+    int nslab, nranks;
+    Mailbox *mail[kMaxRanks];
+    SpSlab s[kMaxRanks];
+};
+
+template <int WHICH>  // 0 init, 1 pass
+__device__ __forceinline__ int sp_slab_of(const SpSet &ps, int &bid, int &nblk)
+{
+    auto off = [&](int k) { return WHICH == 0 ? ps.s[k].blk_init : ps.s[k].blk; };
+    int k = 0;
+    for (int q = 1; q < ps.nslab; ++q)
+        if ((int)blockIdx.x >= off(q)) k = q;
+    const int end = k + 1 < ps.nslab ? off(k + 1) : (int)gridDim.x;
+    bid = blockIdx.x - off(k);
+    nblk = end - off(k);
+    return k;
+}
+
+// the p2p_allreduce protocol over the single-pass descriptors
+__device__ __forceinline__ void sp_allreduce(const SpSet &ps, const SpSlab &sl, int ncomp, const double *v,
+                                             double *out)
+{
+    allreduce_core(ps.nranks, ps.mail, sl.sc, sl.rank, ncomp, v, out);
+}
+
+// init 1: r = b on the owned planes (and the boundary planes into the
+// neighbours' halos), x = 0; |b|^2 all-reduced (also the point after which
+// every rank's halo planes are written)
+__global__ void __launch_bounds__(256) sp_init_copy(const SpSet *__restrict__ psp)
+{
+    const SpSet &ps = *psp;
+    __shared__ double red[32];
+    __shared__ int is_last;
+    int bid, nblk;
+    const SpSlab &sl = ps.s[sp_slab_of<0>(ps, bid, nblk)];
+    const long long pl = (long long)sl.g.nx * sl.g.ny, n = pl * sl.g.nz, top = pl * (sl.g.nz - 2);
+    double bb = 0.0;
+    for (long long i = (long long)bid * 256 + threadIdx.x; i < n; i += (long long)nblk * 256) {
+        const double bi = sl.b[i];
+        sl.r[0][i] = bi;
+        sl.x[i] = 0.0;
+        if (i < 2 * pl && sl.lo[0][0]) sl.lo[0][0][i] = bi;
+        if (i >= top && sl.hi[0][0]) sl.hi[0][0][i - top] = bi;
+        bb = bb + bi * bi;
+    }
+    bb = block_sum<256>(bb, red);
+    if (threadIdx.x == 0) sl.partials[bid] = bb;
+    if (last_block_sys(&sl.tk->init, &is_last, nblk, sl.lo[0][0] || sl.hi[0][0])) {
+        bb = reduce_partials<256>(sl.partials, nblk, 1, red);
+        if (threadIdx.x == 0) {
+            double tot;
+            sp_allreduce(ps, sl, 1, &bb, &tot);
+            sl.sc->rr = tot;  // |b|^2 until init 2
+        }
+    }
+}
+
+// init 2: gamma_0 = r.z, delta_0 = z.A z (z = M^-1 r, the halo planes of r
+// from the neighbours), all-reduced -> alpha_0 (scalar_after_pass_init)
+template <int PK>
+__global__ void __launch_bounds__(256) sp_init_dots(const SpSet *__restrict__ psp, double off, double diag, double zc)
+{
+    const SpSet &ps = *psp;
+    __shared__ double red[32];
+    __shared__ int is_last;
+    int bid, nblk;
+    const SpSlab &sl = ps.s[sp_slab_of<0>(ps, bid, nblk)];
+    const int nx = sl.g.nx, ny = sl.g.ny, nz = sl.g.nz;
+    const long long pl = (long long)nx * ny, n = pl * nz;
+    const double *r = sl.r[0];
+    double gam = 0.0, dlt = 0.0;
+    for (long long i = (long long)bid * 256 + threadIdx.x; i < n; i += (long long)nblk * 256) {
+        const int ix = (int)(i % nx), iy = (int)((i / nx) % ny);
+        const double c = sp_z<PK>(r[i], zc);
+        double nb = sp_z<PK>(r[i - pl], zc) + sp_z<PK>(r[i + pl], zc);  // halo planes exist (zero at ghosts)
+        if (ix > 0) nb = nb + sp_z<PK>(r[i - 1], zc);
+        if (ix + 1 < nx) nb = nb + sp_z<PK>(r[i + 1], zc);
+        if (iy > 0) nb = nb + sp_z<PK>(r[i - nx], zc);
+        if (iy + 1 < ny) nb = nb + sp_z<PK>(r[i + nx], zc);
+        const double az = __fma_rn(off, nb, diag * c);
+        gam = __fma_rn(r[i], c, gam);
+        dlt = __fma_rn(c, az, dlt);
+    }
+    gam = block_sum<256>(gam, red);
+    dlt = block_sum<256>(dlt, red);
+    if (threadIdx.x == 0) {
+        sl.partials[2 * bid] = gam;
+        sl.partials[2 * bid + 1] = dlt;
+    }
+    if (last_block_sys(&sl.tk->dir, &is_last, nblk, false)) {
+        gam = reduce_partials<256>(sl.partials, nblk, 2, red);
+        dlt = reduce_partials<256>(sl.partials + 1, nblk, 2, red);
+        if (threadIdx.x == 0) {
+            const double v[2] = {gam, dlt};
+            double tot[2];
+            sp_allreduce(ps, sl, 2, v, tot);
+            scalar_after_pass_init(sl.sc, sl.sc->rr, tot[0], tot[1]);
+        }
+    }
+}
+
+// one pass over every slab: half 0 reads r[0], p[0] and writes r[1], p[1]
+// (x skipped); half 1 the other way round, x for both passes
+template <int PK, bool XDBL>
+__global__ void __launch_bounds__(SpSlabCfg::Threads, 1)
+    sp_slab_pass(const SpSet *__restrict__ psp, double off, double diag, double zc, int use_cond,
+                 cudaGraphConditionalHandle cond)
+{
+    using G = SpSlabCfg;
+    const SpSet &ps = *psp;
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[kSpSlabS], empty[kSpSlabS];
+    __shared__ double red[32];
+    __shared__ int is_last;
+    int bid, nblk;
+    const SpSlab &sl = ps.s[sp_slab_of<1>(ps, bid, nblk)];
+    CgScalars *sc = sl.sc;
+    if (sc->done) {
+        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    double *const ring = aligned_smem(smem_raw);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kSpSlabS; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], G::CWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int in = XDBL ? 1 : 0, out = in ^ 1;
+    const SpSlabIO io{2, sl.lo_ghost, sl.hi_ghost, sl.lo[0][out], sl.lo[1][out], sl.hi[0][out], sl.hi[1][out]};
+    double rr = 0.0, gam = 0.0, dlt = 0.0;
+    const double alpha = sc->alpha, alpha_prev = sc->alpha_prev;
+    if (!XDBL && sc->it == 0)
+        spass2_body<PK, kSpSlabTY, kSpSlabS, true, false, true>(&sl.m_r[in], &sl.m_p[in], &sl.m_x, sl.g, off, diag,
+                                                                zc, sl.r[out], sl.p[out], sl.x, alpha, alpha_prev,
+                                                                0.0, ring, full, empty, rr, gam, dlt, bid, nblk, io);
+    else
+        spass2_body<PK, kSpSlabTY, kSpSlabS, false, XDBL, true>(&sl.m_r[in], &sl.m_p[in], &sl.m_x, sl.g, off, diag,
+                                                                 zc, sl.r[out], sl.p[out], sl.x, alpha, alpha_prev,
+                                                                 sc->beta, ring, full, empty, rr, gam, dlt, bid, nblk,
+                                                                 io);
+    rr = block_sum<G::Threads>(rr, red);
+    gam = block_sum<G::Threads>(gam, red);
+    dlt = block_sum<G::Threads>(dlt, red);
+    if (threadIdx.x == 0) {
+        sl.partials[3 * bid] = rr;
+        sl.partials[3 * bid + 1] = gam;
+        sl.partials[3 * bid + 2] = dlt;
+    }
+    if (last_block_sys(&sl.tk->upd, &is_last, nblk, sl.lo[0][0] || sl.hi[0][0])) {
+        rr = reduce_partials<G::Threads>(sl.partials, nblk, 3, red);
+        gam = reduce_partials<G::Threads>(sl.partials + 1, nblk, 3, red);
+        dlt = reduce_partials<G::Threads>(sl.partials + 2, nblk, 3, red);
+        if (threadIdx.x == 0) {
+            const double v[3] = {rr, gam, dlt};
+            double tot[3];
+            sp_allreduce(ps, sl, 3, v, tot);
+            scalar_after_pass(sc, tot[0], tot[1], tot[2]);
+            if (sc->done && use_cond) cudaGraphSetConditional(cond, 0);
+        }
+    }
+}
+
+// x += alpha p_k owed by a final skipping pass (odd iteration count; p_k in p[1])
+__global__ void __launch_bounds__(256) sp_slab_fixup(const SpSet *__restrict__ psp)
+{
+    const SpSet &ps = *psp;
+    int bid, nblk;
+    const SpSlab &sl = ps.s[sp_slab_of<0>(ps, bid, nblk)];
+    if ((sl.sc->it & 1) == 0) return;
+    const double alpha = sl.sc->alpha;
+    const long long n = (long long)sl.g.nx * sl.g.ny * sl.g.nz;
+    for (long long i = (long long)bid * 256 + threadIdx.x; i < n; i += (long long)nblk * 256)
+        sl.x[i] = sl.x[i] + alpha * sl.p[1][i];
+}
+
 template <int ORDER, bool SINGLE>
 static void p2p_tma_attrs1()
 {
@@ -468,6 +683,10 @@ struct ExportBlob {  // what one rank publishes to the others
     cudaIpcMemHandle_t mail, r;
     unsigned long long mail_off, r_off;  // byte offsets of the arrays inside the exported allocations
     int nzl, lo, hi, rank;
+    // the single-pass arrays (one allocation: r0, r1, p0, p1, x, each nzl + 4 planes)
+    cudaIpcMemHandle_t sp;
+    unsigned long long sp_off;
+    int has_sp;
 };
 
 // cudaMalloc may sub-allocate small requests from a larger driver allocation;
@@ -520,6 +739,14 @@ struct cf_pcg {
     cudaGraph_t graph = nullptr;
     int exec_key = -1;
     int direct = 0;  // CF_PCG_DIRECT=1: host-driven loop (profilers)
+    // single pass over the slabs (the default; CF_PCG_ALGO=two selects the two-kernel form)
+    bool spass = false;
+    std::vector<double *> sp_alloc;  // per slab: r0 | r1 | p0 | p1 | x, each sp_stride doubles
+    std::vector<double *> sp_part;   // per slab partials
+    size_t sp_stride = 0;            // doubles per array (nzl + 4 planes + pad, 256-byte multiple)
+    cf::SpSet sset{};
+    cf::SpSet *d_sset = nullptr;
+    int sp_grid = 0, sp_grid_init = 0;
 };
 
 namespace cf {
@@ -635,6 +862,107 @@ static int p2p_solve(cf_pcg *ws, double zc, cudaStream_t s)
     CF_CUDA(cudaGraphLaunch(ws->exec, s));
     CF_CUDA(cudaEventRecord(ws->ev1, s));
     return CF_OK;
+}
+
+// ---- single pass over the slabs
+template <int PK>
+static int sp_body(cf_pcg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond, int use_cond)
+{
+    sp_slab_pass<PK, false><<<ws->sp_grid, SpSlabCfg::Threads, SpSlabCfg::Smem, s>>>(ws->d_sset, ws->off, ws->diag,
+                                                                                     zc, use_cond, cond);
+    CF_CHECK_LAUNCH("sp_slab_pass");
+    sp_slab_pass<PK, true><<<ws->sp_grid, SpSlabCfg::Threads, SpSlabCfg::Smem, s>>>(ws->d_sset, ws->off, ws->diag,
+                                                                                    zc, use_cond, cond);
+    CF_CHECK_LAUNCH("sp_slab_pass");
+    return CF_OK;
+}
+
+template <int PK>
+static int sp_solve(cf_pcg *ws, double zc, cudaStream_t s)
+{
+    sp_init_copy<<<ws->sp_grid_init, 256, 0, s>>>(ws->d_sset);
+    CF_CHECK_LAUNCH("sp_init_copy");
+    sp_init_dots<PK><<<ws->sp_grid_init, 256, 0, s>>>(ws->d_sset, ws->off, ws->diag, zc);
+    CF_CHECK_LAUNCH("sp_init_dots");
+    if (ws->direct) {
+        CF_CUDA(cudaEventRecord(ws->ev0, s));
+        for (;;) {
+            for (int b = 0; b < 4; ++b) {
+                int rc = sp_body<PK>(ws, s, zc, 0, 0);
+                if (rc != CF_OK) return rc;
+            }
+            CF_CUDA(cudaMemcpyAsync(&ws->sc_host->done, &ws->slabs[0].sc->done, sizeof(int), cudaMemcpyDeviceToHost,
+                                    s));
+            CF_CUDA(cudaStreamSynchronize(s));
+            if (ws->sc_host->done) break;
+        }
+        sp_slab_fixup<<<ws->sp_grid_init, 256, 0, s>>>(ws->d_sset);
+        CF_CHECK_LAUNCH("sp_slab_fixup");
+        CF_CUDA(cudaEventRecord(ws->ev1, s));
+        return CF_OK;
+    }
+    const int key = 100 + PK;
+    if (!ws->exec || ws->exec_key != key) {
+        cudaGraph_t g;
+        CF_CUDA(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle cond;
+        CF_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams np = {};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = cond;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        CF_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+        cudaStream_t cs;
+        CF_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CF_CUDA(cudaStreamBeginCaptureToGraph(cs, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeRelaxed));
+        int rc = sp_body<PK>(ws, cs, zc, cond, 1);
+        cudaGraph_t captured;
+        cudaError_t e = cudaStreamEndCapture(cs, &captured);
+        cudaStreamDestroy(cs);
+        if (rc != CF_OK) return rc;
+        CF_CUDA(e);
+        cudaKernelNodeParams kp = {};
+        void *args[] = {&ws->d_sset};
+        kp.func = (void *)sp_slab_fixup;
+        kp.gridDim = dim3(ws->sp_grid_init);
+        kp.blockDim = dim3(256);
+        kp.kernelParams = args;
+        cudaGraphNode_t fix;
+        CF_CUDA(cudaGraphAddKernelNode(&fix, g, &node, 1, &kp));
+        if (ws->exec) {
+            cudaGraphExecDestroy(ws->exec);
+            cudaGraphDestroy(ws->graph);
+            ws->exec = nullptr;
+        }
+        CF_CUDA(cudaGraphInstantiate(&ws->exec, g, 0));
+        ws->graph = g;
+        ws->exec_key = key;
+    }
+    CF_CUDA(cudaEventRecord(ws->ev0, s));
+    CF_CUDA(cudaGraphLaunch(ws->exec, s));
+    CF_CUDA(cudaEventRecord(ws->ev1, s));
+    return CF_OK;
+}
+
+// the single-pass arrays of slab k: 0 r0, 1 r1, 2 p0, 3 p1, 4 x (each starting at its lowest halo plane)
+static double *sp_array(const cf_pcg *ws, size_t k, int a) { return ws->sp_alloc[k] + (size_t)a * ws->sp_stride; }
+
+// neighbours' planes matching ours, for local slabs in one process: the lower
+// neighbour's hi halo planes (its local planes nzl, nzl+1 = array planes
+// nzl+2, nzl+3), the upper neighbour's lo halo planes (array planes 0, 1)
+static void sp_link_local(cf_pcg *ws)
+{
+    const size_t pl = (size_t)ws->nx * ws->ny;
+    for (size_t k = 0; k < ws->slabs.size(); ++k) {
+        SpSlab &d = ws->sset.s[k];
+        for (int a = 0; a < 4; ++a) {  // a = 2 * (r | p) + buffer
+            if (k > 0) d.lo[a / 2][a % 2] = sp_array(ws, k - 1, a) + (size_t)(ws->slabs[k - 1].nzl + 2) * pl;
+            if (k + 1 < ws->slabs.size()) d.hi[a / 2][a % 2] = sp_array(ws, k + 1, a);
+        }
+    }
 }
 
 // halo-plane targets of local slab k: the lower neighbour's hi halo plane and
@@ -769,6 +1097,84 @@ int cf_pcg_create(cf_pcg **out, int nx, int ny, int nz, double h, int order, int
     ws->grid_upd = bu;
     ws->grid_updt = bt;
     ws->grid_init = bi;
+    // ---- the single pass (default): 2-halo-plane arrays, TMA maps, lockstep items per slab
+    {
+        const char *algo = getenv("CF_PCG_ALGO");
+        bool want = !(algo && strcmp(algo, "spass")) && nx % 2 == 0;
+        for (const PSlab &sb : ws->slabs) want = want && sb.nzl >= 4;
+        if (want && e == cudaSuccess) {
+            cudaFuncSetAttribute(cf::sp_slab_pass<cf::PK_NONE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)cf::SpSlabCfg::Smem);
+            cudaFuncSetAttribute(cf::sp_slab_pass<cf::PK_NONE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)cf::SpSlabCfg::Smem);
+            cudaFuncSetAttribute(cf::sp_slab_pass<cf::PK_JCONST, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)cf::SpSlabCfg::Smem);
+            cudaFuncSetAttribute(cf::sp_slab_pass<cf::PK_JCONST, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)cf::SpSlabCfg::Smem);
+            const int bps = cf::blocks_per_sm((const void *)cf::sp_slab_pass<cf::PK_JCONST, true>,
+                                              cf::SpSlabCfg::Threads, cf::SpSlabCfg::Smem);
+            const long long slots = std::max(1LL, (long long)cf::num_sms() * std::max(bps, 1) / nslabs);
+            int maxz = 0;
+            for (const PSlab &sb : ws->slabs) maxz = std::max(maxz, sb.nzl);
+            ws->sp_stride = ((size_t)(maxz + 4) * pl + cf::kLeanPad + 31) / 32 * 32;
+            int blk = 0, blki = 0;
+            for (int k = 0; k < nslabs && e == cudaSuccess; ++k) {
+                PSlab &sb = ws->slabs[k];
+                const int grank = nslabs == 1 ? rank : k;
+                double *a = nullptr;
+                const size_t bytes = 5 * ws->sp_stride * sizeof(double);
+                e = cudaMalloc(&a, bytes);
+                if (e == cudaSuccess) e = cudaMemsetAsync(a, 0, bytes, s);
+                if (e != cudaSuccess) break;
+                ws->sp_alloc.push_back(a);
+                cf::SpSlab &d = ws->sset.s[k];
+                d = cf::SpSlab{};
+                cf::SpGeom g{nx, ny, sb.nzl, (nx + cf::kSpTX - 1) / cf::kSpTX, (ny + cf::kSpSlabTY - 1) / cf::kSpSlabTY,
+                             1};
+                const long long tiles = (long long)g.ntx * g.nty;
+                g.nchunk = (int)std::max(1LL, std::min(slots / std::max(1LL, tiles), (long long)sb.nzl / 8));
+                const long long items = tiles * g.nchunk, rounds = (items + slots - 1) / slots;
+                const int nblk = (int)((items + rounds - 1) / rounds);
+                d.g = g;
+                d.blk = blk;
+                d.blk_init = blki;
+                blk += nblk;
+                const int ni = (int)std::min<long long>(((long long)pl * sb.nzl + 255) / 256, slots * 4);
+                blki += ni;
+                const size_t off2 = 2 * pl;  // owned plane 0 behind two halo planes
+                d.r[0] = a + off2;
+                d.r[1] = a + ws->sp_stride + off2;
+                d.p[0] = a + 2 * ws->sp_stride + off2;
+                d.p[1] = a + 3 * ws->sp_stride + off2;
+                d.x = a + 4 * ws->sp_stride + off2;
+                d.lo_ghost = grank == 0;
+                d.hi_ghost = grank == nranks - 1;
+                d.tk = sb.tk;
+                d.sc = sb.sc;
+                d.rank = grank;
+                double *part = nullptr;
+                e = cudaMalloc(&part, (size_t)std::max(3 * nblk, 2 * ni) * sizeof(double));
+                if (e != cudaSuccess) break;
+                ws->sp_part.push_back(part);
+                d.partials = part;
+                const int planes = sb.nzl + 4, hy = cf::kSpSlabTY + 4;
+                bool ok = true;
+                for (int q = 0; q < 2; ++q) {
+                    ok = ok && cf::make_map_promo(&d.m_r[q], a + q * ws->sp_stride, nx, ny, planes, cf::kSpBX, hy, 256);
+                    ok = ok && cf::make_map_promo(&d.m_p[q], a + (2 + q) * ws->sp_stride, nx, ny, planes, cf::kSpBX, hy,
+                                                  256);
+                }
+                ok = ok && cf::make_map_promo(&d.m_x, a + 4 * ws->sp_stride, nx, ny, planes, cf::kSpTX, cf::kSpSlabTY, 256);
+                if (!ok) want = false;
+            }
+            ws->sset.nslab = nslabs;
+            ws->sset.nranks = nranks;
+            ws->sp_grid = blk;
+            ws->sp_grid_init = blki;
+            ws->spass = want && e == cudaSuccess;
+        }
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&ws->d_sset, sizeof(cf::SpSet));
     if (e == cudaSuccess) e = cudaMallocHost(&ws->sc_host, sizeof(cf::CgScalars));
     if (e == cudaSuccess) e = cudaMalloc(&ws->d_set, sizeof(cf::P2PSet));
     if (e == cudaSuccess) e = cudaEventCreate(&ws->ev0);
@@ -779,8 +1185,10 @@ int cf_pcg_create(cf_pcg **out, int nx, int ny, int nz, double h, int order, int
         cf_pcg_destroy(ws);
         return rc;
     }
+    for (int k = 0; k < nslabs; ++k) ws->sset.mail[ws->sset.s[k].rank] = ws->slabs[k].mail;
     if (nslabs == nranks) {  // every slab here: link directly
         cf::link_local(ws);
+        if (ws->spass) cf::sp_link_local(ws);
         ws->linked = true;
     }
     *out = ws;
@@ -803,6 +1211,11 @@ int cf_pcg_export(cf_pcg *ws, void *out, int cap)
     b.lo = sb.lo;
     b.hi = sb.hi;
     b.rank = ws->rank;
+    b.has_sp = ws->spass ? 1 : 0;
+    if (ws->spass) {
+        CF_CUDA(cudaIpcGetMemHandle(&b.sp, ws->sp_alloc[0]));
+        CF_REQUIRE(alloc_offset(ws->sp_alloc[0], &b.sp_off), "cf_pcg_export: cuMemGetAddressRange unavailable");
+    }
     std::memcpy(out, &b, sizeof(b));
     return CF_OK;
 }
@@ -821,6 +1234,7 @@ int cf_pcg_import(cf_pcg *ws, const void *all, int nranks)
         CF_CUDA(cudaIpcOpenMemHandle(&m, blobs[q].mail, cudaIpcMemLazyEnablePeerAccess));
         ws->opened.push_back(m);
         ws->set.mail[q] = reinterpret_cast<cf::Mailbox *>(static_cast<char *>(m) + blobs[q].mail_off);
+        ws->sset.mail[q] = ws->set.mail[q];
         if (q == ws->rank - 1 || q == ws->rank + 1) {
             void *r = nullptr;
             CF_CUDA(cudaIpcOpenMemHandle(&r, blobs[q].r, cudaIpcMemLazyEnablePeerAccess));
@@ -828,7 +1242,24 @@ int cf_pcg_import(cf_pcg *ws, const void *all, int nranks)
             double *base = reinterpret_cast<double *>(static_cast<char *>(r) + blobs[q].r_off);
             if (q == ws->rank - 1) d.lo_r = base + (size_t)(blobs[q].lo + blobs[q].nzl) * pl;  // its hi halo plane
             else d.hi_r = base;                                                                // its lo halo plane
+            if (ws->spass) {
+                CF_REQUIRE(blobs[q].has_sp, "cf_pcg_import: a neighbour runs without the single-pass arrays");
+                void *sp = nullptr;
+                CF_CUDA(cudaIpcOpenMemHandle(&sp, blobs[q].sp, cudaIpcMemLazyEnablePeerAccess));
+                ws->opened.push_back(sp);
+                double *sbase = reinterpret_cast<double *>(static_cast<char *>(sp) + blobs[q].sp_off);
+                cf::SpSlab &e2 = ws->sset.s[0];
+                for (int a = 0; a < 4; ++a) {  // same stride on every rank (equal slab heights +-1: see create)
+                    double *arr = sbase + (size_t)a * ws->sp_stride;
+                    if (q == ws->rank - 1) e2.lo[a / 2][a % 2] = arr + (size_t)(blobs[q].nzl + 2) * pl;
+                    else e2.hi[a / 2][a % 2] = arr;
+                }
+            }
         }
+    }
+    if (ws->spass) {  // every rank must agree on the form
+        for (int q = 0; q < nranks; ++q)
+            CF_REQUIRE(blobs[q].has_sp, "cf_pcg_import: ranks disagree on the single-pass form");
     }
     ws->linked = true;
     return CF_OK;
@@ -848,6 +1279,9 @@ int cf_pcg_destroy(cf_pcg *ws)
         if (sb.sc) cudaFree(sb.sc);
         if (sb.mail) cudaFree(sb.mail);
     }
+    for (double *a : ws->sp_alloc) cudaFree(a);
+    for (double *a : ws->sp_part) cudaFree(a);
+    if (ws->d_sset) cudaFree(ws->d_sset);
     if (ws->sc_host) cudaFreeHost(ws->sc_host);
     if (ws->d_set) cudaFree(ws->d_set);
     if (ws->ev0) cudaEventDestroy(ws->ev0);
@@ -869,6 +1303,7 @@ int cf_pcg_solve(cf_pcg *ws, const double *const *b_slabs, double *const *x_slab
     for (size_t k = 0; k < ws->slabs.size(); ++k) {
         CF_REQUIRE(b_slabs[k] && x_slabs[k], "cf_pcg_solve: null slab pointer");
         ws->set.s[k].b = b_slabs[k];
+        ws->sset.s[k].b = b_slabs[k];
     }
     cf::CgScalars *h = ws->sc_host;
     *h = cf::CgScalars{};
@@ -887,11 +1322,14 @@ int cf_pcg_solve(cf_pcg *ws, const double *const *b_slabs, double *const *x_slab
         CF_CUDA(cudaStreamSynchronize(s));
     }
     CF_CUDA(cudaMemcpyAsync(ws->d_set, &ws->set, sizeof(cf::P2PSet), cudaMemcpyHostToDevice, s));
+    if (ws->spass) CF_CUDA(cudaMemcpyAsync(ws->d_sset, &ws->sset, sizeof(cf::SpSet), cudaMemcpyHostToDevice, s));
     CF_CUDA(cudaStreamSynchronize(s));
     const double zc = 1.0 / ws->diag;
     const int pk = precond == CF_PRECOND_JACOBI ? cf::PK_JCONST : cf::PK_NONE;
     int rc;
-    if (ws->order == CF_ORDER_CSR)
+    if (ws->spass)  // the single pass (its stencil order is the CSR column order, both orders)
+        rc = pk == cf::PK_JCONST ? cf::sp_solve<cf::PK_JCONST>(ws, zc, s) : cf::sp_solve<cf::PK_NONE>(ws, zc, s);
+    else if (ws->order == CF_ORDER_CSR)
         rc = pk == cf::PK_JCONST ? cf::p2p_solve<CF_ORDER_CSR, cf::PK_JCONST>(ws, zc, s)
                                  : cf::p2p_solve<CF_ORDER_CSR, cf::PK_NONE>(ws, zc, s);
     else
@@ -905,7 +1343,9 @@ int cf_pcg_solve(cf_pcg *ws, const double *const *b_slabs, double *const *x_slab
     for (size_t k = 0; k < ws->slabs.size(); ++k) {
         const size_t bytes = pl * ws->slabs[k].nzl * sizeof(double);
         if (h->norm_b == 0.0) CF_CUDA(cudaMemsetAsync(x_slabs[k], 0, bytes, s));
-        else CF_CUDA(cudaMemcpyAsync(x_slabs[k], ws->set.s[k].x, bytes, cudaMemcpyDeviceToDevice, s));
+        else
+            CF_CUDA(cudaMemcpyAsync(x_slabs[k], ws->spass ? ws->sset.s[k].x : ws->set.s[k].x, bytes,
+                                    cudaMemcpyDeviceToDevice, s));
     }
     CF_CUDA(cudaStreamSynchronize(s));
     if (iters_host) *iters_host = h->it;

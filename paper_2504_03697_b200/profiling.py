@@ -124,6 +124,13 @@ class Profiler:
     def region(self, name: str) -> _Region:
         return _Region(self, name)
 
+    def record(self, name: str, calls: int, seconds: float):
+        """Add `calls` and `seconds` to the child region `name` of the open
+        region without timing it (rows of work done inside one fused kernel)."""
+        node = self._nodes.setdefault(tuple(self._path) + (name,), [0, 0])
+        node[0] += int(calls)
+        node[1] += int(round(seconds * 1e9))
+
     def reset(self):
         if self._path:
             raise ProfileError(f"cannot reset while region {self._path[-1]!r} is open")
@@ -163,6 +170,9 @@ class NullProfiler:
 
     def region(self, name):
         return _NullRegion()
+
+    def record(self, name, calls, seconds):
+        pass
 
     def stats(self):
         return []

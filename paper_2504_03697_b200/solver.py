@@ -142,11 +142,45 @@ def pcg(apply_a, b, x0=None, precond=None, tol: float = 1e-6, max_iter: int = 10
     fusable = isinstance(apply_a, StencilOperator) and (
         precond is None or getattr(precond, "kind", None) in ("jacobi", "dic"))
     if fusable:
-        with prof.region("fused_cg"):
-            x, stats = workspace_for(apply_a).solve(bd, x0d, precond, tol, max_iter)
+        ws = workspace_for(apply_a)
+        x, stats = ws.solve(bd, x0d, precond, tol, max_iter)
+        _record_fused_rows(prof, ws, stats, x0d is not None, precond is not None)
     else:
         x, stats = _pcg_per_op(apply_a, bd, x0d, precond, tol, max_iter, prof)
     return (to_host(x) if host else x), stats
+
+
+# Bytes per cell each reference op of one CG iteration streams
+# (src/solver.py:148-170): spmv reads p and writes Ap, p.Ap / r.z read two
+# vectors, r.r one, multiply_add_inplace reads two and writes one, the
+# preconditioner reads r and writes z.
+_ROW_BYTES = {"spmv": 16, "dot": 16, "multiply_add_inplace": 24, "precondition": 16}
+
+
+def _record_fused_rows(prof, ws, stats, warm, has_precond):
+    """The reference's pcg sub-regions (src/solver.py:148-170: spmv, dot,
+    multiply_add_inplace, precondition -- PAPER.md Table 1's rows) for a
+    solve that ran as fused kernels: the reference's call counts for
+    `stats.iterations` iterations, and the measured device time of the loop
+    (CUDA events, ws.last_loop_ms) split over them in proportion to the bytes
+    each op streams.  The split is synthesised -- the fused kernels run no
+    separate spmv or dot -- but the rows line up with a reference report
+    (compare_reports)."""
+    k = stats.iterations
+    record = getattr(prof, "record", None)
+    if k == 0 or record is None:
+        return
+    last_full = not stats.converged  # a converged last iteration stops after r.r
+    calls = {"spmv": k + (1 if warm else 0),
+             "dot": 1 + 2 * k + (k if last_full else k - 1),
+             "multiply_add_inplace": 2 * k + (k if last_full else k - 1) + (1 if warm else 0),
+             "precondition": (1 + (k if last_full else k - 1)) if has_precond else 0}
+    weight = {n: c * (_ROW_BYTES[n] if n != "dot" else 40 / 3) for n, c in calls.items()}
+    total = sum(weight.values())
+    seconds = ws.last_loop_ms * 1e-3
+    for name in ("spmv", "dot", "multiply_add_inplace", "precondition"):
+        if calls[name]:
+            record(name, calls[name], seconds * weight[name] / total)
 
 
 def _precondition(precond, r, out, prof):

@@ -97,7 +97,10 @@ def test_slab_time_steps_match_single_domain(cuda, nslabs, collective):
         b = sim.step()
         assert abs(a.solve.iterations - b.solve.iterations) <= 2
         assert b.div_pre == pytest.approx(a.div_pre, rel=1e-12)
-        assert b.div_post == pytest.approx(a.div_post, rel=1e-4, abs=1e-12)
+        # div_post is the projection's leftover divergence: at CG tol 1e-12 it is
+        # rounding noise of the last iterates (the single-reduction recurrence
+        # stagnates a little above the two-kernel one), so compare magnitudes
+        assert b.div_post <= 5 * a.div_post + 1e-12 and a.div_post <= 5 * b.div_post + 1e-12
     su, sv, sw, sp = sim.gather()
     ru, rv, rw = ref.vel.numpy()
     assert rel(np.concatenate([su.ravel(), sv.ravel(), sw.ravel()]),
@@ -219,3 +222,26 @@ def test_weak_scaling_box_slabs(cuda, collective):
     assert rel(np.concatenate([su.ravel(), sv.ravel(), sw.ravel()]),
                np.concatenate([ru.ravel(), rv.ravel(), rw.ravel()])) <= 1e-10
     assert rel(sp, ref.p.numpy()) <= 1e-9
+
+
+@pytest.mark.parametrize("algo", ["spass", "two"])
+@pytest.mark.parametrize("nslabs", [1, 3, 8])
+def test_peer_slab_forms(cuda, monkeypatch, algo, nslabs):
+    """Both peer-memory slab forms -- the single pass (default: two halo
+    planes, one all-reduce per iteration) and the two-kernel form
+    (CF_PCG_ALGO=two) -- against the single-domain solve, 1-8 slabs, Jacobi
+    and no preconditioner."""
+    from paper_2504_03697_b200.distributed import emulated_pcg
+
+    monkeypatch.setenv("CF_PCG_ALGO", algo)
+    n = 64
+    h = 1.0 / n
+    b = np.random.default_rng(10 + nslabs).uniform(-1, 1, n ** 3)
+    op = cuda.StencilOperator(n, h, "sym")
+    for pre in (cuda.jacobi_from(op), None):
+        x1, s1 = cuda.pcg(op, b, precond=pre, tol=1e-10, max_iter=20000)
+        xs, ss, _ = emulated_pcg(op, b, nslabs, tol=1e-10, max_iter=20000, collective="p2p",
+                                 precond="jacobi" if pre is not None else None)
+        assert ss.converged
+        assert abs(ss.iterations - s1.iterations) <= 2, (algo, ss.iterations, s1.iterations)
+        assert rel(xs, x1) <= 1e-9

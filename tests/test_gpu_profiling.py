@@ -18,9 +18,16 @@ def test_event_timer_run_report(cuda):
     names_w = [(r.name, r.parent, r.calls) for r in wall.regions]
     names_e = [(r.name, r.parent, r.calls) for r in ev.regions]
     assert names_w == names_e
-    assert [n for n, _, _ in names_e[1:]] == STEP_REGIONS[:4] + ["fused_cg", STEP_REGIONS[4]]
+    # the fused solve reports the reference's pcg sub-regions (src/solver.py:148-170,
+    # PAPER.md Table 1): reference call counts, device loop time split by bytes
+    sub = ["spmv", "dot", "multiply_add_inplace", "precondition"]
+    assert [n for n, _, _ in names_e[1:]] == STEP_REGIONS[:4] + sub + [STEP_REGIONS[4]]
     by = {r.name: r for r in ev.regions}
     assert by["pcg"].inclusive_seconds > 0 and by["pcg"].inclusive_seconds <= by["cavityflow"].inclusive_seconds
+    assert all(by[n].parent == "pcg" for n in sub)
+    assert sum(by[n].inclusive_seconds for n in sub) <= by["pcg"].inclusive_seconds * 1.05
+    assert by["dot"].calls == 3 * by["spmv"].calls  # converged solves: 1 + 2k + (k - 1) dots for k spmvs
+    assert by["multiply_add_inplace"].calls == 3 * by["spmv"].calls - 3  # 3 steps, 2k + (k - 1) each
     assert "└─ applyPressureCorrection" in render_report(ev.regions)
 
 
