@@ -570,10 +570,14 @@ __global__ void __launch_bounds__(256) sp_init_dots(const SpSet *__restrict__ ps
 
 // one pass over every slab: half 0 reads r[0], p[0] and writes r[1], p[1]
 // (x skipped); half 1 the other way round, x for both passes
-template <int PK, bool XDBL>
+// SINGLE (one slab per GPU, the multi-GPU case): the slab's descriptor --
+// maps, geometry, pointers -- comes as a __grid_constant__ kernel parameter,
+// so the loop reads constant-bank values as the single-domain kernel does;
+// the multi-slab emulation reads it from the device copy of the set.
+template <int PK, bool XDBL, bool SINGLE>
 __global__ void __launch_bounds__(SpSlabCfg::Threads, 1)
-    sp_slab_pass(const SpSet *__restrict__ psp, double off, double diag, double zc, int use_cond,
-                 cudaGraphConditionalHandle cond)
+    sp_slab_pass(const SpSet *__restrict__ psp, const __grid_constant__ SpSlab one, double off, double diag,
+                 double zc, int use_cond, cudaGraphConditionalHandle cond)
 {
     using G = SpSlabCfg;
     const SpSet &ps = *psp;
@@ -582,7 +586,11 @@ __global__ void __launch_bounds__(SpSlabCfg::Threads, 1)
     __shared__ double red[32];
     __shared__ int is_last;
     int bid, nblk;
-    const SpSlab &sl = ps.s[sp_slab_of<1>(ps, bid, nblk)];
+    if (SINGLE) {
+        bid = blockIdx.x;
+        nblk = gridDim.x;
+    }
+    const SpSlab &sl = SINGLE ? one : ps.s[sp_slab_of<1>(ps, bid, nblk)];
     CgScalars *sc = sl.sc;
     if (sc->done) {
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
@@ -865,14 +873,20 @@ static int p2p_solve(cf_pcg *ws, double zc, cudaStream_t s)
 }
 
 // ---- single pass over the slabs
+template <int PK, bool SINGLE>
+static void sp_body_t(cf_pcg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond, int use_cond)
+{
+    sp_slab_pass<PK, false, SINGLE><<<ws->sp_grid, SpSlabCfg::Threads, SpSlabCfg::Smem, s>>>(
+        ws->d_sset, ws->sset.s[0], ws->off, ws->diag, zc, use_cond, cond);
+    sp_slab_pass<PK, true, SINGLE><<<ws->sp_grid, SpSlabCfg::Threads, SpSlabCfg::Smem, s>>>(
+        ws->d_sset, ws->sset.s[0], ws->off, ws->diag, zc, use_cond, cond);
+}
+
 template <int PK>
 static int sp_body(cf_pcg *ws, cudaStream_t s, double zc, cudaGraphConditionalHandle cond, int use_cond)
 {
-    sp_slab_pass<PK, false><<<ws->sp_grid, SpSlabCfg::Threads, SpSlabCfg::Smem, s>>>(ws->d_sset, ws->off, ws->diag,
-                                                                                     zc, use_cond, cond);
-    CF_CHECK_LAUNCH("sp_slab_pass");
-    sp_slab_pass<PK, true><<<ws->sp_grid, SpSlabCfg::Threads, SpSlabCfg::Smem, s>>>(ws->d_sset, ws->off, ws->diag,
-                                                                                    zc, use_cond, cond);
+    if (ws->slabs.size() == 1) sp_body_t<PK, true>(ws, s, zc, cond, use_cond);
+    else sp_body_t<PK, false>(ws, s, zc, cond, use_cond);
     CF_CHECK_LAUNCH("sp_slab_pass");
     return CF_OK;
 }
@@ -1103,15 +1117,17 @@ int cf_pcg_create(cf_pcg **out, int nx, int ny, int nz, double h, int order, int
         bool want = !(algo && strcmp(algo, "spass")) && nx % 2 == 0;
         for (const PSlab &sb : ws->slabs) want = want && sb.nzl >= 4;
         if (want && e == cudaSuccess) {
-            cudaFuncSetAttribute(cf::sp_slab_pass<cf::PK_NONE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)cf::SpSlabCfg::Smem);
-            cudaFuncSetAttribute(cf::sp_slab_pass<cf::PK_NONE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)cf::SpSlabCfg::Smem);
-            cudaFuncSetAttribute(cf::sp_slab_pass<cf::PK_JCONST, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)cf::SpSlabCfg::Smem);
-            cudaFuncSetAttribute(cf::sp_slab_pass<cf::PK_JCONST, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)cf::SpSlabCfg::Smem);
-            const int bps = cf::blocks_per_sm((const void *)cf::sp_slab_pass<cf::PK_JCONST, true>,
+            const void *kerns[] = {(const void *)cf::sp_slab_pass<cf::PK_NONE, false, false>,
+                                   (const void *)cf::sp_slab_pass<cf::PK_NONE, true, false>,
+                                   (const void *)cf::sp_slab_pass<cf::PK_JCONST, false, false>,
+                                   (const void *)cf::sp_slab_pass<cf::PK_JCONST, true, false>,
+                                   (const void *)cf::sp_slab_pass<cf::PK_NONE, false, true>,
+                                   (const void *)cf::sp_slab_pass<cf::PK_NONE, true, true>,
+                                   (const void *)cf::sp_slab_pass<cf::PK_JCONST, false, true>,
+                                   (const void *)cf::sp_slab_pass<cf::PK_JCONST, true, true>};
+            for (const void *kf : kerns)
+                cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf::SpSlabCfg::Smem);
+            const int bps = cf::blocks_per_sm((const void *)cf::sp_slab_pass<cf::PK_JCONST, true, true>,
                                               cf::SpSlabCfg::Threads, cf::SpSlabCfg::Smem);
             const long long slots = std::max(1LL, (long long)cf::num_sms() * std::max(bps, 1) / nslabs);
             int maxz = 0;
