@@ -182,9 +182,15 @@ int cf_pcg_destroy(cf_pcg *ws);
 int cf_pcg_solve(cf_pcg *ws, const double *const *b_slabs, double *const *x_slabs, double tol, int64_t max_iter,
                  int precond, int64_t *iters_host, double *res_host, void *stream);
 int cf_pcg_last_loop_ms(cf_pcg *ws, float *ms_host);
+/* The slab CG form (CF_CG_FORM_SPASS: the single pass, default; CF_CG_FORM_TWO:
+ * the two-kernel form, CF_PCG_ALGO=two or slabs thinner than 4 planes). */
+int cf_pcg_form(cf_pcg *ws, int *form_host);
 /* Diagnostics (tests): which 0 = this rank's r allocation incl. halo planes
  * (read or write), 1 / 2 = the peer plane this rank's bottom / top r plane is
- * stored into (read only) -- checks the IPC linking without running kernels. */
+ * stored into (read only); 3 = the single pass's r0 array (nzl + 4 planes,
+ * two halo planes each side), 4 / 5 = the two peer planes its bottom /
+ * top two planes are stored into -- checks the IPC linking without running
+ * kernels. */
 int cf_pcg_debug_io(cf_pcg *ws, int which, int write, double *host, int64_t n);
 
 /* ---- time-step kernels (src/sim.py:134-289, :352-449) ------------------- */

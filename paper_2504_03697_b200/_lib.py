@@ -30,6 +30,8 @@ ORDER_SYM = 1
 PRECOND_NONE = 0
 PRECOND_JACOBI = 1
 PRECOND_DIC = 2
+CG_FORM_TWO = 1  # include/cfgpu.h CF_CG_FORM_*
+CG_FORM_SPASS = 2
 
 _lib = None
 
@@ -76,6 +78,7 @@ _SIGNATURES = {
     "cf_pcg_destroy": ([_vp], _int),
     "cf_pcg_solve": ([_vp, _vp, _vp, _dbl, _i64, _int, _pi64, _pd, _vp], _int),
     "cf_pcg_last_loop_ms": ([_vp, _pf], _int),
+    "cf_pcg_form": ([_vp, ctypes.POINTER(_int)], _int),
     "cf_pcg_debug_io": ([_vp, _int, _int, _vp, _i64], _int),
     "cf_forces_bc": ([_vp, _vp, _vp, _int, _int, _int, _int, _dbl, _int, _vp], _int),
     "cf_advect": ([_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl, _vp], _int),

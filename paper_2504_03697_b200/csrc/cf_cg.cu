@@ -1048,6 +1048,7 @@ static int spass_body_launch(cf_cg *ws, cudaStream_t s, double zc, cudaGraphCond
 {
     if (ws->sp_form == 1 && ws->sp_ty == 8) spass_launch<PK, 8, 5, 1>(ws, s, zc, cond, use_cond);
     else if (ws->sp_form == 1) spass_launch<PK, 16, 6, 1>(ws, s, zc, cond, use_cond);
+    else if (ws->sp_ty == 8) spass_launch<PK, 8, 5, 2>(ws, s, zc, cond, use_cond);
     else spass_launch<PK, 16, 6, 2>(ws, s, zc, cond, use_cond);
     CF_CHECK_LAUNCH("cg_spass_kernel");
     return CF_OK;
@@ -1395,9 +1396,10 @@ static void set_grids(cf_cg *ws)
     ws->spass = ws->tma && ws->bx.nx % 2 == 0 && ws->n + kLeanPad < (1LL << 32) && !(algo && strcmp(algo, "spass"));
     if (ws->spass) {
         if (const char *e = getenv("CF_SPASS_FORM")) ws->sp_form = atoi(e) == 1 ? 1 : 2;
-        if (const char *e = getenv("CF_SPASS_TY")) ws->sp_ty = atoi(e) == 8 && ws->sp_form == 1 ? 8 : 16;
+        if (const char *e = getenv("CF_SPASS_TY")) ws->sp_ty = atoi(e) == 8 ? 8 : 16;
         if (ws->sp_form == 1 && ws->sp_ty == 8) spass_setup<8, 5, 1>(ws);
         else if (ws->sp_form == 1) spass_setup<16, 6, 1>(ws);
+        else if (ws->sp_ty == 8) spass_setup<8, 5, 2>(ws);
         else spass_setup<16, 6, 2>(ws);
     }
     if (const char *e = getenv("CF_CG_UPD_SKIP")) ws->kind_upd_skip = kern_kind("CF_CG_UPD_SKIP", ws->kind_upd, ws->tma, pair_ok);

@@ -63,7 +63,7 @@ struct Sp {
     // + two p planes and two z' planes (double-buffered, generic writes only)
     static constexpr size_t Smem = ((size_t)S * StageD + 4 * BoxD) * sizeof(double) + 128;
     // small tiles run two CTAs per SM (two independent lockstep groups)
-    static constexpr int MinBlocks = Threads <= 512 && FORM == 1 ? 2 : 1;
+    static constexpr int MinBlocks = (Threads <= 512 && FORM == 1) || Threads <= 256 ? 2 : 1;
 };
 
 // Work items (tile, z-chunk), chunk-major: item j = chunk j / T, tile j % T

@@ -1380,13 +1380,23 @@ int cf_pcg_solve(cf_pcg *ws, const double *const *b_slabs, double *const *x_slab
 
 int cf_pcg_debug_io(cf_pcg *ws, int which, int write, double *host, int64_t n)
 {
-    CF_REQUIRE(ws && host && n >= 0 && ws->slabs.size() == 1 && which >= 0 && which <= 2,
+    CF_REQUIRE(ws && host && n >= 0 && ws->slabs.size() == 1 && which >= 0 && which <= 5,
                "cf_pcg_debug_io: bad arguments");
     const size_t pl = (size_t)ws->nx * ws->ny;
     const PSlab &sb = ws->slabs[0];
     double *dev = nullptr;
     size_t cap = 0;
-    if (which == 0) {
+    if (which >= 3) {  // the single pass's r0: own array (nzl + 4 planes), the neighbours' matching planes
+        CF_REQUIRE(ws->spass, "cf_pcg_debug_io: no single-pass arrays");
+        if (which == 3) {
+            dev = ws->sp_alloc[0];
+            cap = pl * (size_t)(sb.nzl + 4);
+        } else {
+            dev = which == 4 ? ws->sset.s[0].lo[0][0] : ws->sset.s[0].hi[0][0];
+            cap = 2 * pl;
+            CF_REQUIRE(!write, "cf_pcg_debug_io: peer planes are read-only here");
+        }
+    } else if (which == 0) {
         dev = sb.alloc[0];
         cap = pl * (size_t)(sb.nzl + sb.lo + sb.hi);
     } else {
@@ -1401,6 +1411,13 @@ int cf_pcg_debug_io(cf_pcg *ws, int which, int write, double *host, int64_t n)
     if (write) CF_CUDA(cudaMemcpy(dev, host, (size_t)n * sizeof(double), cudaMemcpyHostToDevice));
     else CF_CUDA(cudaMemcpy(host, dev, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost));
     CF_CUDA(cudaDeviceSynchronize());
+    return CF_OK;
+}
+
+int cf_pcg_form(cf_pcg *ws, int *form_host)
+{
+    CF_REQUIRE(ws && form_host, "cf_pcg_form: null argument");
+    *form_host = ws->spass ? CF_CG_FORM_SPASS : CF_CG_FORM_TWO;
     return CF_OK;
 }
 

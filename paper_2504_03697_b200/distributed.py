@@ -138,6 +138,10 @@ class PeerSlabCG:
                                      _lib.stream()), "cf_pcg_create")
         self._h = hdl
         self.last_loop_ms = 0.0
+        form = ctypes.c_int()
+        _lib.check(lib.cf_pcg_form(hdl, ctypes.byref(form)), "cf_pcg_form")
+        # the single pass over slabs (one collective per iteration) or the two-kernel form
+        self.single_pass = form.value == _lib.CG_FORM_SPASS
         if distributed and nranks > 1:  # publish this rank's IPC handles, open the peers'
             import torch.distributed as dist
 

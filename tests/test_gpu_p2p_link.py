@@ -50,8 +50,29 @@ def _worker(rank, world, port, q):
                 buf = np.empty(pl)
                 _lib.check(lib.cf_pcg_debug_io(cg._h, which, 0, buf.ctypes.data, pl), "read")
                 got[which] = buf
+        # the single pass's arrays: two halo planes each side, two planes per neighbour
+        sp = {}
+        if cg.single_pass:
+            sp_planes = dec.z1 - dec.z0 + 4
+            mine2 = _pattern(rank + 10, sp_planes)
+            _lib.check(lib.cf_pcg_debug_io(cg._h, 3, 1, mine2.ctypes.data, mine2.size), "write sp")
+        dist.barrier()
+        if cg.single_pass:
+            for which, peer in ((4, rank - 1), (5, rank + 1)):
+                if 0 <= peer < world:
+                    buf = np.empty(2 * pl)
+                    _lib.check(lib.cf_pcg_debug_io(cg._h, which, 0, buf.ctypes.data, 2 * pl), "read sp")
+                    sp[which] = buf
         dist.barrier()
         res = {}
+        for which, buf in sp.items():
+            peer = rank - 1 if which == 4 else rank + 1
+            pdec = SlabDecomposition(NX, NY, NZ, world, peer)
+            ref = _pattern(peer + 10, pdec.z1 - pdec.z0 + 4).reshape(-1, pl)
+            # lower neighbour: its hi halo planes (array planes nzl + 2, + 3); upper: its planes 0, 1
+            lo_plane = (pdec.z1 - pdec.z0) + 2 if which == 4 else 0
+            want = ref[lo_plane:lo_plane + 2].ravel()
+            res[which] = bool(np.array_equal(buf, want)) or (buf[:3].tolist(), want[:3].tolist())
         for which, buf in got.items():
             peer = rank - 1 if which == 1 else rank + 1
             pdec = SlabDecomposition(NX, NY, NZ, world, peer)
@@ -86,4 +107,5 @@ def test_ipc_linking_across_processes(cuda, world):
     for rank, res, err in out:
         assert err is None, (rank, err)
         expect = {1} if rank == world - 1 else ({2} if rank == 0 else {1, 2})
+        expect |= {w + 3 for w in expect}  # the single pass's arrays (the default form)
         assert set(res) == expect and all(v is True for v in res.values()), (rank, res)
