@@ -496,6 +496,7 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
     bytes_in = sum(x.numel() * x.element_size() for x in phys[:3])
     bytes_out = sum(x.numel() * x.element_size() for x in phys)
     clock_summary = clocks.summary()
+    single_pass = bool(getattr(sim.cg, "single_pass", False))
     c5 = None
     if not args.no_extra and args.config5_steps > 0:
         del sim, sl, phys, pinned
@@ -522,11 +523,17 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
         "sim_steps_per_s": args.steps / (ms_max / 1e3), "cg_iterations": its,
         "fused_iter_us": iter_s * 1e6, "fused_iter_gbs_per_gpu": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": f"per-GPU z-slab CG iteration (dir + update + all-reduces + r halo; {args.collective})",
+                     "traffic": None,
+                     "kernel": (f"per-GPU z-slab CG iteration: one single-reduction pass (sp_slab_pass; halo planes "
+                                f"stored into the neighbours, one mailbox all-reduce; {args.collective})"
+                                if single_pass else
+                                f"per-GPU z-slab CG iteration (dir + update + all-reduces + r halo; {args.collective})"),
                      "algorithmic_bytes_per_iteration": 88 * cells_rank, "peak_kind": peak_kind},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_in * world,
                 "d2h_bytes_per_step": bytes_out * world},
-        "gpu_launches": sum(6 * i + 10 for i in its),
+        # step kernels (forces, advect, divergence, correction, halo packing ~10) + the CG's:
+        # single pass 2 init + 1 per iteration (+ odd-count early exit) + fix-up; two-kernel 6 per iteration
+        "gpu_launches": sum((i + (i & 1) + 3 + 10) if single_pass else (6 * i + 10) for i in its),
         "clocks": clock_summary,
         **({"config5": c5} if c5 else {}),
     }))
