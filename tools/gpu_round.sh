@@ -12,5 +12,8 @@ CF_CG_DIRECT=8 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read
 for part in step cg; do
   CF_CG_DIRECT=2 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/table_$part.csv python tools/ncu_table.py 256 $part > gpurun_out/table_$part.log 2>&1; echo table_$part=$?
 done
-CF_CG_DIRECT=2 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"cg_spass|advect_tma" -c 3 -o gpurun_out/round_full python tools/ncu_table.py 256 all > gpurun_out/ncu_full.log 2>&1; echo ncufull=$?
+CF_CG_DIRECT=2 timeout 600 ncu --set full --clock-control none --import-source on -k regex:cg_spass -s 4 -c 2 -o gpurun_out/round_cg_full python tools/probe_cg.py --n 256 --iters 10 --repeat 1 > gpurun_out/ncu_full.log 2>&1; echo ncufull=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:advect_tma -s 1 -c 1 -o gpurun_out/round_adv_full python tools/advect_check.py 256 0.5 > gpurun_out/ncu_adv.log 2>&1; echo ncuadv=$?
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --force-slabs --no-cpu-baseline > gpurun_out/bench_slabs.json 2> gpurun_out/bench_slabs.err; echo slabs=$?
+python tools/slab_probe.py --n 256 --iters 100 --slabs 1,2,4,8 > gpurun_out/slab_probe.txt 2>&1; echo slabprobe=$?
 timeout 1200 python tools/bench_configs.py > gpurun_out/configs.json 2> gpurun_out/configs.err; echo cfg=$?
