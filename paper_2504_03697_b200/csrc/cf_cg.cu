@@ -665,6 +665,7 @@ struct cf_cg {
     bool spass = false;
     int sp_ty = 16;  // tile height: 16 (one CTA per SM) or 8 (two; form 1 only)
     int sp_form = 2;  // 2: two rows per warp, SoA planes; 1: one row per warp (CF_SPASS_FORM=1)
+    int *sp_perm = nullptr;  // device tile permutation of the phase-aligned schedule
     cf::SpGeom sp_g{};
     int sp_ctas = 0;
     CUtensorMap m_spr[2]{}, m_spp[2]{}, m_spx{};
@@ -1063,7 +1064,7 @@ static void spass_setup(cf_cg *ws)
     cudaFuncSetAttribute(cg_spass_kernel<PK_NONE, TY, S, true, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::Smem);
     cudaFuncSetAttribute(cg_spass_kernel<PK_JCONST, TY, S, false, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::Smem);
     cudaFuncSetAttribute(cg_spass_kernel<PK_JCONST, TY, S, true, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::Smem);
-    SpGeom g{ws->bx.nx, ws->bx.ny, ws->bx.nz, (ws->bx.nx + kSpTX - 1) / kSpTX, (ws->bx.ny + TY - 1) / TY, 1};
+    SpGeom g{ws->bx.nx, ws->bx.ny, ws->bx.nz, (ws->bx.nx + kSpTX - 1) / kSpTX, (ws->bx.ny + TY - 1) / TY, 1, nullptr};
     const int bps = blocks_per_sm((const void *)cg_spass_kernel<PK_JCONST, TY, S, true, FORM>, G::Threads, G::Smem);
     const long long slots = (long long)num_sms() * (bps > 0 ? bps : 1), tiles = (long long)g.ntx * g.nty;
     // z-chunks: as many as fill the resident slots in one round, each >= 8 planes
@@ -1072,6 +1073,25 @@ static void spass_setup(cf_cg *ws)
     g.nchunk = (int)c;
     const long long items = tiles * c, rounds = (items + slots - 1) / slots;
     ws->sp_ctas = (int)((items + rounds - 1) / rounds);  // equal rounds for every CTA
+    // CF_SPASS_SCHED=phase: every resident slot busy on equal contiguous
+    // ranges, tiles permuted so that neighbours keep their phase (SpGeom)
+    const char *sched = getenv("CF_SPASS_SCHED");
+    if (sched && !strcmp(sched, "phase")) {
+        const long long G2 = std::max(1LL, std::min(slots, tiles * g.nz / 8));
+        // position p starts at unit p * nz; its phase within a range of
+        // tiles * nz / G2 units, scaled by G2 to stay integral
+        std::vector<std::pair<long long, int>> ph((size_t)tiles);
+        for (long long p = 0; p < tiles; ++p) ph[(size_t)p] = {(long long)g.nz * p * G2 % (tiles * g.nz), (int)p};
+        std::stable_sort(ph.begin(), ph.end());
+        std::vector<int> perm((size_t)tiles);
+        for (long long i = 0; i < tiles; ++i) perm[(size_t)ph[(size_t)i].second] = (int)i;  // y-major tiles by phase
+        if (!ws->sp_perm) cudaMalloc(&ws->sp_perm, (size_t)tiles * sizeof(int));
+        if (ws->sp_perm) {
+            cudaMemcpy(ws->sp_perm, perm.data(), (size_t)tiles * sizeof(int), cudaMemcpyHostToDevice);
+            g.perm = ws->sp_perm;
+            ws->sp_ctas = (int)G2;
+        }
+    }
     ws->sp_g = g;
     ws->spass = bps >= 1;
 }
@@ -1520,6 +1540,7 @@ int cf_cg_destroy(cf_cg *ws)
         if (b) cudaFree(b);
     if (ws->per_bar) cudaFree(ws->per_bar);
     if (ws->dic_lptr) cudaFree(ws->dic_lptr);
+    if (ws->sp_perm) cudaFree(ws->sp_perm);
     if (ws->dic.wave.prog_f) cudaFree(ws->dic.wave.prog_f);
     if (ws->dic.wave.ex_f) cudaFree(ws->dic.wave.ex_f);
     if (ws->dic.wave.ey_f) cudaFree(ws->dic.wave.ey_f);

@@ -73,9 +73,50 @@ struct Sp {
 // neighbours moments earlier and come from L2 (measured at 256^3: 128
 // lockstep CTAs 157 us per iteration against 169 for 148 CTAs on equal
 // contiguous (tile, plane) ranges, whose neighbours ran tens of planes apart).
+// perm != null selects the phase-aligned contiguous schedule instead: the
+// (tile position, plane) units are split into gridDim.x equal contiguous
+// ranges (every SM busy, ranges may cross a tile boundary), and perm maps a
+// position to a tile so that tiles adjacent in x share their phase and tiles
+// adjacent in y are L / (tiles / distinct phases) planes apart -- a few
+// planes, inside what L2 holds between neighbours (host: sp_phase_perm).
 struct SpGeom {
     int nx, ny, nz, ntx, nty, nchunk;
+    const int *perm;
     __host__ __device__ int items() const { return ntx * nty * nchunk; }
+};
+
+// This CTA's (tile, z0, z1) segments under either schedule.
+struct SpSegs {
+    const SpGeom &g;
+    const int nblk;
+    int j;              // item schedule: next item
+    long long u, u1;    // contiguous schedule: next unit, end
+    __device__ __forceinline__ SpSegs(const SpGeom &g_, int bid, int nblk_) : g(g_), nblk(nblk_), j(bid)
+    {
+        const long long units = (long long)g.ntx * g.nty * g.nz;
+        u = units * bid / nblk;
+        u1 = units * (bid + 1) / nblk;
+    }
+    __device__ __forceinline__ bool next(int &tile, int &za, int &zb)
+    {
+        if (!g.perm) {
+            if (j >= g.items()) return false;
+            const int t = g.ntx * g.nty;
+            tile = j % t;
+            const int chunk = j / t;
+            za = g.nz * chunk / g.nchunk;
+            zb = g.nz * (chunk + 1) / g.nchunk;
+            j += nblk;
+            return true;
+        }
+        if (u >= u1) return false;
+        const long long pos = u / g.nz;
+        za = (int)(u - pos * g.nz);
+        zb = (int)min((long long)g.nz, za + (u1 - u));
+        u += zb - za;
+        tile = g.perm[pos];
+        return true;
+    }
 };
 
 // z-slab form (cf_p2p.cu): the slab's arrays hold 2 halo planes below and
@@ -118,9 +159,9 @@ __device__ __forceinline__ void sp_produce(const CUtensorMap *mr, const CUtensor
     int slot = 0;
     uint32_t phase = 0;
     bool wrapped = false;  // the ring has been filled once: wait for releases
-    for (int j = bid; j < g.items(); j += nblk) {
-        const int tile = j % (g.ntx * g.nty), chunk = j / (g.ntx * g.nty);
-        const int za = g.nz * chunk / g.nchunk, zb = g.nz * (chunk + 1) / g.nchunk;
+    SpSegs segs(g, bid, nblk);
+    int tile, za, zb;
+    while (segs.next(tile, za, zb)) {
         const int x0 = (tile % g.ntx) * kSpTX, y0 = (tile / g.ntx) * TY;
         for (int s = 0; s < zb - za + 4; ++s) {
             if (wrapped) mbar_wait(&empty[slot], phase ^ 1u);
@@ -388,9 +429,9 @@ __device__ __forceinline__ void spass2_body(const CUtensorMap *mr, const CUtenso
         }
     };
     const bool edge = warp >= G::RowWarps;
-    for (int j = bid; j < g.items(); j += nblk) {
-        const int tile = j % (g.ntx * g.nty), chunk = j / (g.ntx * g.nty);
-        const int za = g.nz * chunk / g.nchunk, zb = g.nz * (chunk + 1) / g.nchunk;
+    SpSegs segs(g, bid, nblk);
+    int tile, za, zb;
+    while (segs.next(tile, za, zb)) {
         const int x0 = (tile % g.ntx) * kSpTX, y0 = (tile / g.ntx) * TY;
         const int L = zb - za, last = L + 3;
         if (!edge) {

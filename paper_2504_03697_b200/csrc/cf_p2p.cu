@@ -1146,7 +1146,7 @@ int cf_pcg_create(cf_pcg **out, int nx, int ny, int nz, double h, int order, int
                 cf::SpSlab &d = ws->sset.s[k];
                 d = cf::SpSlab{};
                 cf::SpGeom g{nx, ny, sb.nzl, (nx + cf::kSpTX - 1) / cf::kSpTX, (ny + cf::kSpSlabTY - 1) / cf::kSpSlabTY,
-                             1};
+                             1, nullptr};
                 const long long tiles = (long long)g.ntx * g.nty;
                 g.nchunk = (int)std::max(1LL, std::min(slots / std::max(1LL, tiles), (long long)sb.nzl / 8));
                 const long long items = tiles * g.nchunk, rounds = (items + slots - 1) / slots;
