@@ -667,7 +667,7 @@ __global__ void __launch_bounds__(Sp<TY, S, FORM>::Threads, Sp<TY, S, FORM>::Min
     using G = Sp<TY, S, FORM>;
     extern __shared__ unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full[S], empty[S];
-    __shared__ double red[32];
+    __shared__ double red[96];
     __shared__ int is_last;
     if (sc->done) {
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
@@ -700,18 +700,14 @@ __global__ void __launch_bounds__(Sp<TY, S, FORM>::Threads, Sp<TY, S, FORM>::Min
             spass2_body<PK, TY, S, false, XDBL>(&mr, &mp, &mx, g, off, diag, zc, r_out, p_new, x, alpha, alpha_prev,
                                                 beta, ring, full, empty, rr, gam, dlt, blockIdx.x, gridDim.x, io);
     }
-    rr = block_sum<G::Threads>(rr, red);
-    gam = block_sum<G::Threads>(gam, red);
-    dlt = block_sum<G::Threads>(dlt, red);
+    block_sum3<G::Threads>(rr, gam, dlt, red);
     if (threadIdx.x == 0) {
         partials[3 * blockIdx.x] = rr;
         partials[3 * blockIdx.x + 1] = gam;
         partials[3 * blockIdx.x + 2] = dlt;
     }
-    if (last_block(&tk->upd, &is_last)) {
-        rr = reduce_partials<G::Threads>(partials, gridDim.x, 3, red);
-        gam = reduce_partials<G::Threads>(partials + 1, gridDim.x, 3, red);
-        dlt = reduce_partials<G::Threads>(partials + 2, gridDim.x, 3, red);
+    if (last_block(&tk->upd, &is_last) && threadIdx.x < 32) {
+        warp_reduce_partials3(partials, gridDim.x, rr, gam, dlt);
         if (threadIdx.x == 0) {
             scalar_after_pass(sc, rr, gam, dlt);
             if (sc->done && use_cond) cudaGraphSetConditional(cond, 0);

@@ -74,6 +74,57 @@ __device__ __forceinline__ double block_sum(double v, double *smem)
     return v;
 }
 
+// Three sums with one pair of barriers (smem: 96 doubles); the totals on thread 0.
+template <int NT>
+__device__ __forceinline__ void block_sum3(double &a, double &b, double &c, double *smem)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, o);
+        b += __shfl_down_sync(0xffffffffu, b, o);
+        c += __shfl_down_sync(0xffffffffu, c, o);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NW = NT / 32;
+    __syncthreads();
+    if (lane == 0) {
+        smem[wid] = a;
+        smem[32 + wid] = b;
+        smem[64 + wid] = c;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        a = lane < NW ? smem[lane] : 0.0;
+        b = lane < NW ? smem[32 + lane] : 0.0;
+        c = lane < NW ? smem[64 + lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_down_sync(0xffffffffu, a, o);
+            b += __shfl_down_sync(0xffffffffu, b, o);
+            c += __shfl_down_sync(0xffffffffu, c, o);
+        }
+    }
+}
+
+// Fixed-order sums of `count` interleaved partial triples by warp 0 (no block
+// barrier); the totals on thread 0.
+__device__ __forceinline__ void warp_reduce_partials3(const double *p, int count, double &a, double &b, double &c)
+{
+    const int lane = threadIdx.x & 31;
+    a = b = c = 0.0;
+    for (int i = lane; i < count; i += 32) {
+        a += __ldcg(p + 3 * (size_t)i);
+        b += __ldcg(p + 3 * (size_t)i + 1);
+        c += __ldcg(p + 3 * (size_t)i + 2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, o);
+        b += __shfl_down_sync(0xffffffffu, b, o);
+        c += __shfl_down_sync(0xffffffffu, c, o);
+    }
+}
+
 template <int NT>
 __device__ __forceinline__ double block_max(double v, double *smem)
 {
