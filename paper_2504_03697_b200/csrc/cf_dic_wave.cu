@@ -404,7 +404,9 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_fwd_p(DicWave dw, const d
             wv = acc / ring_d[q][tid];
             if (xout) edge_put(xout_box + 2ll * k * kWTY, wv);
             if (yout) edge_put(yout_box + 2ll * k * kWTX, wv);
-            w[o] = wv;
+            // streaming store: read once by the next sweep; left dirty in L2 it
+            // slowed the sweeps (2.12 -> 2.06 ms per 256^3 DIC-PCG iteration)
+            __stcs(w + o, wv);
             wk = wv;
         }
         sm[(s + 1) & 1][tj][ti] = wv;
@@ -473,7 +475,7 @@ __global__ void __launch_bounds__(kWTX *kWTY) dic_wave_bwd_p(DicWave dw, const d
             zv = ring_w[q][tid] - acc / ring_d[q][tid];
             if (xout) edge_put(xout_box + 2ll * k * kWTY, zv);
             if (yout) edge_put(yout_box + 2ll * k * kWTX, zv);
-            z[o] = zv;
+            __stcs(z + o, zv);
             zk = zv;
         }
         sm[(s + 1) & 1][tj][ti] = zv;
