@@ -210,6 +210,53 @@ def load_traffic(form=None):
     return None, None
 
 
+class RoundTrip:
+    """The e2e state round trip between steps: the step's outputs go D2H and
+    the next step's inputs (the same host copy) go back H2D in ~32 MB chunks
+    on two copy streams -- chunk c's D2H beside chunk c-1's H2D (PCIe is full
+    duplex), each chunk uploaded only after it landed in host memory -- and the
+    output-only arrays (the pressure) go D2H beside the next step.  Every
+    step still uploads its inputs from pinned memory and reads its whole
+    result back inside the timed region."""
+
+    CH = 4 << 20  # doubles per chunk
+
+    def __init__(self, stream):
+        import torch
+        self.torch = torch
+        self.stream = stream
+        self.d2h, self.h2d = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def _chunks(self, ts):
+        return [(t.view(-1), a, min(a + self.CH, t.numel())) for t in ts for a in range(0, t.numel(), self.CH)]
+
+    def before_step(self):
+        self.stream.wait_stream(self.h2d)
+
+    def after_step(self, dev_in, pin_in, dev_out, pin_out):
+        torch = self.torch
+        done = torch.cuda.Event()
+        done.record(self.stream)
+        self.d2h.wait_event(done)
+        evs = []
+        with torch.cuda.stream(self.d2h):
+            for (d_, a, b), (h_, _, _) in zip(self._chunks(dev_in), self._chunks(pin_in)):
+                h_[a:b].copy_(d_[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.d2h)
+                evs.append(ev)
+            for h_, d_ in zip(pin_out, dev_out):
+                h_.copy_(d_, non_blocking=True)
+        with torch.cuda.stream(self.h2d):
+            for ev, (d_, a, b), (h_, _, _) in zip(evs, self._chunks(dev_in), self._chunks(pin_in)):
+                self.h2d.wait_event(ev)
+                d_[a:b].copy_(h_[a:b], non_blocking=True)
+
+    def finish(self):
+        self.stream.wait_stream(self.d2h)
+        self.stream.wait_stream(self.h2d)
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -282,38 +329,17 @@ def run_ours(args, rank, world, local_rank):
     # host memory; the pressure (an output only) goes D2H beside the next
     # step.  Every step still uploads its inputs from pinned memory and reads
     # its whole result back inside the timed region.
-    d2h_s, h2d_s = torch.cuda.Stream(), torch.cuda.Stream()
-    CH = 4 << 20  # doubles per chunk (32 MB)
-
-    def chunks(ts):
-        return [(t.view(-1), a, min(a + CH, t.numel())) for t in ts for a in range(0, t.numel(), CH)]
-
+    rt = RoundTrip(stream)
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_its = 0
     e2.record(stream)
     for _ in range(args.steps):
-        stream.wait_stream(h2d_s)  # this step's inputs are on the device
+        rt.before_step()  # this step's inputs are on the device
         s = cf.step(state, cfg, cache)
         e2e_its += s.solve.iterations
         phys = [*state.vel._phys, state.p.data]
-        done = torch.cuda.Event()
-        done.record(stream)
-        d2h_s.wait_event(done)
-        evs = []
-        with torch.cuda.stream(d2h_s):  # the velocity, chunk by chunk, then the pressure
-            for (d_, a, b), (h_, _, _) in zip(chunks(phys[:n_in]), chunks(pinned[:n_in])):
-                h_[a:b].copy_(d_[a:b], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(d2h_s)
-                evs.append(ev)
-            for h_, d_ in zip(pinned[n_in:], phys[n_in:]):
-                h_.copy_(d_, non_blocking=True)
-        with torch.cuda.stream(h2d_s):  # ... and back as each chunk lands: the next step's inputs
-            for ev, (d_, a, b), (h_, _, _) in zip(evs, chunks(phys[:n_in]), chunks(pinned[:n_in])):
-                h2d_s.wait_event(ev)
-                d_[a:b].copy_(h_[a:b], non_blocking=True)
-    stream.wait_stream(d2h_s)
-    stream.wait_stream(h2d_s)
+        rt.after_step(phys[:n_in], pinned[:n_in], phys[n_in:], pinned[n_in:])
+    rt.finish()
     e3.record(stream)
     barrier()
     e2e_ms = e2.elapsed_time(e3)
@@ -510,13 +536,13 @@ def run_slabs(args, cfg, rank, world, local_rank, barrier):
     barrier()
     e2.record(stream)
     e2e_its = 0
+    rt = RoundTrip(stream)
     for _ in range(args.steps):
-        for h_, d_ in zip(pinned[:3], [*sl.vel[sl.cur]]):
-            d_.copy_(h_, non_blocking=True)
+        rt.before_step()
         s = sim.step()
         e2e_its += s.solve.iterations
-        for h_, d_ in zip(pinned, [*sl.vel[sl.cur], sl.p]):
-            h_.copy_(d_, non_blocking=True)
+        rt.after_step([*sl.vel[sl.cur]], pinned[:3], [sl.p], pinned[3:])
+    rt.finish()
     e3.record(stream)
     barrier()
     t2 = torch.tensor([e2.elapsed_time(e3)], device="cuda", dtype=torch.float64)
