@@ -17,6 +17,13 @@
 //   halo   r boundary planes: D2D copies between local slabs, ncclSend/Recv
 //          with the neighbouring ranks
 //
+// The halo overlaps the reduction: the neighbour send/recv pairs go into the
+// same NCCL group as the (r.r, r.z) all-reduce, so one NCCL launch moves both
+// concurrently, and the D2D copies between local slabs run on a side stream
+// forked after the update kernels and joined before the next dir kernels.
+// (Nothing of the next iteration can start earlier: every plane of the dir
+// kernel needs beta, the all-reduce's result.)
+//
 // Every rank applies the same all-reduced scalars, so convergence decisions
 // are identical everywhere; kernels early-exit once `done` is set, and the
 // host polls `done` once per batch of iterations.
@@ -113,6 +120,8 @@ struct cf_dcg {
     cf::CgScalars *sc = nullptr, *sc_host = nullptr;
     double *red = nullptr, *red_sum = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t side = nullptr;                      // local halo copies
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     float last_ms = 0.f;
     int batch = 8;
     cudaGraphExec_t exec = nullptr;  // two captured iterations
@@ -150,30 +159,73 @@ static int reduce_phase(cf_dcg *ws, int ncomp, int phase, cudaStream_t s)
     return CF_OK;
 }
 
-// r boundary planes into the neighbours' halo planes.
-static int exchange_r(cf_dcg *ws, cudaStream_t s)
+// The neighbour-rank half of the r halo: this rank's boundary planes out, the
+// neighbours' into the halo planes (enqueued inside the caller's NCCL group).
+static int halo_p2p(cf_dcg *ws, cudaStream_t s)
+{
+    const size_t pl = (size_t)ws->nx * ws->ny;
+    Slab &f = ws->slabs.front(), &l = ws->slabs.back();
+    if (ws->lo_rank >= 0) {
+        CF_NCCL(ncclSend(f.r, pl, ncclDouble, ws->lo_rank, ws->comm, s));
+        CF_NCCL(ncclRecv(f.r - pl, pl, ncclDouble, ws->lo_rank, ws->comm, s));
+    }
+    if (ws->hi_rank >= 0) {
+        CF_NCCL(ncclSend(l.r + pl * (l.nzl - 1), pl, ncclDouble, ws->hi_rank, ws->comm, s));
+        CF_NCCL(ncclRecv(l.r + pl * l.nzl, pl, ncclDouble, ws->hi_rank, ws->comm, s));
+    }
+    return CF_OK;
+}
+
+// The local half: slab k's top plane -> slab k+1's lo halo, slab k+1's bottom
+// plane -> slab k's hi halo.
+static int halo_local(cf_dcg *ws, cudaStream_t s)
 {
     const size_t pl = (size_t)ws->nx * ws->ny;
     const size_t bytes = pl * sizeof(double);
     auto &sl = ws->slabs;
     for (size_t k = 0; k + 1 < sl.size(); ++k) {
-        // slab k's top plane -> slab k+1's lo halo; slab k+1's bottom plane -> slab k's hi halo
         CF_CUDA(cudaMemcpyAsync(sl[k + 1].r - pl, sl[k].r + pl * (sl[k].nzl - 1), bytes, cudaMemcpyDeviceToDevice, s));
         CF_CUDA(cudaMemcpyAsync(sl[k].r + pl * sl[k].nzl, sl[k + 1].r, bytes, cudaMemcpyDeviceToDevice, s));
     }
-    if (ws->comm && (ws->lo_rank >= 0 || ws->hi_rank >= 0)) {
-        Slab &f = sl.front(), &l = sl.back();
-        CF_NCCL(ncclGroupStart());
-        if (ws->lo_rank >= 0) {
-            CF_NCCL(ncclSend(f.r, pl, ncclDouble, ws->lo_rank, ws->comm, s));
-            CF_NCCL(ncclRecv(f.r - pl, pl, ncclDouble, ws->lo_rank, ws->comm, s));
+    return CF_OK;
+}
+
+// After the update kernels: the (r.r, r.z) reduction and the r halo
+// exchange, overlapped (see the header).  `overlap` false (the init) runs
+// them one after the other.
+static int reduce_and_exchange(cf_dcg *ws, int phase, bool overlap, cudaStream_t s)
+{
+    const bool local = ws->slabs.size() > 1;
+    const bool peers = ws->comm && (ws->lo_rank >= 0 || ws->hi_rank >= 0);
+    if (!overlap) {
+        int rc = reduce_phase(ws, 2, phase, s);
+        if (rc == CF_OK && local) rc = halo_local(ws, s);
+        if (rc == CF_OK && peers) {
+            CF_NCCL(ncclGroupStart());
+            rc = halo_p2p(ws, s);
+            CF_NCCL(ncclGroupEnd());
         }
-        if (ws->hi_rank >= 0) {
-            CF_NCCL(ncclSend(l.r + pl * (l.nzl - 1), pl, ncclDouble, ws->hi_rank, ws->comm, s));
-            CF_NCCL(ncclRecv(l.r + pl * l.nzl, pl, ncclDouble, ws->hi_rank, ws->comm, s));
-        }
-        CF_NCCL(ncclGroupEnd());
+        return rc;
     }
+    if (local) {
+        CF_CUDA(cudaEventRecord(ws->ev_fork, s));
+        CF_CUDA(cudaStreamWaitEvent(ws->side, ws->ev_fork, 0));
+        int rc = halo_local(ws, ws->side);
+        if (rc != CF_OK) return rc;
+        CF_CUDA(cudaEventRecord(ws->ev_join, ws->side));
+    }
+    dcg_sum_kernel<<<1, 32, 0, s>>>(ws->red, (int)ws->slabs.size(), 2, ws->red_sum, ws->sc);
+    CF_CHECK_LAUNCH("dcg_sum_kernel");
+    if (ws->comm) {
+        CF_NCCL(ncclGroupStart());
+        ncclResult_t r = ncclAllReduce(ws->red_sum, ws->red_sum, 2, ncclDouble, ncclSum, ws->comm, s);
+        int rc = r == ncclSuccess ? (peers ? halo_p2p(ws, s) : CF_OK) : nccl_fail(r, "ncclAllReduce");
+        CF_NCCL(ncclGroupEnd());
+        if (rc != CF_OK) return rc;
+    }
+    dcg_scalar_kernel<<<1, 32, 0, s>>>(ws->sc, ws->red_sum, phase);
+    CF_CHECK_LAUNCH("dcg_scalar_kernel");
+    if (local) CF_CUDA(cudaStreamWaitEvent(s, ws->ev_join, 0));
     return CF_OK;
 }
 
@@ -198,9 +250,7 @@ static int iteration(cf_dcg *ws, int half, double zc, cudaStream_t s)
             sb.tk, 0, 0, ws->red + 2 * k);
         CF_CHECK_LAUNCH("cg_update_tma (slab)");
     }
-    rc = reduce_phase(ws, 2, PH_UPD, s);
-    if (rc != CF_OK) return rc;
-    return exchange_r(ws, s);
+    return reduce_and_exchange(ws, PH_UPD, true, s);
 }
 
 // Two iterations (p buffers back to their original roles) captured once into
@@ -298,7 +348,10 @@ int cf_dcg_destroy(cf_dcg *ws)
     if (ws->red_sum) cudaFree(ws->red_sum);
     if (ws->ev0) cudaEventDestroy(ws->ev0);
     if (ws->ev1) cudaEventDestroy(ws->ev1);
+    if (ws->ev_fork) cudaEventDestroy(ws->ev_fork);
+    if (ws->ev_join) cudaEventDestroy(ws->ev_join);
     if (ws->exec) cudaGraphExecDestroy(ws->exec);
+    if (ws->side) cudaStreamDestroy(ws->side);
     if (ws->comm) ncclCommDestroy(ws->comm);
     delete ws;
     return CF_OK;
@@ -380,6 +433,9 @@ int cf_dcg_create(cf_dcg **out, int nx, int ny, int nz, double h, int order, int
     if (e == cudaSuccess) e = cudaMalloc(&ws->red_sum, 2 * sizeof(double));
     if (e == cudaSuccess) e = cudaEventCreate(&ws->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&ws->ev1);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ws->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ws->ev_join, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ws->side, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         int rc = cf::cuda_fail(e, "cf_dcg_create");
         cf_dcg_destroy(ws);
@@ -427,8 +483,7 @@ int cf_dcg_solve(cf_dcg *ws, const double *const *b_slabs, double *const *x_slab
                                                                   ws->red + 2 * k);
         CF_CHECK_LAUNCH("dcg_init_kernel");
     }
-    int rc = cf::reduce_phase(ws, 2, cf::PH_INIT, s);
-    if (rc == CF_OK) rc = cf::exchange_r(ws, s);
+    int rc = cf::reduce_and_exchange(ws, cf::PH_INIT, false, s);
     if (rc != CF_OK) return rc;
     CF_CUDA(cudaEventRecord(ws->ev0, s));
     if (ws->order == CF_ORDER_CSR)

@@ -14,6 +14,8 @@ for part in step cg; do
 done
 CF_CG_DIRECT=2 timeout 600 ncu --set full --clock-control none --import-source on -k regex:cg_spass -s 4 -c 2 -o gpurun_out/round_cg_full python tools/probe_cg.py --n 256 --iters 10 --repeat 1 > gpurun_out/ncu_full.log 2>&1; echo ncufull=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:advect_tma -s 1 -c 1 -o gpurun_out/round_adv_full python tools/advect_check.py 256 0.5 > gpurun_out/ncu_adv.log 2>&1; echo ncuadv=$?
+python tools/slab_projection.py 1 2 4 8 > gpurun_out/slab_projection.txt 2>&1; echo proj=$?
+for i in 1 2 3; do python tools/dic_step_probe.py 40; done > gpurun_out/dic_probe.txt 2>&1; echo dic=$?
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --force-slabs --no-cpu-baseline > gpurun_out/bench_slabs.json 2> gpurun_out/bench_slabs.err; echo slabs=$?
 python tools/slab_probe.py --n 256 --iters 100 --slabs 1,2,4,8 > gpurun_out/slab_probe.txt 2>&1; echo slabprobe=$?
 timeout 1200 python tools/bench_configs.py > gpurun_out/configs.json 2> gpurun_out/configs.err; echo cfg=$?
