@@ -105,6 +105,11 @@ int cf_dic_apply(int64_t n, const int32_t *lp, const int32_t *lc, const double *
                  const int32_t *uc, const double *uv, const double *d, const int32_t *level_rows,
                  const int64_t *level_ptr_host, int nlevels, const double *r, double *w, double *z,
                  void *stream);
+/* q[i] = a[i] / d[i] computed the way the skewed DIC sweeps divide (the
+ * reciprocal refinement of the compiler's fp64 division hoisted out of the
+ * sweep, its last three operations per cell; src/precond.py:44, :54 `s / d[i]`).
+ * Bit-identical to IEEE division; exposed so the tests can check exactly that. */
+int cf_dic_divide(int64_t n, const double *a, const double *d, double *q, void *stream);
 
 /* ---- fused conjugate gradient (src/solver.py:33-171) -------------------- */
 typedef struct cf_cg cf_cg;

@@ -59,6 +59,7 @@ _SIGNATURES = {
     "cf_level_schedule": ([_i64, _vp, _vp, _vp, _vp], _int),
     "cf_dic_factor": ([_i64, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp, _vp, _vp], _int),
     "cf_dic_apply": ([_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp, _vp, _vp, _vp], _int),
+    "cf_dic_divide": ([_i64, _vp, _vp, _vp, _vp], _int),
     "cf_cg_set_dic": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int], _int),
     "cf_cg_create": ([ctypes.POINTER(_vp), _int, _int, _int, _dbl, _int, _vp], _int),
     "cf_cg_destroy": ([_vp], _int),

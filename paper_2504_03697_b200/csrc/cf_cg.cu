@@ -1544,6 +1544,7 @@ int cf_cg_destroy(cf_cg *ws)
     if (ws->dic.wave.prog_f) cudaFree(ws->dic.wave.prog_f);
     if (ws->dic.wave.ex_f) cudaFree(ws->dic.wave.ex_f);
     if (ws->dic.wave.ey_f) cudaFree(ws->dic.wave.ey_f);
+    cf::dic_skew_free(ws->dic.skew);
     if (ws->sc) cudaFree(ws->sc);
     if (ws->tk) cudaFree(ws->tk);
     if (ws->sc_host) cudaFreeHost(ws->sc_host);

@@ -33,6 +33,25 @@ struct DicWave {
     bool ok = false;
 };
 
+// Skewed-warp form of the sweeps (cf_dic_skew.cu): a warp owns a 32 x J tile
+// column, lane l the cells x0 + l, and walks it with a skew of one step per
+// lane, so every in-tile dependency is a register (y, z) or a shuffle (x).
+struct DicSkew {
+    int J = 0, logJ = 0;                 // tile rows (power of two)
+    int ntx = 0, nty = 0, nz = 0;        // tiles in x / y, planes
+    int nrows = 0;                       // steps per tile (padded to whole blocks)
+    int trows = 0;                       // rows per tile of the skewed arrays (nrows + padding on both sides)
+    int grid = 0;                        // CTAs launched (one warp each, tickets -> tiles)
+    double *buf = nullptr;               // the allocation behind dy and wsk
+    double *dy = nullptr;                // (d~, its refined reciprocal) pairs: [tile][row][lane]
+    double *wsk = nullptr;               // w: [tile][row][lane]
+    // face mailboxes of the two sweeps: x [tile][q], y [tile][k][lane]
+    double *mx_f = nullptr, *my_f = nullptr, *mx_b = nullptr, *my_b = nullptr;
+    long long sk_cap = 0, mx_cap = 0, my_cap = 0;  // allocated doubles (re-sized per setup)
+    double gf = 0.0, gb = 0.0;           // ghost values: L * gf = +0, U * gb = -0 (exact no-ops in the sums)
+    bool ok = false;
+};
+
 struct DicData {
     long long n = 0;
     const int32_t *lp = nullptr, *lc = nullptr;  // strict lower triangle (CSR)
@@ -43,6 +62,7 @@ struct DicData {
     const int32_t *rows = nullptr;               // rows sorted by level
     std::vector<long long> level_ptr;            // host: level l = rows[level_ptr[l]:level_ptr[l+1]]
     DicWave wave;                                // used instead of the levels when wave.ok
+    DicSkew skew;                                // used instead of the tiled wavefront when skew.ok
 };
 
 // z = M^-1 r through w; if `done` is non-null every launch exits when *done
@@ -54,5 +74,11 @@ int dic_apply_launch(const DicData &dd, const double *r, double *w, double *z, c
 // (dd.wave.ok tells); and apply them.  cf_dic_wave.cu.
 int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s);
 int dic_wave_apply(const DicData &dd, const double *r, double *w, double *z, const int *done, cudaStream_t s);
+
+// Skewed-warp sweeps (cf_dic_skew.cu): set up after dic_wave_setup verified
+// the pattern (uses wave.lval / uval / ticket); apply = both sweeps.
+int dic_skew_setup(DicData &dd, cudaStream_t s);
+int dic_skew_apply(const DicData &dd, const double *r, double *z, const int *done, cudaStream_t s);
+void dic_skew_free(DicSkew &sk);
 
 }  // namespace cf

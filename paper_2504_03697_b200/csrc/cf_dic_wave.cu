@@ -604,7 +604,7 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
     int bpf = 0, bpb = 0;
     CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpf, wk.fwd, wk.threads, 0));
     CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpb, wk.bwd, wk.threads, 0));
-    if ((long long)std::min(bpf, bpb) * num_sms() < ntiles) return CF_OK;
+    const bool resident = (long long)std::min(bpf, bpb) * num_sms() >= ntiles;
     // the off-diagonal values (the first lower / upper entry of the first row that has one)
     double vals[2] = {0.0, 0.0};
     int32_t p[2];
@@ -634,6 +634,19 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
     dw.prog_b = dw.prog_f + ntiles;
     dw.ticket = dw.prog_f + 2 * ntiles;
     CF_CUDA(cudaMemsetAsync(dw.prog_f, 0, (2 * (size_t)ntiles + 2) * sizeof(int), s));
+    dw.lval = vals[0];
+    dw.uval = vals[1];
+    // the skewed-warp sweeps (cf_dic_skew.cu) replace the tiled wavefront when they can be set up
+    {
+        const int rc = dic_skew_setup(dd, s);
+        if (rc != CF_OK) return rc;
+        if (dd.skew.ok) {
+            CF_CUDA(cudaStreamSynchronize(s));
+            dw.ok = true;
+            return CF_OK;
+        }
+    }
+    if (!resident) return CF_OK;
     if (mailbox_shape(dw.shape)) {  // mailboxes of the pipelined sweeps: x edges ty, y edges tx slots per tile plane
         const long long nbx = 2ll * ntiles * nz * ty, nby = 2ll * ntiles * nz * tx;  // 16-byte slots
         int rc = ensure_buf(dw.ex_f, dw.ex_cap, 2 * nbx);
@@ -665,6 +678,7 @@ int dic_wave_setup(DicData &dd, int nx, int ny, int nz, cudaStream_t s)
 int dic_wave_apply(const DicData &dd, const double *r, double *w, double *z, const int *done, cudaStream_t s)
 {
     const DicWave &dw = dd.wave;
+    if (dd.skew.ok) return dic_skew_apply(dd, r, z, done, s);
     const int ntiles = dw.ntx * dw.nty;
     if (dw.shape >= 5) {  // wider / taller tiles, depth 2
         if (dw.shape == 5) dic_wave_fwd_p<32, 8, 2><<<ntiles, 256, 0, s>>>(dw, dd.d, r, w, done);

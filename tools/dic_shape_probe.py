@@ -12,6 +12,8 @@ import paper_2504_03697_b200 as cf  # noqa: E402
 
 shapes = [(16, 8, 256), (16, 8, 1024), (32, 8, 256), (16, 16, 256), (64, 8, 256), (16, 64, 256),
           (256, 8, 256), (16, 256, 256), (128, 128, 128), (256, 256, 256)]
+if len(sys.argv) == 4:  # one box from the command line: nx ny nz
+    shapes = [tuple(int(a) for a in sys.argv[1:4])]
 for shp in shapes[: int(os.environ.get("NSHAPES", len(shapes)))]:
     nx, ny, nz = shp
     b = np.random.default_rng(0).uniform(-1, 1, nx * ny * nz)
