@@ -19,3 +19,6 @@ for i in 1 2 3; do python tools/dic_step_probe.py 40; done > gpurun_out/dic_prob
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --force-slabs --no-cpu-baseline > gpurun_out/bench_slabs.json 2> gpurun_out/bench_slabs.err; echo slabs=$?
 python tools/slab_probe.py --n 256 --iters 100 --slabs 1,2,4,8 > gpurun_out/slab_probe.txt 2>&1; echo slabprobe=$?
 timeout 1200 python tools/bench_configs.py > gpurun_out/configs.json 2> gpurun_out/configs.err; echo cfg=$?
+bash tools/gpu_skew_ncu.sh > gpurun_out/skew_ncu.out 2>&1; echo skewncu=$?
+bash tools/gpu_skew_dbg.sh > gpurun_out/skew_dbg.out 2>&1; echo skewdbg=$?
+timeout 300 python tools/dic_probe.py 128 256 2>&1 | grep dic > gpurun_out/dic_sizes.txt; echo dicsizes=$?

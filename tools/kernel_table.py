@@ -40,6 +40,8 @@ def alg_bytes(name, n):
         (r"csr_spmv_kernel", 12 * nnz + 4 * (N + 1) + 16 * N, "int32 CSR + x read; y written"),
         (r"sym_spmv_kernel", 24 * N + 24 * U + 8 * (N + 1), "diag, upper + transpose arrays, x read; y written"),
         (r"dic_wave_(fwd|bwd)", 24 * N, "r (w), d read; w (z) written"),
+        (r"dic_skew_fwd", 32 * N, "r, (d, 1/d) read; w written"),
+        (r"dic_skew_bwd", 40 * N, "w, (d, 1/d) read; z written"),
     ]
     for pat, b, what in table:
         if re.search(pat, name):
