@@ -240,6 +240,67 @@ __global__ void __launch_bounds__(kCellThreads) divergence_kernel(Vel3 in, SlabZ
     }
 }
 
+// The same as a z-march (round 2): a CTA owns a 32 x 8 column of cells over a
+// chunk of planes, a thread one (i, j) column -- no integer division per
+// cell, running pointers, w at k kept from the previous plane, and with a
+// power-of-two h the reference's "/ h" as an exact multiplication.  Same
+// operations in the same order: bit-identical (the flat kernel above stays
+// for the parity test and odd pitches).
+constexpr int kDivTX = 32, kDivTY = 8;
+template <bool POW2>
+__global__ void __launch_bounds__(kCellThreads) divergence_march(Vel3 in, SlabZ sz, double h, double inv_h,
+                                                                 double scale, int do_scale, int nchunk, double *out,
+                                                                 double *partials, unsigned int *ticket,
+                                                                 double *result)
+{
+    __shared__ double red[32];
+    __shared__ int is_last;
+    const int nx = sz.nx, ny = sz.ny, nzl = sz.z1 - sz.z0;
+    const int tx = threadIdx.x % kDivTX, ty = threadIdx.x / kDivTX;
+    const int ntx = (nx + kDivTX - 1) / kDivTX;
+    int bid = blockIdx.x;
+    const int chunk = bid % nchunk;
+    bid /= nchunk;
+    const int i = (bid % ntx) * kDivTX + tx, j = (bid / ntx) * kDivTY + ty;
+    const int k0 = sz.z0 + (int)((long long)chunk * nzl / nchunk), k1 = sz.z0 + (int)((long long)(chunk + 1) * nzl / nchunk);
+    double mx = 0.0;
+    if (i < nx && j < ny && k0 < k1) {
+        const Comp &cu = in.c[0], &cv = in.c[1], &cw = in.c[2];
+        const double *pu = cu.a + cu.off(i, j, k0), *pv = cv.a + cv.off(i, j, k0), *pw = cw.a + cw.off(i, j, k0);
+        const unsigned su = (unsigned)cu.ld * (unsigned)cu.nb, sv = (unsigned)cv.ld * (unsigned)cv.nb,
+                       sw = (unsigned)cw.ld * (unsigned)cw.nb, rv = (unsigned)cv.ld;
+        double *po = out + ((long long)(k0 - sz.z0) * ny + j) * nx + i;
+        const long long so = (long long)nx * ny;
+        double w0 = __ldg(pw);
+        for (int k = k0; k < k1; ++k) {
+            const double u0 = __ldg(pu), u1 = __ldg(pu + 1), v0 = __ldg(pv), v1 = __ldg(pv + rv), w1 = __ldg(pw + sw);
+            // src/grid.py:145-154: ((((u1-u0)+v1)-v0)+w1)-w0, then /h, then * scale (src/sim.py:360)
+            double t = u1 - u0;
+            t = t + v1;
+            t = t - v0;
+            t = t + w1;
+            t = t - w0;
+            double d = POW2 ? t * inv_h : t / h;
+            if (do_scale) d = scale * d;
+            *po = d;
+            mx = fmax(mx, fabs(d));
+            w0 = w1;
+            pu += su;
+            pv += sv;
+            pw += sw;
+            po += so;
+        }
+    }
+    mx = block_max<kCellThreads>(mx, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = mx;
+    if (last_block(ticket, &is_last)) {
+        double v = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += kCellThreads) v = fmax(v, __ldcg(partials + b));
+        v = block_max<kCellThreads>(v, red);
+        if (threadIdx.x == 0) *result = v;
+    }
+}
+
 // src/sim.py:434-449.  One thread per owned cell: it recomputes the
 // corrected values of its six faces from the OLD field (p with a one-plane
 // halo in z, ghost p = 0 outside the box), takes the cell divergence of the
@@ -292,6 +353,84 @@ __global__ void __launch_bounds__(kCellThreads) correct_kernel(Vel3 in, double *
         if (i == nx - 1) nu[cu.off(nx, j, k)] = 0.0;
         if (j == ny - 1) nv[cv.off(i, ny, k)] = 0.0;
         if (k == nz - 1) nw[cw.off(i, j, nz)] = 0.0;
+    }
+    mx = block_max<kCellThreads>(mx, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = mx;
+    if (last_block(ticket, &is_last)) {
+        double v = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += kCellThreads) v = fmax(v, __ldcg(partials + b));
+        v = block_max<kCellThreads>(v, red);
+        if (threadIdx.x == 0) *result = v;
+    }
+}
+
+// The correction as a z-march (round 2; see divergence_march): a thread owns an
+// (i, j) column of a chunk of planes, keeps p at k and k+1 and the corrected
+// upper w face (which is the next cell's lower one: the same operands and
+// operations) in registers -- 10 loads per cell instead of 13, no integer
+// division, "/ h" as an exact multiplication for a power-of-two h.
+// Bit-identical to correct_kernel.
+template <bool POW2>
+__global__ void __launch_bounds__(kCellThreads) correct_march(Vel3 in, double *nu, double *nv, double *nw,
+                                                              const double *__restrict__ p, SlabZ sz, double h,
+                                                              double inv_h, double coef, int nchunk, double *partials,
+                                                              unsigned int *ticket, double *result)
+{
+    __shared__ double red[32];
+    __shared__ int is_last;
+    const int nx = sz.nx, ny = sz.ny, nz = sz.nz, nzl = sz.z1 - sz.z0;
+    const int tx = threadIdx.x % kDivTX, ty = threadIdx.x / kDivTX;
+    const int ntx = (nx + kDivTX - 1) / kDivTX;
+    int bid = blockIdx.x;
+    const int chunk = bid % nchunk;
+    bid /= nchunk;
+    const int i = (bid % ntx) * kDivTX + tx, j = (bid / ntx) * kDivTY + ty;
+    const int k0 = sz.z0 + (int)((long long)chunk * nzl / nchunk), k1 = sz.z0 + (int)((long long)(chunk + 1) * nzl / nchunk);
+    double mx = 0.0;
+    if (i < nx && j < ny && k0 < k1) {
+        const Comp &cu = in.c[0], &cv = in.c[1], &cw = in.c[2];
+        const bool hxm = i > 0, hxp = i < nx - 1, hym = j > 0, hyp = j < ny - 1;
+        const int pl = nx * ny;
+        const double *pp = p + ((long long)(k0 - sz.z0) * ny + j) * nx + i;
+        unsigned ou = cu.off(i, j, k0), ov = cv.off(i, j, k0), ow = cw.off(i, j, k0);
+        const unsigned su = (unsigned)cu.ld * (unsigned)cu.nb, sv = (unsigned)cv.ld * (unsigned)cv.nb,
+                       sw = (unsigned)cw.ld * (unsigned)cw.nb, rv = (unsigned)cv.ld;
+        double pc = __ldg(pp);
+        // lower face: interior -> coef*(p - p_prev); wall -> coef*p
+        // upper face: interior -> coef*(p_next - p); wall -> coef*(0.0 - p)
+        double w0 = __ldg(cw.a + ow) - coef * (k0 > 0 ? pc - __ldg(pp - pl) : pc);
+        for (int k = k0; k < k1; ++k) {
+            const bool hzp = k < nz - 1;
+            const double pn = hzp ? __ldg(pp + pl) : 0.0;
+            const double du0 = hxm ? pc - __ldg(pp - 1) : pc;
+            const double du1 = hxp ? __ldg(pp + 1) - pc : 0.0 - pc;
+            const double dv0 = hym ? pc - __ldg(pp - nx) : pc;
+            const double dv1 = hyp ? __ldg(pp + nx) - pc : 0.0 - pc;
+            const double dw1 = hzp ? pn - pc : 0.0 - pc;
+            const double u0 = __ldg(cu.a + ou) - coef * du0;
+            const double u1 = __ldg(cu.a + ou + 1) - coef * du1;
+            const double v0 = __ldg(cv.a + ov) - coef * dv0;
+            const double v1 = __ldg(cv.a + ov + rv) - coef * dv1;
+            const double w1 = __ldg(cw.a + ow + sw) - coef * dw1;
+            double t = u1 - u0;
+            t = t + v1;
+            t = t - v0;
+            t = t + w1;
+            t = t - w0;
+            mx = fmax(mx, fabs(POW2 ? t * inv_h : t / h));
+            nu[ou] = hxm ? u0 : 0.0;
+            nv[ov] = hym ? v0 : 0.0;
+            nw[ow] = k == 0 ? 0.0 : w0;
+            if (!hxp) nu[ou + 1] = 0.0;
+            if (!hyp) nv[ov + rv] = 0.0;
+            if (!hzp) nw[ow + sw] = 0.0;
+            w0 = w1;
+            pc = pn;
+            pp += pl;
+            ou += su;
+            ov += sv;
+            ow += sw;
+        }
     }
     mx = block_max<kCellThreads>(mx, red);
     if (threadIdx.x == 0) partials[blockIdx.x] = mx;
@@ -372,6 +511,78 @@ __global__ void __launch_bounds__(kFaceThreads) diffuse_kernel(Vel3 in, double *
         s = s + zp;
         s = s - 6.0 * c;
         *dst = c + kdt * s;
+    }
+}
+
+// The same as a z-march (round 2; see divergence_march): blockIdx.y = component,
+// a thread owns an (i, j) column of faces over a chunk of planes and keeps the
+// component at k-1, k, k+1 in registers (five loads per face instead of
+// seven, no 64-bit division).  Bit-identical to diffuse_kernel.
+__global__ void __launch_bounds__(kFaceThreads) diffuse_march(Vel3 in, double *nu, double *nv, double *nw, SlabZ sz,
+                                                              double kdt, DiffBC bc, int nchunk)
+{
+    const int comp = blockIdx.y;
+    // (selected field by field: indexing the parameter array with blockIdx.y would copy it to local memory)
+    const Comp me{comp == 0 ? in.c[0].a : (comp == 1 ? in.c[1].a : in.c[2].a),
+                  sz.nx + (comp == 0), sz.ny + (comp == 1), sz.nz + (comp == 2),
+                  comp == 0 ? in.c[0].ld : (comp == 1 ? in.c[1].ld : in.c[2].ld), in.c[0].k_base};
+    double *out = comp == 0 ? nu : (comp == 1 ? nv : nw);
+    const int kend = comp == 2 ? sz.w_end() : sz.z1, nzl = kend - sz.z0;
+    const bool ns = bc.no_slip != 0;
+    const int nx = sz.nx, ny = sz.ny, nz = sz.nz;
+    const int tx = threadIdx.x % kDivTX, ty = threadIdx.x / kDivTX;
+    const int ntx = (nx + 1 + kDivTX - 1) / kDivTX;
+    int bid = blockIdx.x;
+    const int chunk = bid % nchunk;
+    bid /= nchunk;
+    const int i = (bid % ntx) * kDivTX + tx, j = (bid / ntx) * kDivTY + ty;
+    const int k0 = sz.z0 + (int)((long long)chunk * nzl / nchunk), k1 = sz.z0 + (int)((long long)(chunk + 1) * nzl / nchunk);
+    if (i >= me.na || j >= me.nb || k0 >= k1) return;
+    const bool colwall = (comp == 0 && (i == 0 || i == nx)) || (comp == 1 && (j == 0 || j == ny));
+    const unsigned sp = (unsigned)me.ld * (unsigned)me.nb, rw = (unsigned)me.ld;
+    unsigned o = me.off(i, j, k0);
+    const int last = me.nc - 1;  // last stored plane of this component
+    double cm = k0 > 0 ? __ldg(me.a + o - sp) : 0.0, c = __ldg(me.a + o);
+    for (int k = k0; k < k1; ++k, o += sp) {
+        const double cp = k < last ? __ldg(me.a + o + sp) : 0.0;
+        if (colwall || (comp == 2 && (k == 0 || k == nz))) {
+            out[o] = 0.0;
+        } else {
+            // neighbours along the component's own axis always exist (walls are 0)
+            double xm, xp, ym, yp, zm, zp;
+            if (comp == 0) {
+                xm = __ldg(me.a + o - 1);
+                xp = __ldg(me.a + o + 1);
+            } else {
+                xm = i > 0 ? __ldg(me.a + o - 1) : ghost(c, ns);
+                xp = i < nx - 1 ? __ldg(me.a + o + 1) : ghost(c, ns);
+            }
+            if (comp == 1) {
+                ym = __ldg(me.a + o - rw);
+                yp = __ldg(me.a + o + rw);
+            } else {
+                ym = j > 0 ? __ldg(me.a + o - rw) : ghost(c, ns);
+                if (j < ny - 1) yp = __ldg(me.a + o + rw);
+                else if (bc.lid_dirichlet) yp = comp == 0 ? 2.0 * bc.lid_u - c : -c;
+                else yp = ghost(c, ns);
+            }
+            if (comp == 2) {
+                zm = cm;
+                zp = cp;
+            } else {
+                zm = k > 0 ? cm : ghost(c, ns);
+                zp = k < nz - 1 ? cp : ghost(c, ns);
+            }
+            double s = xm + xp;
+            s = s + ym;
+            s = s + yp;
+            s = s + zm;
+            s = s + zp;
+            s = s - 6.0 * c;
+            out[o] = c + kdt * s;
+        }
+        cm = c;
+        c = cp;
     }
 }
 
@@ -551,6 +762,23 @@ static int divergence(const double *u, const double *v, const double *w, SlabZ s
     CF_REQUIRE(slab_ok(sz) && h > 0 && pitches_ok(sz, ldu, ldv, ldw), "divergence: bad slab/pitch");
     Vel3 in = make_vel(u, v, w, sz, ldu, ldv, ldw);
     cudaStream_t s = as_stream(stream);
+    const char *de = std::getenv("CF_DIVERGENCE");
+    const long long tiles = (long long)((sz.nx + kDivTX - 1) / kDivTX) * ((sz.ny + kDivTY - 1) / kDivTY);
+    const int nchunk = wave_chunks(tiles, sz.z1 - sz.z0, (long long)num_sms() * 8, 4);
+    if (!(de && !strcmp(de, "flat")) && tiles * nchunk <= kScratchPartials) {
+        const int grid = (int)(tiles * nchunk);
+        const bool p2 = is_pow2(h);
+        return reduce_max_to_host(
+            [&](double *part, unsigned int *tk, double *res) {
+                if (p2)
+                    divergence_march<true><<<grid, kCellThreads, 0, s>>>(in, sz, h, 1.0 / h, scale, scale != 1.0,
+                                                                          nchunk, out, part, tk, res);
+                else
+                    divergence_march<false><<<grid, kCellThreads, 0, s>>>(in, sz, h, 1.0 / h, scale, scale != 1.0,
+                                                                           nchunk, out, part, tk, res);
+            },
+            maxabs_host, s);
+    }
     int grid = grid_for((long long)sz.nx * sz.ny * (sz.z1 - sz.z0), kCellThreads, 8);
     return reduce_max_to_host(
         [&](double *part, unsigned int *tk, double *res) {
@@ -567,6 +795,23 @@ static int correct(const double *u, const double *v, const double *w, double *nu
     CF_REQUIRE(nu != u && nv != v && nw != w, "pressure_correct: output aliases input");
     Vel3 in = make_vel(u, v, w, sz, ldu, ldv, ldw);
     cudaStream_t s = as_stream(stream);
+    const char *ce = std::getenv("CF_CORRECT");
+    const long long tiles = (long long)((sz.nx + kDivTX - 1) / kDivTX) * ((sz.ny + kDivTY - 1) / kDivTY);
+    const int nchunk = wave_chunks(tiles, sz.z1 - sz.z0, (long long)num_sms() * 8, 4);
+    if (!(ce && !strcmp(ce, "flat")) && tiles * nchunk <= kScratchPartials) {
+        const int grid = (int)(tiles * nchunk);
+        const bool p2 = is_pow2(h);
+        return reduce_max_to_host(
+            [&](double *part, unsigned int *tk, double *res) {
+                if (p2)
+                    correct_march<true><<<grid, kCellThreads, 0, s>>>(in, nu, nv, nw, p, sz, h, 1.0 / h, coef, nchunk,
+                                                                       part, tk, res);
+                else
+                    correct_march<false><<<grid, kCellThreads, 0, s>>>(in, nu, nv, nw, p, sz, h, 1.0 / h, coef, nchunk,
+                                                                        part, tk, res);
+            },
+            div_post_host, s);
+    }
     int grid = grid_for((long long)sz.nx * sz.ny * (sz.z1 - sz.z0), kCellThreads, 8);
     return reduce_max_to_host(
         [&](double *part, unsigned int *tk, double *res) {
@@ -581,6 +826,17 @@ static int diffuse(const double *u, const double *v, const double *w, double *nu
     CF_REQUIRE(slab_ok(sz) && pitches_ok(sz, ldu, ldv, ldw), "diffuse: bad slab/pitch");
     CF_REQUIRE(nu != u && nv != v && nw != w, "diffuse: output aliases input");
     Vel3 in = make_vel(u, v, w, sz, ldu, ldv, ldw);
+    const char *fe = std::getenv("CF_DIFFUSE");
+    if (!(fe && !strcmp(fe, "flat"))) {
+        const long long tiles = (long long)((sz.nx + 1 + kDivTX - 1) / kDivTX) * ((sz.ny + 1 + kDivTY - 1) / kDivTY);
+        const int nchunk = wave_chunks(3 * tiles, sz.z1 - sz.z0 + 1, (long long)num_sms() * 8, 4);
+        if (tiles * nchunk < (1LL << 31)) {
+            dim3 grid((unsigned)(tiles * nchunk), 3);
+            diffuse_march<<<grid, kFaceThreads, 0, as_stream(stream)>>>(in, nu, nv, nw, sz, kdt, bc, nchunk);
+            CF_CHECK_LAUNCH("diffuse_march");
+            return CF_OK;
+        }
+    }
     long long faces = (long long)(sz.nx + 1) * (sz.ny + 1) * (sz.z1 - sz.z0 + 1);
     dim3 grid(grid_for(faces, kFaceThreads, 8), 3);
     diffuse_kernel<<<grid, kFaceThreads, 0, as_stream(stream)>>>(in, nu, nv, nw, sz, kdt, bc);

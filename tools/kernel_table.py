@@ -33,9 +33,9 @@ def alg_bytes(name, n):
         (r"cg_x_fixup", 24 * N, "x, p read; x written (only after an odd count)"),
         (r"advect_kernel", 48 * F, "3 components read (gathers) and written"),
         (r"advect_tma_kernel", 48 * F, "3 components read (TMA boxes) and written"),
-        (r"diffuse_kernel", 48 * F, "3 components read and written"),
-        (r"divergence_kernel", 24 * F + 8 * N, "3 components read; b written"),
-        (r"correct_kernel", 48 * F + 8 * N, "3 components + p read; 3 components written"),
+        (r"diffuse_(kernel|march)", 48 * F, "3 components read and written"),
+        (r"divergence_(kernel|march)", 24 * F + 8 * N, "3 components read; b written"),
+        (r"correct_(kernel|march)", 48 * F + 8 * N, "3 components + p read; 3 components written"),
         (r"stencil_apply_pair", 16 * N, "x read; y written"),
         (r"csr_spmv_kernel", 12 * nnz + 4 * (N + 1) + 16 * N, "int32 CSR + x read; y written"),
         (r"sym_spmv_kernel", 24 * N + 24 * U + 8 * (N + 1), "diag, upper + transpose arrays, x read; y written"),
