@@ -85,6 +85,38 @@ def test_box_step_kernels_bitwise(cuda, shape):
         assert np.array_equal(a, b), c
 
 
+@pytest.mark.parametrize("shape", [(33, 10, 14), (32, 16, 8)])
+def test_box_step_kernels_flat_forms(cuda, monkeypatch, shape):
+    """The one-thread-per-cell forms of the divergence / correction / diffusion
+    kernels (CF_DIVERGENCE / CF_CORRECT / CF_DIFFUSE = flat) against the
+    z-marches that replaced them as the default: bit-identical outputs (both
+    are also pinned to the oracle by the tests around this one), with h a
+    power of two (32: the exact-multiplication branch) and not."""
+    from paper_2504_03697_b200 import sim
+    from paper_2504_03697_b200.sim import solve_diffusion
+
+    nx, ny, nz = shape
+    n = max(shape)
+    u, v, w = random_field(shape, 11)
+    p = np.random.default_rng(12).standard_normal(nx * ny * nz)
+    cfg = cuda.SimConfig(n=n, h=1.0 / n, dt=0.01, t_end=0.0, viscosity=0.05 * (24.0 / n) ** 2 / 4,
+                         lid_velocity=1.0, no_slip=True, shape=shape)
+    out = []
+    for form in ("flat", None):
+        for k in ("CF_DIVERGENCE", "CF_CORRECT", "CF_DIFFUSE"):
+            if form:
+                monkeypatch.setenv(k, form)
+            else:
+                monkeypatch.delenv(k, raising=False)
+        st = cuda.SimState(vel=cuda.VelocityField(cfg.spec, u, v, w), p=cuda.ScalarField(cfg.spec, p))
+        div = cuda.divergence(st.vel).numpy()
+        dif = solve_diffusion(st, cfg).numpy()
+        div_post = sim.apply_pressure_correction(st, st.p, cfg)
+        out.append((div, flat(*dif), div_post, flat(*st.vel.numpy())))
+    for a, b in zip(*out):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
 @pytest.mark.parametrize("shape", [(16, 12, 20), (48, 20, 24)])
 def test_box_diffusion_bitwise(cuda, shape):
     from paper_2504_03697_b200.sim import solve_diffusion
