@@ -41,7 +41,7 @@ struct DicSkew {
     int ntx = 0, nty = 0, nz = 0;        // tiles in x / y, planes
     int nrows = 0;                       // steps per tile (padded to whole blocks)
     int trows = 0;                       // rows per tile of the skewed arrays (nrows + padding on both sides)
-    int grid = 0;                        // CTAs launched (one warp each, tickets -> tiles)
+    int grid = 0;                        // CTAs launched (tickets -> tiles)
     double *buf = nullptr;               // the allocation behind dy and wsk
     double *dy = nullptr;                // (d~, its refined reciprocal) pairs: [tile][row][lane]
     double *wsk = nullptr;               // w: [tile][row][lane]
