@@ -369,9 +369,11 @@ __global__ void __launch_bounds__(kCellThreads) correct_kernel(Vel3 in, double *
 // upper w face (which is the next cell's lower one: the same operands and
 // operations) in registers -- 10 loads per cell instead of 13, no integer
 // division, "/ h" as an exact multiplication for a power-of-two h.
-// Bit-identical to correct_kernel.
+// Bit-identical to correct_kernel.  Six CTAs per SM (40 registers, a few
+// spilled words) measured best: 186 us per 256^3 call against 211 / 221 / 272
+// at five / four (no cap) / eight.
 template <bool POW2>
-__global__ void __launch_bounds__(kCellThreads) correct_march(Vel3 in, double *nu, double *nv, double *nw,
+__global__ void __launch_bounds__(kCellThreads, 6) correct_march(Vel3 in, double *nu, double *nv, double *nw,
                                                               const double *__restrict__ p, SlabZ sz, double h,
                                                               double inv_h, double coef, int nchunk, double *partials,
                                                               unsigned int *ticket, double *result)
